@@ -1,0 +1,205 @@
+/* spdistal_b200.h -- C-ABI of the B200-native SpDISTAL leaf/partition backend.
+ *
+ * This is the drop-in boundary under the reference's runtime
+ * (dspar, /root/reference/proj/core).  The reference's hot path is
+ *
+ *   Plan plan(const ScheduledStatement&, const TensorSet&)         planner.hpp:42
+ *   ExecResult execute(const Plan&, const TensorSet&, const MachineGrid&,
+ *                      const Residency&, ExecMode)                  sim.hpp:121-122
+ *
+ * and the level-function "plugin" interface of the format abstraction
+ * (LevelPartitioner, partition_from_parent/child, level_partition.hpp:23-85).
+ * The entry points below replace, one for one, the pieces of that path that
+ * move to the GPU: tensor storage (tensor.hpp:54-114), the universe / nonzero
+ * level partitions (level_partition.cpp:134-212, deppart.cpp:15-53,
+ * planner.cpp:10-69), the six leaf kernels executed by LeafRun
+ * (sim.cpp:258-494), the deterministic reduce_combine (sim.cpp:791-811) and the
+ * two-phase output assembly (sim.cpp:647-789).  INTEGRATION.md shows the
+ * ExecMode::Gpu adapter a maintainer adds to sim.cpp to call them.
+ *
+ * Conventions
+ *  - Plain C types only: int64_t coordinates/positions, double values, opaque
+ *    handles.  No torch or CUDA types appear in a signature (streams are
+ *    passed as void*).
+ *  - Every function returns an int status mirroring the reference's error
+ *    classes and the CLI's exit-code mapping (cli.cpp:297-319):
+ *      SPD_OK (0); SPD_ERR_RUNTIME (1) = std::runtime_error / logic_error /
+ *      ClosureViolation; SPD_ERR_VALIDATION (2) = ValidationError /
+ *      ParseError / std::invalid_argument.  spd_last_error() returns the
+ *      thread-local message of the last failure.
+ *  - Device storage format: a compressed level is an int64 row pointer
+ *    (parent positions + 1 entries), lossless versus the reference's inclusive
+ *    (lo,hi) pos pairs because pos tiles [0,nnz) with canonical empties
+ *    (tensor.cpp:258-281); crd int64; vals fp64.  Dense levels store nothing
+ *    but their extents (dom), as in the reference.
+ *  - Asynchrony: calls are enqueued on the context's stream; functions that
+ *    return host data synchronise that stream.  Nothing falls back to the CPU:
+ *    without a CUDA device every compute entry point fails with SPD_ERR_RUNTIME.
+ */
+#ifndef SPDISTAL_B200_H
+#define SPDISTAL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPD_OK 0
+#define SPD_ERR_RUNTIME 1
+#define SPD_ERR_VALIDATION 2
+
+#define SPD_DENSE 0      /* LevelKind::Dense,      tensor.hpp:13 */
+#define SPD_COMPRESSED 1 /* LevelKind::Compressed, tensor.hpp:13 */
+
+typedef struct spd_context spd_context;
+typedef struct spd_tensor spd_tensor;
+
+/* CoordRange (index_space.hpp:12-23): inclusive [lo, hi], empty iff lo > hi. */
+typedef struct spd_range {
+  int64_t lo, hi;
+} spd_range;
+
+/* One colour of one distributed loop (PlanLoop, plan.hpp:49-62) in compact
+ * range form -- what the reference materialises as index sets (Partition,
+ * partition.hpp:16-46) is, for the contiguous partitions of these schedules,
+ * fully described by these spans:
+ *   color:  PlanLoop::color_bounds[c] (coordinates for a universe split,
+ *           positions for a nonzero split)
+ *   q:      leaf-level crd/vals positions owned (image of the rows /
+ *           the nonzero entry itself)
+ *   par:    span of the split level's pos partition: the parent entries whose
+ *           range meets q (preimage colours only the non-empty ones,
+ *           deppart.cpp:46)
+ *   top:    top-level coordinate bounds: the universe entry, or
+ *           project_to_universe's [min,max] (planner.cpp:50-69) for a nonzero
+ *           split -- the bounds other tensors (the output) are partitioned by. */
+typedef struct spd_color {
+  spd_range color, q, par, top;
+} spd_color;
+
+/* Stats (sim.hpp:25-36) of one execute. */
+typedef struct spd_stats {
+  int64_t workers;
+  int64_t combines; /* extra contributions summed by reduce_combine */
+  double imbalance; /* max work * workers / total work; 1 when no work */
+  double kernel_ms; /* device time of the leaf + combine launches (CUDA events) */
+  int64_t launches; /* kernels launched by this call */
+} spd_stats;
+
+/* ---- errors ----------------------------------------------------------- */
+const char* spd_last_error(void);
+/* Semantic version of this ABI (major*10000 + minor*100 + patch). */
+int spd_abi_version(void);
+
+/* ---- (1) context: one per GPU (one process per GPU) -------------------- */
+/* device: CUDA ordinal.  stream: a cudaStream_t to enqueue on, or NULL for a
+ * context-owned non-blocking stream. */
+int spd_context_create(int device, void* stream, spd_context** out);
+int spd_context_destroy(spd_context* ctx);
+int spd_context_synchronize(spd_context* ctx);
+/* Multi-GPU: rank/world of this context inside one NCCL communicator over
+ * NVLink.  `unique_id` is the 128-byte ncclUniqueId created by rank 0
+ * (spd_nccl_unique_id) and broadcast by the host's launcher. */
+int spd_nccl_unique_id(void* out128);
+int spd_context_init_comm(spd_context* ctx, const void* unique_id128, int rank, int world);
+int spd_context_rank(const spd_context* ctx, int* rank, int* world);
+
+/* ---- (2) tensors: the coordinate-tree encoding (tensor.hpp:54-114) ------ */
+/* Upload from the reference's own host storage, SparseTensor::from_parts
+ * (tensor.cpp:184-197): per stored level, dense levels pass NULL; compressed
+ * levels pass inclusive (lo,hi) pos pairs (2*npos int64) and crd.  Stored
+ * levels follow the format's level grouping (consecutive dense modes collapse,
+ * tensor.cpp:30-41).  kinds/mode_order describe the FormatSpec (one entry per
+ * mode).  The pairs are staged with cudaMemcpyAsync, converted to row
+ * pointers and checked against SparseTensor::validate (tensor.cpp:241-286) on
+ * the GPU; a violated invariant returns SPD_ERR_VALIDATION. */
+int spd_tensor_upload(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
+                      const int* mode_order, const int64_t* const* pos_pairs,
+                      const int64_t* const* crd, const double* vals, spd_tensor** out);
+/* Same, with host row pointers (device format) instead of pos pairs. */
+int spd_tensor_upload_rowptr(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
+                             const int* mode_order, const int64_t* const* rowptr,
+                             const int64_t* const* crd, const double* vals, int validate,
+                             spd_tensor** out);
+/* Zero-copy wrap of device-resident arrays in device format (the caller keeps
+ * ownership and must keep them alive; for device-resident pipelines). */
+int spd_tensor_wrap_device(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
+                           const int* mode_order, int64_t* const* rowptr_dev,
+                           int64_t* const* crd_dev, double* vals_dev, spd_tensor** out);
+int spd_tensor_destroy(spd_tensor* t);
+/* Geometry: stored levels, per level kind / parent positions / positions
+ * (level_positions, tensor.hpp:80-82) and the leaf (vals) count. */
+int spd_tensor_num_levels(const spd_tensor* t, int* nlevels);
+int spd_tensor_level(const spd_tensor* t, int level, int* kind, int64_t* parent_positions,
+                     int64_t* positions);
+int spd_tensor_nvals(const spd_tensor* t, int64_t* nvals);
+/* Device pointers of a level / of vals (NULL where the level stores nothing). */
+int spd_tensor_device_ptrs(const spd_tensor* t, int level, int64_t** rowptr, int64_t** crd);
+int spd_tensor_vals_ptr(const spd_tensor* t, double** vals);
+/* Download (synchronises): pos as (lo,hi) pairs, or row pointers. */
+int spd_tensor_download_level(const spd_tensor* t, int level, int64_t* pos_pairs, int64_t* crd);
+int spd_tensor_download_rowptr(const spd_tensor* t, int level, int64_t* rowptr);
+int spd_tensor_download_vals(const spd_tensor* t, double* vals);
+int spd_tensor_download_vals_range(const spd_tensor* t, int64_t first, int64_t count, double* vals);
+
+/* ---- (3) partitioning: level functions on the GPU ---------------------- */
+/* Universe partition of the top Dense level by divide_bounds(dim, pieces)
+ * (planner.cpp:10-20, level_partition.cpp:142-181) derived down the tree by
+ * partition_from_parent (copy + image, :214-232).  `colors_out` (host, pieces
+ * entries) may be NULL when only the device copy is wanted. */
+int spd_partition_universe(spd_context* ctx, const spd_tensor* t, int64_t pieces,
+                           spd_color* colors_out);
+/* Nonzero partition of compressed level `level` (entries divide_bounds(nnz,
+ * pieces), level_partition.cpp:186-211), preimages up the tree
+ * (partition_from_child :234-251, deppart.cpp:33-53) and projected top bounds
+ * (planner.cpp:50-69).  The owner searches run warp-parallel on the GPU. */
+int spd_partition_nonzero(spd_context* ctx, const spd_tensor* t, int level, int64_t pieces,
+                          spd_color* colors_out);
+/* Test support (K2m): materialise colour `color`'s subset of a bundle region
+ * exactly as the reference's Partition holds it (sorted unique indices).
+ *   which: 0 dom, 1 pos, 2 crd of `level`; 3 vals.
+ * Uses the colours of the last spd_partition_* call on this context.  Writes
+ * up to `cap` indices and returns the count in *count. */
+int spd_partition_materialize(spd_context* ctx, const spd_tensor* t, int level, int which,
+                              int64_t color, int64_t* out, int64_t cap, int64_t* count);
+
+/* ---- (4) leaf kernels + combine (one execute of a plan) ---------------- */
+/* Every op runs the colours [first_color, first_color + ncolors) of the last
+ * spd_partition_* on this context on this GPU, combines overlapping partials
+ * deterministically in ascending colour order (reduce_combine,
+ * sim.cpp:791-811) and writes the output.  With a communicator and
+ * ncolors == 1 per rank, boundary partials are exchanged with NCCL.
+ * Dense outputs are row-major device arrays; untouched entries are 0.0
+ * (assemble_output's all-dense path, sim.cpp:665-674).  `stats` may be NULL. */
+int spd_spmv(spd_context* ctx, const spd_tensor* B, const double* c_dev, double* a_dev,
+             int64_t first_color, int64_t ncolors, spd_stats* stats);
+/* A(i,j) = B(i,k) * C(k,j), C dense K x N row-major (format dd). */
+int spd_spmm(spd_context* ctx, const spd_tensor* B, const double* C_dev, int64_t N,
+             double* A_dev, int64_t first_color, int64_t ncolors, spd_stats* stats);
+/* A(i,j) = B(i,j) * C(i,k) * D(k,j): output vals on B's pattern (pattern
+ * reuse, sim.cpp:571-606).  D(k,j) is read at D[k*dk + j*dj]. */
+int spd_sddmm(spd_context* ctx, const spd_tensor* B, const double* C_dev, const double* D_dev,
+              int64_t K, int64_t dk, int64_t dj, double* Avals_dev, int64_t first_color,
+              int64_t ncolors, spd_stats* stats);
+/* A(i,j) = B(i,j,k) * c(k) on a dss CSF; output vals on B's first two levels. */
+int spd_spttv(spd_context* ctx, const spd_tensor* B, const double* c_dev, double* Avals_dev,
+              int64_t first_color, int64_t ncolors, spd_stats* stats);
+/* A(i,l) = B(i,j,k) * C(j,l) * D(k,l) on a dss CSF; C: J x R, D: K x R, A: I x R. */
+int spd_spmttkrp(spd_context* ctx, const spd_tensor* B, const double* C_dev,
+                 const double* D_dev, int64_t R, double* A_dev, int64_t first_color,
+                 int64_t ncolors, spd_stats* stats);
+/* A = B + C + D over CSR operands with identical dims, row split: two-phase
+ * assembly (count -> scan -> fill, sim.cpp:676-788) producing a new CSR
+ * tensor with the structural-union pattern. */
+int spd_spadd3(spd_context* ctx, const spd_tensor* B, const spd_tensor* C, const spd_tensor* D,
+               spd_tensor** A_out, int64_t first_color, int64_t ncolors, spd_stats* stats);
+
+/* Per-colour Stats::PerWorker::work of the last op (sim.cpp:352), `pieces`
+ * entries. */
+int spd_last_work(spd_context* ctx, int64_t* work, int64_t pieces);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,200 @@
+// Internal definitions shared by the sm_100a translation units of
+// libspdistal_b200.so.  Nothing here is part of the C-ABI (include/spdistal_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "spdistal_b200.h"
+
+namespace spd {
+
+// Error classes of the reference (errors.hpp:11-40) mapped onto ABI codes.
+struct ValidationError : std::runtime_error {
+  explicit ValidationError(const std::string& m) : std::runtime_error(m) {}
+};
+struct RuntimeError : std::runtime_error {
+  explicit RuntimeError(const std::string& m) : std::runtime_error(m) {}
+};
+
+void set_last_error(const std::string& msg);
+
+#define SPD_CUDA(call)                                                                   \
+  do {                                                                                   \
+    cudaError_t spd_e_ = (call);                                                         \
+    if (spd_e_ != cudaSuccess)                                                           \
+      throw ::spd::RuntimeError(std::string("CUDA error ") + cudaGetErrorString(spd_e_) + \
+                                " at " __FILE__ ":" + std::to_string(__LINE__));         \
+  } while (0)
+#define SPD_NCCL(call)                                                                   \
+  do {                                                                                   \
+    ncclResult_t spd_r_ = (call);                                                        \
+    if (spd_r_ != ncclSuccess)                                                           \
+      throw ::spd::RuntimeError(std::string("NCCL error ") + ncclGetErrorString(spd_r_) + \
+                                " at " __FILE__ ":" + std::to_string(__LINE__));         \
+  } while (0)
+#define SPD_CHECK_LAUNCH() SPD_CUDA(cudaGetLastError())
+
+// Runs `f` and maps exceptions onto the ABI status codes.
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return SPD_OK;
+  } catch (const ValidationError& e) {
+    set_last_error(e.what());
+    return SPD_ERR_VALIDATION;
+  } catch (const std::invalid_argument& e) {
+    set_last_error(e.what());
+    return SPD_ERR_VALIDATION;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return SPD_ERR_RUNTIME;
+  }
+}
+
+// Grow-only device scratch buffer.
+struct DeviceBuffer {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  void* reserve(size_t n) {
+    if (n > bytes) {
+      if (ptr) SPD_CUDA(cudaFree(ptr));
+      ptr = nullptr;
+      size_t want = n + n / 4;
+      SPD_CUDA(cudaMalloc(&ptr, want));
+      bytes = want;
+    }
+    return ptr;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+};
+
+// One colour as the kernels see it: the public spd_color plus the output
+// write range (the rows this colour must store, tiling [0, rows) across
+// colours in order).
+struct DevColor {
+  spd_color pub;
+  int64_t w_lo, w_hi;       // output rows written by this colour (op-specific)
+  int64_t chunk_begin;      // first virtual chunk of this colour (op-specific)
+  int64_t pad;
+};
+static_assert(sizeof(spd_color) == 64, "spd_color layout");
+
+enum class SplitKind { None = 0, Universe = 1, NonZero = 2 };
+
+}  // namespace spd
+
+struct spd_level_store {
+  int kind = SPD_DENSE;
+  std::vector<int64_t> dom;   // dense: extents of the collapsed modes
+  int64_t parent_positions = 1;
+  int64_t positions = 0;      // level_positions
+  int64_t* rowptr = nullptr;  // compressed: parent_positions + 1
+  int64_t* crd = nullptr;     // compressed: positions
+};
+
+struct spd_tensor {
+  spd_context* ctx = nullptr;
+  int order = 0;
+  std::vector<int64_t> dims;
+  std::vector<int> kinds, mode_order;
+  std::vector<std::vector<int>> groups;  // level grouping (tensor.cpp:30-41)
+  std::vector<spd_level_store> levels;
+  int64_t nvals = 0;
+  double* vals = nullptr;
+  bool owns = true;
+  // Derived device index for 3-level trees: rows -> leaf positions
+  // (rp2[rp1[i]]), built on first use by SpMTTKRP.
+  int64_t* leaf_rowptr = nullptr;
+};
+
+struct spd_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+  // Last partition (spd_partition_*): device + host copies of the colours.
+  spd::SplitKind split = spd::SplitKind::None;
+  const spd_tensor* split_tensor = nullptr;
+  int split_level = 0;
+  int64_t pieces = 0;
+  spd::DeviceBuffer colors_dev;      // spd::DevColor[pieces]
+  std::vector<spd_color> colors_host;
+  bool colors_host_valid = false;
+
+  std::vector<int64_t> last_work;    // per colour
+  spd::DeviceBuffer scratch[6];
+  spd::DeviceBuffer counters;        // small int64 device counters
+  int64_t* pinned_counters = nullptr;
+};
+
+namespace spd {
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// First index i in [0, n) with a[i] > key (n if none): a 32-ary search in
+// which every round issues one coalescable load per lane -- 5 dependent
+// rounds for 16.7M rows instead of 24 for a scalar binary search.  Must be
+// called by a full, converged warp; returns the same value on every lane.
+__device__ __forceinline__ int64_t warp_upper_bound(const int64_t* __restrict__ a, int64_t n,
+                                                    int64_t key) {
+  const int lane = lane_id();
+  int64_t lo = 0, hi = n;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    int64_t step = (hi - lo + 31) / 32;
+    int64_t idx = lo + lane * step;
+    bool pred = idx < hi && __ldg(a + idx) <= key;
+    unsigned m = __ballot_sync(0xffffffffu, pred);
+    int cnt = __popc(m);
+    if (cnt == 0) return lo;
+    int64_t nlo = lo + (int64_t)(cnt - 1) * step + 1;
+    int64_t nhi = lo + (int64_t)cnt * step;
+    hi = nhi < hi ? nhi : hi;
+    lo = nlo;
+  }
+  int64_t idx = lo + lane;
+  bool pred = idx < hi && __ldg(a + idx) <= key;
+  unsigned m = __ballot_sync(0xffffffffu, pred);
+  return lo + __popc(m);
+}
+
+// Parent entry whose range contains position q (tensor.cpp:221-235):
+// the last p with rowptr[p] <= q, over rowptr[0..npos].
+__device__ __forceinline__ int64_t warp_owner(const int64_t* __restrict__ rowptr, int64_t npos,
+                                              int64_t q) {
+  return warp_upper_bound(rowptr, npos + 1, q) - 1;
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Host-side helpers implemented in context.cu.
+spd_context* checked(spd_context* ctx);
+void activate(spd_context* ctx);
+const std::vector<spd_color>& host_colors(spd_context* ctx);  // syncs if needed
+void require_partition(spd_context* ctx, const spd_tensor* t, int64_t first, int64_t count);
+void fill_stats(spd_context* ctx, spd_stats* st, int64_t combines, const std::vector<int64_t>& work,
+                int64_t launches, bool timed);
+
+}  // namespace spd

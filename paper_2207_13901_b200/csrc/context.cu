@@ -1,0 +1,576 @@
+// Context, NCCL communicator, and device-resident tensor storage (K0).
+//
+// Storage follows the reference's coordinate-tree encoding
+// (SparseTensor, /root/reference/proj/core/include/dspar/tensor.hpp:54-114):
+// levels grouped like level_grouping (tensor.cpp:30-41), a compressed level
+// kept as an int64 row pointer (lossless versus the reference's inclusive
+// (lo,hi) pos pairs, tensor.cpp:258-281), crd int64 and vals fp64, all in HBM.
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace spd {
+
+static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+
+spd_context* checked(spd_context* ctx) {
+  if (!ctx) throw ValidationError("null spd_context");
+  return ctx;
+}
+
+void activate(spd_context* ctx) { SPD_CUDA(cudaSetDevice(ctx->device)); }
+
+// ---------------------------------------------------------------------------
+// K0: pos pairs -> row pointer, with SparseTensor::validate's compressed-level
+// checks (tensor.cpp:258-281) evaluated element-parallel:
+//   every range is canonical-empty or non-empty, and starts where the previous
+//   one ended: lo_p == hi_{p-1} + 1 (lo_0 == 0); the last ends at nnz - 1.
+// Error bits: 1 tiling / canonical form, 2 crd order, 4 crd bounds.
+__global__ void k_pairs_to_rowptr(const int64_t* __restrict__ pairs, int64_t npos, int64_t nnz,
+                                  int64_t* __restrict__ rowptr, int* __restrict__ err) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; p < npos; p += stride) {
+    int64_t lo = pairs[2 * p], hi = pairs[2 * p + 1];
+    int64_t prev_end = p == 0 ? -1 : pairs[2 * p - 1];
+    bool ok = hi >= lo - 1 && lo == prev_end + 1;
+    if (p == npos - 1) ok = ok && hi + 1 == nnz;
+    if (!ok) atomicOr(err, 1);
+    rowptr[p] = lo;
+    if (p == npos - 1) rowptr[npos] = nnz;
+  }
+}
+
+__global__ void k_check_rowptr(const int64_t* __restrict__ rowptr, int64_t npos, int64_t nnz,
+                               int* __restrict__ err) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; p < npos; p += stride) {
+    bool ok = rowptr[p + 1] >= rowptr[p];
+    if (p == 0) ok = ok && rowptr[0] == 0;
+    if (p == npos - 1) ok = ok && rowptr[npos] == nnz;
+    if (!ok) atomicOr(err, 1);
+  }
+}
+
+// crd strictly increasing inside every range and within [0, dim): a position
+// q > 0 is compared with q-1 unless q starts a range.  Range starts are found
+// with a per-position owner test that needs no extra buffer: q starts a range
+// iff rowptr[owner(q)] == q, evaluated here by marking starts first.
+__global__ void k_mark_starts(const int64_t* __restrict__ rowptr, int64_t npos,
+                              unsigned char* __restrict__ start) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; p < npos; p += stride)
+    if (rowptr[p + 1] > rowptr[p]) start[rowptr[p]] = 1;
+}
+
+__global__ void k_check_crd(const int64_t* __restrict__ crd, int64_t nnz, int64_t dim,
+                            const unsigned char* __restrict__ start, int* __restrict__ err) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; q < nnz; q += stride) {
+    int64_t c = crd[q];
+    if (c < 0 || c >= dim) atomicOr(err, 4);
+    if (q > 0 && !start[q] && c <= crd[q - 1]) atomicOr(err, 2);
+  }
+}
+
+__global__ void k_rowptr_to_pairs(const int64_t* __restrict__ rowptr, int64_t npos,
+                                  int64_t* __restrict__ pairs) {
+  int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (; p < npos; p += stride) {
+    pairs[2 * p] = rowptr[p];
+    pairs[2 * p + 1] = rowptr[p + 1] - 1;
+  }
+}
+
+static int grid_for(spd_context* ctx, int64_t n, int block = 256) {
+  int64_t g = ceil_div(n, block);
+  int64_t cap = (int64_t)ctx->num_sms * 8;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+static void* dev_alloc(spd_context* ctx, size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0) bytes = 8;
+  SPD_CUDA(cudaMallocAsync(&p, bytes, ctx->stream));
+  return p;
+}
+
+static void dev_free(spd_context* ctx, void* p) {
+  if (p) cudaFreeAsync(p, ctx->stream);
+}
+
+// Builds the level skeleton from the FormatSpec (tensor.cpp:30-41, 81-92).
+static spd_tensor* make_skeleton(spd_context* ctx, int order, const int64_t* dims,
+                                 const int* kinds, const int* mode_order) {
+  if (order < 0) throw ValidationError("tensor order must be non-negative");
+  std::vector<bool> seen(order, false);
+  for (int k = 0; k < order; k++) {
+    int m = mode_order[k];
+    if (m < 0 || m >= order || seen[m]) throw ValidationError("format: mode order is not a permutation");
+    seen[m] = true;
+    if (kinds[k] != SPD_DENSE && kinds[k] != SPD_COMPRESSED)
+      throw ValidationError("format: unknown level kind");
+    if (dims[k] < 0) throw ValidationError("tensor: negative dimension");
+  }
+  auto* t = new spd_tensor();
+  t->ctx = ctx;
+  t->order = order;
+  t->dims.assign(dims, dims + order);
+  t->kinds.assign(kinds, kinds + order);
+  t->mode_order.assign(mode_order, mode_order + order);
+  for (int k = 0; k < order; k++) {
+    if (kinds[k] == SPD_DENSE && !t->groups.empty() && kinds[t->groups.back().back()] == SPD_DENSE)
+      t->groups.back().push_back(k);
+    else
+      t->groups.push_back({k});
+  }
+  t->levels.resize(t->groups.size());
+  return t;
+}
+
+struct LevelInput {
+  const int64_t* pos_pairs;  // or rowptr
+  const int64_t* crd;
+};
+
+// Uploads/validates all levels. `pairs`: pos given as (lo,hi) pairs.
+static spd_tensor* upload_impl(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
+                               const int* mode_order, const int64_t* const* pos,
+                               const int64_t* const* crd, const double* vals, bool pairs,
+                               bool validate) {
+  activate(ctx);
+  spd_tensor* t = make_skeleton(ctx, order, dims, kinds, mode_order);
+  int* err_d = nullptr;
+  int err_h = 0;
+  try {
+    SPD_CUDA(cudaMallocAsync((void**)&err_d, sizeof(int), ctx->stream));
+    SPD_CUDA(cudaMemsetAsync(err_d, 0, sizeof(int), ctx->stream));
+    int64_t parent = 1;
+    for (size_t l = 0; l < t->groups.size(); l++) {
+      spd_level_store& L = t->levels[l];
+      L.parent_positions = parent;
+      int k0 = t->groups[l][0];
+      if (kinds[k0] == SPD_DENSE) {
+        L.kind = SPD_DENSE;
+        int64_t total = 1;
+        for (int k : t->groups[l]) {
+          L.dom.push_back(dims[mode_order[k]]);
+          total *= dims[mode_order[k]];
+        }
+        parent *= total;
+        L.positions = parent;
+        continue;
+      }
+      L.kind = SPD_COMPRESSED;
+      if (!pos || !pos[l] || (!crd || (!crd[l] && parent > 0)))
+        throw ValidationError("compressed level " + std::to_string(l) + " needs pos and crd");
+      int64_t nnz;
+      if (pairs)
+        nnz = parent == 0 ? 0 : pos[l][2 * (parent - 1) + 1] + 1;
+      else
+        nnz = pos[l][parent];
+      if (nnz < 0) throw ValidationError("tensor: pos ranges must cover exactly [0, nnz)");
+      L.positions = nnz;
+      L.rowptr = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (parent + 1));
+      L.crd = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (nnz > 0 ? nnz : 1));
+      if (pairs) {
+        int64_t* tmp = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * 2 * (parent > 0 ? parent : 1));
+        if (parent > 0) {
+          SPD_CUDA(cudaMemcpyAsync(tmp, pos[l], sizeof(int64_t) * 2 * parent,
+                                   cudaMemcpyHostToDevice, ctx->stream));
+          k_pairs_to_rowptr<<<grid_for(ctx, parent), 256, 0, ctx->stream>>>(tmp, parent, nnz,
+                                                                            L.rowptr, err_d);
+          SPD_CHECK_LAUNCH();
+        } else {
+          SPD_CUDA(cudaMemsetAsync(L.rowptr, 0, sizeof(int64_t), ctx->stream));
+        }
+        dev_free(ctx, tmp);
+      } else {
+        SPD_CUDA(cudaMemcpyAsync(L.rowptr, pos[l], sizeof(int64_t) * (parent + 1),
+                                 cudaMemcpyHostToDevice, ctx->stream));
+        if (validate && parent > 0) {
+          k_check_rowptr<<<grid_for(ctx, parent), 256, 0, ctx->stream>>>(L.rowptr, parent, nnz,
+                                                                         err_d);
+          SPD_CHECK_LAUNCH();
+        }
+      }
+      if (nnz > 0)
+        SPD_CUDA(cudaMemcpyAsync(L.crd, crd[l], sizeof(int64_t) * nnz, cudaMemcpyHostToDevice,
+                                 ctx->stream));
+      if ((validate || pairs) && nnz > 0) {
+        unsigned char* start = (unsigned char*)dev_alloc(ctx, nnz);
+        SPD_CUDA(cudaMemsetAsync(start, 0, nnz, ctx->stream));
+        k_mark_starts<<<grid_for(ctx, parent), 256, 0, ctx->stream>>>(L.rowptr, parent, start);
+        SPD_CHECK_LAUNCH();
+        int64_t dim = dims[mode_order[k0]];
+        k_check_crd<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(L.crd, nnz, dim, start, err_d);
+        SPD_CHECK_LAUNCH();
+        dev_free(ctx, start);
+      }
+      parent = nnz;
+    }
+    t->nvals = parent;
+    t->vals = (double*)dev_alloc(ctx, sizeof(double) * (parent > 0 ? parent : 1));
+    if (parent > 0) {
+      if (!vals) throw ValidationError("tensor: vals length does not match leaf count");
+      SPD_CUDA(cudaMemcpyAsync(t->vals, vals, sizeof(double) * parent, cudaMemcpyHostToDevice,
+                               ctx->stream));
+    }
+    SPD_CUDA(cudaMemcpyAsync(&err_h, err_d, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    SPD_CUDA(cudaStreamSynchronize(ctx->stream));
+    dev_free(ctx, err_d);
+    err_d = nullptr;
+    if (err_h & 1) throw ValidationError("tensor: pos ranges must tile [0, nnz) with canonical empties");
+    if (err_h & 2) throw ValidationError("tensor: crd must be strictly increasing per range");
+    if (err_h & 4) throw ValidationError("tensor: crd value out of dimension bounds");
+  } catch (...) {
+    if (err_d) dev_free(ctx, err_d);
+    for (auto& L : t->levels) {
+      dev_free(ctx, L.rowptr);
+      dev_free(ctx, L.crd);
+    }
+    dev_free(ctx, t->vals);
+    delete t;
+    throw;
+  }
+  return t;
+}
+
+const std::vector<spd_color>& host_colors(spd_context* ctx) {
+  if (!ctx->colors_host_valid) {
+    ctx->colors_host.resize(ctx->pieces);
+    std::vector<DevColor> tmp(ctx->pieces);
+    if (ctx->pieces > 0) {
+      SPD_CUDA(cudaMemcpyAsync(tmp.data(), ctx->colors_dev.ptr, sizeof(DevColor) * ctx->pieces,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+      SPD_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
+    for (int64_t c = 0; c < ctx->pieces; c++) ctx->colors_host[c] = tmp[c].pub;
+    ctx->colors_host_valid = true;
+  }
+  return ctx->colors_host;
+}
+
+void require_partition(spd_context* ctx, const spd_tensor* t, int64_t first, int64_t count) {
+  if (ctx->split == SplitKind::None || ctx->split_tensor != t)
+    throw ValidationError("no partition of this tensor on the context: call spd_partition_* first");
+  if (first < 0 || count < 1 || first + count > ctx->pieces)
+    throw ValidationError("colour range outside the partition");
+  bool all = first == 0 && count == ctx->pieces;
+  bool one_per_rank = ctx->comm && count == 1 && ctx->pieces == ctx->world && first == ctx->rank;
+  if (!all && !one_per_rank)
+    throw ValidationError(
+        "a GPU runs either every colour of the partition, or (with a communicator) exactly the "
+        "colour equal to its rank with pieces == world");
+}
+
+void fill_stats(spd_context* ctx, spd_stats* st, int64_t combines, const std::vector<int64_t>& work,
+                int64_t launches, bool timed) {
+  ctx->last_work = work;
+  if (!st) return;
+  st->workers = (int64_t)work.size();
+  st->combines = combines;
+  int64_t total = 0, mx = 0;
+  for (int64_t w : work) total += w, mx = w > mx ? w : mx;
+  st->imbalance = total == 0 ? 1.0 : (double)mx * (double)work.size() / (double)total;
+  st->launches = launches;
+  st->kernel_ms = 0;
+  if (timed) {
+    float ms = 0;
+    SPD_CUDA(cudaEventSynchronize(ctx->ev1));
+    SPD_CUDA(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
+    st->kernel_ms = ms;
+  }
+}
+
+}  // namespace spd
+
+using namespace spd;
+
+extern "C" {
+
+const char* spd_last_error(void) { return g_last_error.c_str(); }
+int spd_abi_version(void) { return 100; }
+
+int spd_context_create(int device, void* stream, spd_context** out) {
+  return guarded([&] {
+    if (!out) throw ValidationError("null out pointer");
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0)
+      throw RuntimeError("no CUDA device available: the B200 backend has no CPU fallback");
+    if (device < 0 || device >= n) throw ValidationError("device ordinal out of range");
+    auto* ctx = new spd_context();
+    ctx->device = device;
+    SPD_CUDA(cudaSetDevice(device));
+    SPD_CUDA(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, device));
+    if (stream) {
+      ctx->stream = (cudaStream_t)stream;
+    } else {
+      SPD_CUDA(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+      ctx->own_stream = true;
+    }
+    // Keep freed blocks in the stream-ordered pool: per-step uploads reuse them.
+    cudaMemPool_t pool;
+    SPD_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t threshold = UINT64_MAX;
+    SPD_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    SPD_CUDA(cudaEventCreate(&ctx->ev0));
+    SPD_CUDA(cudaEventCreate(&ctx->ev1));
+    SPD_CUDA(cudaMallocHost((void**)&ctx->pinned_counters, sizeof(int64_t) * 64));
+    *out = ctx;
+  });
+}
+
+int spd_context_destroy(spd_context* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    ctx->colors_dev.release();
+    for (auto& b : ctx->scratch) b.release();
+    ctx->counters.release();
+    if (ctx->pinned_counters) cudaFreeHost(ctx->pinned_counters);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int spd_context_synchronize(spd_context* ctx) {
+  return guarded([&] {
+    checked(ctx);
+    activate(ctx);
+    SPD_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int spd_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    ncclUniqueId id;
+    SPD_NCCL(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int spd_context_init_comm(spd_context* ctx, const void* unique_id128, int rank, int world) {
+  return guarded([&] {
+    checked(ctx);
+    if (world < 1 || rank < 0 || rank >= world) throw ValidationError("bad rank/world");
+    activate(ctx);
+    ncclUniqueId id;
+    std::memcpy(&id, unique_id128, sizeof(id));
+    if (ctx->comm) SPD_NCCL(ncclCommDestroy(ctx->comm));
+    SPD_NCCL(ncclCommInitRank(&ctx->comm, world, id, rank));
+    ctx->rank = rank;
+    ctx->world = world;
+  });
+}
+
+int spd_context_rank(const spd_context* ctx, int* rank, int* world) {
+  return guarded([&] {
+    if (!ctx) throw ValidationError("null spd_context");
+    *rank = ctx->rank;
+    *world = ctx->world;
+  });
+}
+
+int spd_tensor_upload(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
+                      const int* mode_order, const int64_t* const* pos_pairs,
+                      const int64_t* const* crd, const double* vals, spd_tensor** out) {
+  return guarded([&] {
+    checked(ctx);
+    *out = upload_impl(ctx, order, dims, kinds, mode_order, pos_pairs, crd, vals, true, true);
+  });
+}
+
+int spd_tensor_upload_rowptr(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
+                             const int* mode_order, const int64_t* const* rowptr,
+                             const int64_t* const* crd, const double* vals, int validate,
+                             spd_tensor** out) {
+  return guarded([&] {
+    checked(ctx);
+    *out = upload_impl(ctx, order, dims, kinds, mode_order, rowptr, crd, vals, false,
+                       validate != 0);
+  });
+}
+
+int spd_tensor_wrap_device(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
+                           const int* mode_order, int64_t* const* rowptr_dev,
+                           int64_t* const* crd_dev, double* vals_dev, spd_tensor** out) {
+  return guarded([&] {
+    checked(ctx);
+    activate(ctx);
+    spd_tensor* t = make_skeleton(ctx, order, dims, kinds, mode_order);
+    t->owns = false;
+    int64_t parent = 1;
+    for (size_t l = 0; l < t->groups.size(); l++) {
+      spd_level_store& L = t->levels[l];
+      L.parent_positions = parent;
+      int k0 = t->groups[l][0];
+      if (kinds[k0] == SPD_DENSE) {
+        int64_t total = 1;
+        for (int k : t->groups[l]) L.dom.push_back(dims[mode_order[k]]), total *= dims[mode_order[k]];
+        parent *= total;
+        L.positions = parent;
+        continue;
+      }
+      L.kind = SPD_COMPRESSED;
+      L.rowptr = rowptr_dev[l];
+      L.crd = crd_dev[l];
+      int64_t nnz = 0;
+      SPD_CUDA(cudaMemcpyAsync(&nnz, L.rowptr + parent, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+      SPD_CUDA(cudaStreamSynchronize(ctx->stream));
+      L.positions = nnz;
+      parent = nnz;
+    }
+    t->nvals = parent;
+    t->vals = vals_dev;
+    *out = t;
+  });
+}
+
+int spd_tensor_destroy(spd_tensor* t) {
+  return guarded([&] {
+    if (!t) return;
+    spd_context* ctx = t->ctx;
+    activate(ctx);
+    if (ctx->split_tensor == t) {
+      ctx->split = SplitKind::None;
+      ctx->split_tensor = nullptr;
+    }
+    if (t->owns) {
+      for (auto& L : t->levels) {
+        dev_free(ctx, L.rowptr);
+        dev_free(ctx, L.crd);
+      }
+      dev_free(ctx, t->vals);
+    }
+    dev_free(ctx, t->leaf_rowptr);
+    delete t;
+  });
+}
+
+int spd_tensor_num_levels(const spd_tensor* t, int* nlevels) {
+  return guarded([&] {
+    if (!t) throw ValidationError("null tensor");
+    *nlevels = (int)t->levels.size();
+  });
+}
+
+int spd_tensor_level(const spd_tensor* t, int level, int* kind, int64_t* parent_positions,
+                     int64_t* positions) {
+  return guarded([&] {
+    if (!t || level < 0 || level >= (int)t->levels.size()) throw ValidationError("no such level");
+    const auto& L = t->levels[level];
+    *kind = L.kind;
+    *parent_positions = L.parent_positions;
+    *positions = L.positions;
+  });
+}
+
+int spd_tensor_nvals(const spd_tensor* t, int64_t* nvals) {
+  return guarded([&] {
+    if (!t) throw ValidationError("null tensor");
+    *nvals = t->nvals;
+  });
+}
+
+int spd_tensor_device_ptrs(const spd_tensor* t, int level, int64_t** rowptr, int64_t** crd) {
+  return guarded([&] {
+    if (!t || level < 0 || level >= (int)t->levels.size()) throw ValidationError("no such level");
+    *rowptr = t->levels[level].rowptr;
+    *crd = t->levels[level].crd;
+  });
+}
+
+int spd_tensor_vals_ptr(const spd_tensor* t, double** vals) {
+  return guarded([&] {
+    if (!t) throw ValidationError("null tensor");
+    *vals = t->vals;
+  });
+}
+
+int spd_tensor_download_level(const spd_tensor* t, int level, int64_t* pos_pairs, int64_t* crd) {
+  return guarded([&] {
+    if (!t || level < 0 || level >= (int)t->levels.size()) throw ValidationError("no such level");
+    const auto& L = t->levels[level];
+    if (L.kind != SPD_COMPRESSED) throw ValidationError("level is dense: nothing stored");
+    spd_context* ctx = t->ctx;
+    activate(ctx);
+    if (pos_pairs && L.parent_positions > 0) {
+      int64_t* tmp = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * 2 * L.parent_positions);
+      k_rowptr_to_pairs<<<grid_for(ctx, L.parent_positions), 256, 0, ctx->stream>>>(
+          L.rowptr, L.parent_positions, tmp);
+      SPD_CHECK_LAUNCH();
+      SPD_CUDA(cudaMemcpyAsync(pos_pairs, tmp, sizeof(int64_t) * 2 * L.parent_positions,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+      dev_free(ctx, tmp);
+    }
+    if (crd && L.positions > 0)
+      SPD_CUDA(cudaMemcpyAsync(crd, L.crd, sizeof(int64_t) * L.positions, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    SPD_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int spd_tensor_download_rowptr(const spd_tensor* t, int level, int64_t* rowptr) {
+  return guarded([&] {
+    if (!t || level < 0 || level >= (int)t->levels.size()) throw ValidationError("no such level");
+    const auto& L = t->levels[level];
+    if (L.kind != SPD_COMPRESSED) throw ValidationError("level is dense: nothing stored");
+    spd_context* ctx = t->ctx;
+    activate(ctx);
+    SPD_CUDA(cudaMemcpyAsync(rowptr, L.rowptr, sizeof(int64_t) * (L.parent_positions + 1),
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    SPD_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int spd_tensor_download_vals(const spd_tensor* t, double* vals) {
+  return guarded([&] {
+    if (!t) throw ValidationError("null tensor");
+    spd_context* ctx = t->ctx;
+    activate(ctx);
+    if (t->nvals > 0)
+      SPD_CUDA(cudaMemcpyAsync(vals, t->vals, sizeof(double) * t->nvals, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    SPD_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int spd_tensor_download_vals_range(const spd_tensor* t, int64_t first, int64_t count,
+                                   double* vals) {
+  return guarded([&] {
+    if (!t) throw ValidationError("null tensor");
+    if (first < 0 || count < 0 || first + count > t->nvals) throw ValidationError("range outside vals");
+    spd_context* ctx = t->ctx;
+    activate(ctx);
+    if (count > 0)
+      SPD_CUDA(cudaMemcpyAsync(vals, t->vals + first, sizeof(double) * count,
+                               cudaMemcpyDeviceToHost, ctx->stream));
+    SPD_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int spd_last_work(spd_context* ctx, int64_t* work, int64_t pieces) {
+  return guarded([&] {
+    checked(ctx);
+    if (pieces != (int64_t)ctx->last_work.size()) throw ValidationError("pieces mismatch");
+    for (int64_t c = 0; c < pieces; c++) work[c] = ctx->last_work[c];
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,780 @@
+// Row-reducing leaf kernels on sm_100a: SpMV (K3), SpMM (K4), SpTTV (K6),
+// SpMTTKRP (K7), plus the chunk fixup and the deterministic colour combine
+// (K9, reduce_combine sim.cpp:791-811).  See rowwalk.cuh for the execution
+// scheme and DESIGN.md for the rooflines.
+//
+// Leaf semantics follow the reference's LeafRun (sim.cpp:258-494) as rendered
+// by plan.cpp:158-365 (tests/golden/plan_spmv_row.txt:28-33,
+// plan_spmv_nonzero.txt:23-28): for every stored position of the colour the
+// product of the accessed values is added to the output entry, in position
+// order within a row; this backend reassociates that sum (FMA, chunk and
+// colour partials), which north_star allows within 1e-10 relative.
+#include <algorithm>
+
+#include "rowwalk.cuh"
+
+namespace spd {
+
+#define FULL 0xffffffffu
+
+// ---------------------------------------------------------------------------
+// Setup: output write ranges W_c and chunk starts for every colour, and the
+// chunk range of the colours this GPU runs.  One CTA; O(P).
+__global__ void k_setup(DevColor* __restrict__ cols, int64_t P, int split, int out_level,
+                        const int64_t* __restrict__ R, int64_t nrows, int64_t CH,
+                        int64_t c_first, int64_t c_count, int64_t* __restrict__ counters) {
+  const int lane = lane_id();
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int64_t c = warp; c < P; c += nw) {
+    const spd_color pc = cols[c].pub;
+    int64_t wl = 1, wh = 0;
+    if (split == (int)SplitKind::Universe) {
+      spd_range w = out_level == 0 ? pc.top : pc.par;
+      wl = w.lo, wh = w.hi;
+    } else if (pc.q.lo <= pc.q.hi) {
+      int64_t o = warp_owner(R, nrows, pc.q.lo);
+      wl = ld64(R + o) == pc.q.lo ? o : o + 1;  // first row starting inside the colour
+    }
+    if (lane == 0) cols[c].w_lo = wl, cols[c].w_hi = wh;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  if (split == (int)SplitKind::NonZero) {
+    int64_t next = nrows, first_ne = -1;
+    for (int64_t c = P - 1; c >= 0; c--) {
+      if (cols[c].pub.q.lo <= cols[c].pub.q.hi) {
+        cols[c].w_hi = next - 1;
+        next = cols[c].w_lo;
+        first_ne = c;
+      } else {
+        cols[c].w_lo = next;
+        cols[c].w_hi = next - 1;
+      }
+    }
+    if (first_ne >= 0) {
+      cols[first_ne].w_lo = 0;
+    } else {  // no positions at all: the last colour stores the zero rows
+      cols[P - 1].w_lo = 0;
+      cols[P - 1].w_hi = nrows - 1;
+    }
+  }
+  int64_t run = 0;
+  for (int64_t c = 0; c < P; c++) {
+    const DevColor& d = cols[c];
+    int64_t n = d.pub.q.lo <= d.pub.q.hi ? (d.pub.q.hi - d.pub.q.lo + CH) / CH
+                                           : (d.w_lo <= d.w_hi ? 1 : 0);
+    if (c == c_first) counters[1] = run;
+    cols[c].chunk_begin = run;
+    run += n;
+    if (c == c_first + c_count - 1) counters[2] = run;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SpMM / SpMTTKRP family: lane = output column, positions streamed serially
+// per warp with UNR independent 256-byte row gathers in flight.
+constexpr int kUnr = 8;
+
+template <int CPL>
+struct ColAcc {
+  double v[CPL];
+  __device__ __forceinline__ void zero() {
+#pragma unroll
+    for (int t = 0; t < CPL; t++) v[t] = 0.0;
+  }
+};
+
+template <int CPL>
+__device__ __forceinline__ void store_row(double* __restrict__ out, int64_t W, int64_t r,
+                                          const ColAcc<CPL>& a) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int t = 0; t < CPL; t++) {
+    int64_t col = lane + 32 * t;
+    if (col < W) out[r * W + col] = a.v[t];
+  }
+}
+
+template <int CPL>
+__device__ __forceinline__ void store_rec(double* __restrict__ val, int64_t slot, int64_t W,
+                                          const ColAcc<CPL>& a) {
+  store_row<CPL>(val, W, slot, a);
+}
+
+// Row-transition bookkeeping shared by the column kernels.
+struct ColState {
+  int64_t r, nb;       // current output row and its end (exclusive)
+  bool head;           // current row started before the chunk
+  int64_t head_row;    // head record row (-1 none)
+  int head_cont;
+};
+
+template <int CPL>
+__device__ __forceinline__ void col_row_end(const WalkGeom& g, ColState& st, ColAcc<CPL>& acc,
+                                            int64_t q, double* __restrict__ out,
+                                            const ChunkRecs& rec, int64_t k,
+                                            const ChunkInfo& ci) {
+  if (st.head) {
+    store_rec<CPL>(rec.val, 2 * k, g.W, acc);
+    st.head_row = st.r;
+    st.head_cont = 0;
+    st.head = false;
+  } else {
+    store_row<CPL>(out, g.W, st.r, acc);
+  }
+  acc.zero();
+  st.r = skip_empty_rows(g, st.r + 1, q, st.nb, out, ci.w_lo, ci.w_hi);
+}
+
+template <int CPL>
+__device__ __forceinline__ void col_chunk_end(const WalkGeom& g, ColState& st, ColAcc<CPL>& acc,
+                                              double* __restrict__ out, const ChunkRecs& rec,
+                                              int64_t k, const ChunkInfo& ci) {
+  int64_t tail_row = -1;
+  if (st.nb == ci.e + 1) {
+    if (st.head) {
+      store_rec<CPL>(rec.val, 2 * k, g.W, acc);
+      st.head_row = st.r;
+      st.head_cont = 0;
+    } else {
+      store_row<CPL>(out, g.W, st.r, acc);
+    }
+    int64_t nb;
+    if (st.r + 1 < g.nrows) skip_empty_rows(g, st.r + 1, ci.e + 1, nb, out, ci.w_lo, ci.w_hi);
+  } else if (st.head) {
+    store_rec<CPL>(rec.val, 2 * k, g.W, acc);
+    st.head_row = st.r;
+    st.head_cont = 1;
+  } else {
+    store_rec<CPL>(rec.val, 2 * k + 1, g.W, acc);
+    tail_row = st.r;
+  }
+  if (lane_id() == 0) {
+    rec.row[2 * k] = st.head_row;
+    rec.row[2 * k + 1] = tail_row;
+    rec.cont[k] = st.head_cont;
+  }
+}
+
+__device__ __forceinline__ void empty_chunk(const WalkGeom& g, const ChunkInfo& ci,
+                                            double* __restrict__ out, const ChunkRecs& rec) {
+  zero_rows(out, g.W, ci.w_lo, ci.w_hi);
+  if (lane_id() == 0) {
+    rec.row[2 * ci.local] = -1;
+    rec.row[2 * ci.local + 1] = -1;
+    rec.cont[ci.local] = 0;
+  }
+}
+
+// SpMM: A(i,j) = sum_k B(i,k) * C(k,j).  Row stride of C and A is W = N.
+template <int CPL>
+__global__ void __launch_bounds__(kBlock) k_spmm_walk(WalkGeom g, const int64_t* __restrict__ crd,
+                                                      const double* __restrict__ vals,
+                                                      const double* __restrict__ C,
+                                                      double* __restrict__ A, ChunkRecs rec,
+                                                      const int64_t* __restrict__ counters) {
+  const int lane = lane_id();
+  const int64_t begin = counters[1], end = counters[2];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t N = g.W;
+  for (int64_t v = begin + gw; v < end; v += nw) {
+    const ChunkInfo ci = chunk_info(g, v, begin);
+    if (ci.q_lo > ci.q_hi) {
+      empty_chunk(g, ci, A, rec);
+      continue;
+    }
+    const int64_t k = ci.local, s = ci.s, e = ci.e;
+    ColState st;
+    st.r = warp_owner(g.R, g.nrows, s);
+    st.nb = ld64(g.R + st.r + 1);
+    st.head = ld64(g.R + st.r) < s;
+    st.head_row = -1;
+    st.head_cont = 0;
+    if (s == ci.q_lo) zero_rows(A, N, ci.w_lo, st.r - 1);
+    ColAcc<CPL> acc;
+    acc.zero();
+    for (int64_t base = s; base <= e; base += 32) {
+      const int cnt = (int)min((int64_t)32, e - base + 1);
+      int64_t my_k = 0;
+      double my_v = 0.0;
+      if (lane < cnt) {
+        my_k = ld64(crd + base + lane);
+        my_v = __ldg(vals + base + lane);
+      }
+      for (int u0 = 0; u0 < cnt; u0 += kUnr) {
+        double cv[kUnr][CPL];
+#pragma unroll
+        for (int i = 0; i < kUnr; i++) {
+          const int64_t kk = __shfl_sync(FULL, my_k, (u0 + i) & 31);
+#pragma unroll
+          for (int t = 0; t < CPL; t++) {
+            const int64_t col = lane + 32 * t;
+            cv[i][t] = (u0 + i < cnt && col < N) ? __ldg(C + kk * N + col) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < kUnr; i++) {
+          if (u0 + i < cnt) {
+            const int64_t q = base + u0 + i;
+            if (q == st.nb) col_row_end<CPL>(g, st, acc, q, A, rec, k, ci);
+            const double bv = __shfl_sync(FULL, my_v, u0 + i);
+#pragma unroll
+            for (int t = 0; t < CPL; t++) acc.v[t] = fma(bv, cv[i][t], acc.v[t]);
+          }
+        }
+      }
+    }
+    col_chunk_end<CPL>(g, st, acc, A, rec, k, ci);
+  }
+}
+
+// SpMTTKRP over a dss CSF: A(i,l) = sum_{j,k} B(i,j,k) * C(j,l) * D(k,l).
+// Output rows are i; g.R is the derived leaf row pointer rp2[rp1[i]].  The
+// fibre (j) of each position is tracked alongside; W = R (rank).
+template <int CPL>
+__global__ void __launch_bounds__(kBlock) k_mttkrp_walk(
+    WalkGeom g, const int64_t* __restrict__ rp2, int64_t F, const int64_t* __restrict__ crd1,
+    const int64_t* __restrict__ crd2, const double* __restrict__ vals,
+    const double* __restrict__ C, const double* __restrict__ D, double* __restrict__ A,
+    ChunkRecs rec, const int64_t* __restrict__ counters) {
+  const int lane = lane_id();
+  const int64_t begin = counters[1], end = counters[2];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t Rk = g.W;
+  for (int64_t v = begin + gw; v < end; v += nw) {
+    const ChunkInfo ci = chunk_info(g, v, begin);
+    if (ci.q_lo > ci.q_hi) {
+      empty_chunk(g, ci, A, rec);
+      continue;
+    }
+    const int64_t k = ci.local, s = ci.s, e = ci.e;
+    ColState st;
+    st.r = warp_owner(g.R, g.nrows, s);
+    st.nb = ld64(g.R + st.r + 1);
+    st.head = ld64(g.R + st.r) < s;
+    st.head_row = -1;
+    st.head_cont = 0;
+    if (s == ci.q_lo) zero_rows(A, Rk, ci.w_lo, st.r - 1);
+    int64_t f = warp_owner(rp2, F, s);
+    int64_t fe = ld64(rp2 + f + 1);
+    double cj[CPL];
+    {
+      const int64_t j = ld64(crd1 + f);
+#pragma unroll
+      for (int t = 0; t < CPL; t++) {
+        const int64_t col = lane + 32 * t;
+        cj[t] = col < Rk ? __ldg(C + j * Rk + col) : 0.0;
+      }
+    }
+    ColAcc<CPL> acc;
+    acc.zero();
+    for (int64_t base = s; base <= e; base += 32) {
+      const int cnt = (int)min((int64_t)32, e - base + 1);
+      int64_t my_k = 0;
+      double my_v = 0.0;
+      if (lane < cnt) {
+        my_k = ld64(crd2 + base + lane);
+        my_v = __ldg(vals + base + lane);
+      }
+      for (int u0 = 0; u0 < cnt; u0 += kUnr) {
+        double dv[kUnr][CPL];
+#pragma unroll
+        for (int i = 0; i < kUnr; i++) {
+          const int64_t kk = __shfl_sync(FULL, my_k, (u0 + i) & 31);
+#pragma unroll
+          for (int t = 0; t < CPL; t++) {
+            const int64_t col = lane + 32 * t;
+            dv[i][t] = (u0 + i < cnt && col < Rk) ? __ldg(D + kk * Rk + col) : 0.0;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < kUnr; i++) {
+          if (u0 + i < cnt) {
+            const int64_t q = base + u0 + i;
+            if (q == st.nb) col_row_end<CPL>(g, st, acc, q, A, rec, k, ci);
+            if (q == fe) {
+              do {
+                f++;
+                fe = ld64(rp2 + f + 1);
+              } while (fe == q);
+              const int64_t j = ld64(crd1 + f);
+#pragma unroll
+              for (int t = 0; t < CPL; t++) {
+                const int64_t col = lane + 32 * t;
+                cj[t] = col < Rk ? __ldg(C + j * Rk + col) : 0.0;
+              }
+            }
+            const double bv = __shfl_sync(FULL, my_v, u0 + i);
+#pragma unroll
+            for (int t = 0; t < CPL; t++) acc.v[t] = fma(bv * cj[t], dv[i][t], acc.v[t]);
+          }
+        }
+      }
+    }
+    col_chunk_end<CPL>(g, st, acc, A, rec, k, ci);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SpMV / SpTTV family: lane = position.  Each warp streams its chunk in
+// windows of 32 positions with coalesced crd/vals loads; products are
+// reduced per row with a warp segmented scan (heads from the row pointer
+// window held one row per lane), so a window costs the same whether it holds
+// one row or 32.
+__device__ __forceinline__ void load_rows(const WalkGeom& g, int64_t rb, int64_t& S, int64_t& E) {
+  const int64_t rr = rb + lane_id();
+  if (rr < g.nrows) {
+    S = ld64(g.R + rr);
+    E = ld64(g.R + rr + 1);
+  } else {
+    S = INT64_MAX;
+    E = INT64_MAX;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock) k_spmv_walk(WalkGeom g, const int64_t* __restrict__ crd,
+                                                      const double* __restrict__ vals,
+                                                      const double* __restrict__ x,
+                                                      double* __restrict__ y, ChunkRecs rec,
+                                                      const int64_t* __restrict__ counters) {
+  const int lane = lane_id();
+  const int64_t begin = counters[1], end = counters[2];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = begin + gw; v < end; v += nw) {
+    const ChunkInfo ci = chunk_info(g, v, begin);
+    if (ci.q_lo > ci.q_hi) {
+      empty_chunk(g, ci, y, rec);
+      continue;
+    }
+    const int64_t k = ci.local, s = ci.s, e = ci.e;
+    const int64_t r0 = warp_owner(g.R, g.nrows, s);
+    bool has_cur, cur_head;
+    int64_t cur = r0, cur_end, rb;
+    double acc = 0.0;
+    if (ld64(g.R + r0) < s) {
+      has_cur = true, cur_head = true, cur_end = ld64(g.R + r0 + 1), rb = r0 + 1;
+    } else {
+      has_cur = false, cur_head = false, cur_end = 0, rb = r0;
+    }
+    if (s == ci.q_lo) zero_rows(y, 1, ci.w_lo, r0 - 1);
+    int64_t head_row = -1, tail_row = -1;
+    int head_cont = 0;
+    double head_val = 0.0, tail_val = 0.0;
+    int64_t S, E;
+    load_rows(g, rb, S, E);
+    for (int64_t base = s; base <= e;) {
+      const int64_t last = min(base + 31, e);
+      const int cnt = (int)(last - base + 1);
+      const int64_t q = base + lane;
+      double prod = 0.0;
+      if (lane < cnt) prod = __ldg(vals + q) * __ldg(x + ld64(crd + q));
+      if (has_cur && cur_end - 1 > last) {  // the whole window continues the current row
+        acc += warp_sum(prod);
+        base = last + 1;
+        continue;
+      }
+      // pass 1: heads of the non-empty rows starting in the window
+      unsigned heads = 0;
+      int ngroups = 1;
+      {
+        int64_t Sg = S, Eg = E, gb = rb;
+        for (;;) {
+          const bool hit = Eg > Sg && Sg <= last;
+          const unsigned bit = hit ? 1u << (int)(Sg - base) : 0u;
+          heads |= __reduce_or_sync(FULL, bit);
+          if (__shfl_sync(FULL, Sg, 31) > last) break;
+          gb += 32;
+          load_rows(g, gb, Sg, Eg);
+          ngroups++;
+        }
+      }
+      // segmented inclusive scan
+      double sv = prod;
+      unsigned f = (heads >> lane) & 1u;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const double tv = __shfl_up_sync(FULL, sv, off);
+        const unsigned tf = __shfl_up_sync(FULL, f, off);
+        if (lane >= off) {
+          if (!f) sv += tv;
+          f |= tf;
+        }
+      }
+      if (has_cur) {  // current row ends inside the window
+        const double tot = acc + __shfl_sync(FULL, sv, (int)(cur_end - 1 - base));
+        if (cur_head) {
+          head_row = cur, head_val = tot, head_cont = 0;
+        } else if (lane == 0) {
+          y[cur] = tot;
+        }
+        has_cur = false;
+        acc = 0.0;
+      }
+      // pass 2: rows starting in the window (and empty rows located in it)
+      int64_t Sg = S, Eg = E, gb = rb;
+      for (int gi = 0; gi < ngroups; gi++) {
+        if (gi > 0) {
+          gb += 32;
+          load_rows(g, gb, Sg, Eg);
+        }
+        const int64_t rr = gb + lane;
+        const bool valid = rr < g.nrows && Sg <= last;
+        const bool ne = Eg > Sg;
+        const int src = (valid && ne) ? (int)(min(Eg - 1, last) - base) : 0;
+        const double val = __shfl_sync(FULL, sv, src);
+        if (valid && rr >= ci.w_lo && rr <= ci.w_hi) {
+          if (!ne) y[rr] = 0.0;
+          else if (Eg - 1 <= last) y[rr] = val;
+        }
+        const unsigned cm = __ballot_sync(FULL, valid && ne && Eg - 1 > last);
+        if (cm) {
+          const int t = __ffs(cm) - 1;
+          has_cur = true;
+          cur_head = false;
+          cur = gb + t;
+          cur_end = __shfl_sync(FULL, Eg, t);
+          acc = __shfl_sync(FULL, sv, cnt - 1);
+        }
+        if (gi == ngroups - 1) rb = gb + __popc(__ballot_sync(FULL, valid));
+      }
+      load_rows(g, rb, S, E);
+      base = last + 1;
+    }
+    if (has_cur) {
+      if (cur_head) head_row = cur, head_val = acc, head_cont = 1;
+      else tail_row = cur, tail_val = acc;
+    } else if (rb < g.nrows) {
+      int64_t nb;
+      skip_empty_rows(g, rb, e + 1, nb, y, ci.w_lo, ci.w_hi);
+    }
+    if (lane == 0) {
+      rec.row[2 * k] = head_row;
+      rec.row[2 * k + 1] = tail_row;
+      rec.cont[k] = head_cont;
+      rec.val[2 * k] = head_val;
+      rec.val[2 * k + 1] = tail_val;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Chunk fixup: sums each cut row's records in chunk order.  Rows cut by the
+// end of a colour become colour tail records; the head chain at the start of
+// a colour becomes its packed head record.
+__device__ __forceinline__ int64_t chain_stop(const int* __restrict__ cont, int64_t from,
+                                              int64_t to) {
+  const int lane = lane_id();
+  for (int64_t b = from; b < to; b += 32) {
+    const int64_t k2 = b + lane;
+    const bool stop = k2 < to && cont[k2] == 0;
+    const unsigned m = __ballot_sync(FULL, stop);
+    if (m) return b + __ffs(m) - 1;
+  }
+  return to;
+}
+
+__global__ void __launch_bounds__(kBlock) k_chunk_fixup(WalkGeom g, ChunkRecs rec, ColorRecs col,
+                                                        double* __restrict__ out) {
+  const int lane = lane_id();
+  const int64_t begin = col.counters[1], end = col.counters[2];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t W = g.W;
+  for (int64_t v = begin + gw; v < end; v += nw) {
+    const int64_t c = colour_of_chunk(g, v);
+    const int64_t k = v - begin;
+    const int64_t cend =
+        (c + 1 < g.c_first + g.c_count ? g.cols[c + 1].chunk_begin : end) - begin;
+    const int64_t trow = rec.row[2 * k + 1];
+    if (trow >= 0) {
+      const int64_t stop = chain_stop(rec.cont, k + 1, cend);
+      const int64_t last = stop < cend ? stop : cend - 1;
+      for (int64_t j = lane; j < W; j += 32) {
+        double sum = rec.val[(2 * k + 1) * W + j];
+#pragma unroll 4
+        for (int64_t k2 = k + 1; k2 <= last; k2++) sum += rec.val[2 * k2 * W + j];
+        if (stop < cend) out[trow * W + j] = sum;
+        else col.tail_val[c * W + j] = sum;
+      }
+      if (stop >= cend && lane == 0) col.tail_row[c] = trow;
+    }
+    const int64_t hrow = rec.row[2 * k];
+    if (v == g.cols[c].chunk_begin && hrow >= 0) {
+      const int64_t stop = rec.cont[k] == 0 ? k : chain_stop(rec.cont, k + 1, cend);
+      const int64_t last = stop < cend ? stop : cend - 1;
+      int64_t* pack = col.head_pack + c * (W + 2);
+      for (int64_t j = lane; j < W; j += 32) {
+        double sum = 0.0;
+#pragma unroll 4
+        for (int64_t k2 = k; k2 <= last; k2++) sum += rec.val[2 * k2 * W + j];
+        reinterpret_cast<double*>(pack)[2 + j] = sum;
+      }
+      if (lane == 0) {
+        pack[0] = hrow;
+        pack[1] = stop < cend ? 0 : 1;
+      }
+    }
+  }
+}
+
+// K9: colour combine.  A row cut between colours is owned by the colour
+// where it starts (its tail record); the partials of the following colours
+// that continue it (their head records) are added in ascending colour order,
+// exactly the order of reduce_combine (sim.cpp:797-808).  Also counts
+// Stats::combines = W per extra contributing colour.
+__global__ void k_colour_combine(ColorRecs col, const DevColor* __restrict__ cols, int64_t P,
+                                 int64_t W, int64_t c_first, int64_t c_count,
+                                 double* __restrict__ out) {
+  const int lane = lane_id();
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (c >= P) return;
+  const int64_t* hp = col.head_pack + c * (W + 2);
+  if (hp[0] >= 0 && lane == 0) atomicAdd((unsigned long long*)&col.counters[0], (unsigned long long)W);
+  if (c < c_first || c >= c_first + c_count) return;
+  const int64_t r = col.tail_row[c];
+  if (r < 0) return;
+  for (int64_t j = lane; j < W; j += 32) {
+    double sum = col.tail_val[c * W + j];
+    for (int64_t c2 = c + 1; c2 < P; c2++) {
+      if (cols[c2].pub.q.lo > cols[c2].pub.q.hi) continue;  // colours without positions
+      const int64_t* h2 = col.head_pack + c2 * (W + 2);
+      if (h2[0] != r) break;
+      sum += reinterpret_cast<const double*>(h2)[2 + j];
+      if (!h2[1]) break;
+    }
+    out[r * W + j] = sum;
+  }
+}
+
+__global__ void k_leaf_rowptr(const int64_t* __restrict__ rp1, const int64_t* __restrict__ rp2,
+                              int64_t I, int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= I;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = rp2[rp1[i]];
+}
+
+// ---------------------------------------------------------------------------
+enum class Op { SpMV, SpMM, SpTTV, SpMTTKRP };
+
+struct OpArgs {
+  Op op;
+  const spd_tensor* B;
+  const double* x;  // c (SpMV, SpTTV) / C (SpMM, SpMTTKRP)
+  const double* D;  // SpMTTKRP
+  int64_t W;        // values per output row (1, N, R)
+  double* out;
+};
+
+template <class K>
+static int occupancy_grid(spd_context* ctx, K kernel) {
+  int per_sm = 0;
+  SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
+  if (per_sm < 1) per_sm = 1;
+  return ctx->num_sms * per_sm;
+}
+
+static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_t count,
+                        spd_stats* stats) {
+  checked(ctx);
+  const spd_tensor* B = a.B;
+  if (!B) throw ValidationError("null tensor");
+  require_partition(ctx, B, first, count);
+  activate(ctx);
+  const int nl = (int)B->levels.size();
+  const bool csf = a.op == Op::SpTTV || a.op == Op::SpMTTKRP;
+  if (csf) {
+    if (nl != 3 || B->levels[0].kind != SPD_DENSE || B->levels[1].kind != SPD_COMPRESSED ||
+        B->levels[2].kind != SPD_COMPRESSED || B->levels[0].dom.size() != 1)
+      throw ValidationError("unsupported on gpu: this kernel needs a dss (Dense, Compressed, Compressed) 3-tensor");
+  } else if (nl != 2 || B->levels[0].kind != SPD_DENSE || B->levels[1].kind != SPD_COMPRESSED ||
+             B->levels[0].dom.size() != 1) {
+    throw ValidationError("unsupported on gpu: this kernel needs a ds (CSR-like) matrix");
+  }
+  if (ctx->split == SplitKind::NonZero && ctx->split_level != nl - 1)
+    throw ValidationError("unsupported on gpu: nonzero split must be on the leaf level");
+  if (a.W < 0 || a.W > 128) throw ValidationError("unsupported on gpu: inner extent must be in [0, 128]");
+  const int64_t P = ctx->pieces;
+  const int64_t nnz = B->levels[nl - 1].positions;
+
+  WalkGeom g;
+  int out_level = 0;
+  switch (a.op) {
+    case Op::SpMV:
+    case Op::SpMM:
+      g.R = B->levels[1].rowptr;
+      g.nrows = B->levels[1].parent_positions;
+      break;
+    case Op::SpTTV:
+      g.R = B->levels[2].rowptr;
+      g.nrows = B->levels[2].parent_positions;
+      out_level = 1;
+      break;
+    case Op::SpMTTKRP: {
+      const int64_t I = B->levels[1].parent_positions;
+      spd_tensor* Bm = const_cast<spd_tensor*>(B);
+      if (!Bm->leaf_rowptr) {
+        SPD_CUDA(cudaMallocAsync((void**)&Bm->leaf_rowptr, sizeof(int64_t) * (I + 1), ctx->stream));
+        k_leaf_rowptr<<<(unsigned)std::min<int64_t>(ceil_div(I + 1, 256), 4096), 256, 0,
+                        ctx->stream>>>(B->levels[1].rowptr, B->levels[2].rowptr, I,
+                                       Bm->leaf_rowptr);
+        SPD_CHECK_LAUNCH();
+      }
+      g.R = B->leaf_rowptr;
+      g.nrows = I;
+      break;
+    }
+  }
+  g.cols = (const DevColor*)ctx->colors_dev.ptr;
+  g.c_first = first;
+  g.c_count = count;
+  g.W = a.W;
+  // Positions per chunk: ~256 KB of operand traffic per warp-chunk for the
+  // column kernels, 2048 positions for the scalar ones.
+  g.CH = (a.op == Op::SpMV || a.op == Op::SpTTV) ? 2048 : 1024;
+  const int64_t W = a.W > 0 ? a.W : 1;
+  const int64_t max_chunks = nnz / g.CH + 2 * P + 2;
+
+  ChunkRecs rec;
+  rec.row = (int64_t*)ctx->scratch[0].reserve(sizeof(int64_t) * 2 * max_chunks);
+  rec.cont = (int*)ctx->scratch[1].reserve(sizeof(int) * max_chunks);
+  rec.val = (double*)ctx->scratch[2].reserve(sizeof(double) * 2 * max_chunks * W);
+  ColorRecs col;
+  col.head_pack = (int64_t*)ctx->scratch[3].reserve(sizeof(int64_t) * P * (W + 2));
+  char* cr = (char*)ctx->scratch[4].reserve(sizeof(int64_t) * (P + 4) + sizeof(double) * P * W);
+  col.counters = (int64_t*)cr;
+  col.tail_row = col.counters + 4;
+  col.tail_val = (double*)(col.tail_row + P);
+
+  cudaStream_t s = ctx->stream;
+  int64_t launches = 0;
+  if (stats) SPD_CUDA(cudaEventRecord(ctx->ev0, s));
+  SPD_CUDA(cudaMemsetAsync(col.head_pack, 0xff, sizeof(int64_t) * P * (W + 2), s));
+  SPD_CUDA(cudaMemsetAsync(col.counters, 0, sizeof(int64_t) * 4, s));
+  SPD_CUDA(cudaMemsetAsync(col.tail_row, 0xff, sizeof(int64_t) * P, s));
+  k_setup<<<1, 1024, 0, s>>>((DevColor*)ctx->colors_dev.ptr, P, (int)ctx->split, out_level, g.R,
+                             g.nrows, g.CH, first, count, col.counters);
+  SPD_CHECK_LAUNCH();
+  launches++;
+
+  const spd_level_store& leaf = B->levels[nl - 1];
+  switch (a.op) {
+    case Op::SpMV:
+    case Op::SpTTV: {
+      static int grid = 0;
+      if (!grid) grid = occupancy_grid(ctx, k_spmv_walk);
+      k_spmv_walk<<<grid, kBlock, 0, s>>>(g, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      break;
+    }
+    case Op::SpMM: {
+      if (a.W <= 32) {
+        static int grid = 0;
+        if (!grid) grid = occupancy_grid(ctx, k_spmm_walk<1>);
+        k_spmm_walk<1><<<grid, kBlock, 0, s>>>(g, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      } else if (a.W <= 64) {
+        static int grid = 0;
+        if (!grid) grid = occupancy_grid(ctx, k_spmm_walk<2>);
+        k_spmm_walk<2><<<grid, kBlock, 0, s>>>(g, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      } else {
+        static int grid = 0;
+        if (!grid) grid = occupancy_grid(ctx, k_spmm_walk<4>);
+        k_spmm_walk<4><<<grid, kBlock, 0, s>>>(g, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      }
+      break;
+    }
+    case Op::SpMTTKRP: {
+      const spd_level_store& L1 = B->levels[1];
+      const spd_level_store& L2 = B->levels[2];
+      if (a.W <= 32) {
+        static int grid = 0;
+        if (!grid) grid = occupancy_grid(ctx, k_mttkrp_walk<1>);
+        k_mttkrp_walk<1><<<grid, kBlock, 0, s>>>(g, L2.rowptr, L2.parent_positions, L1.crd,
+                                                 L2.crd, B->vals, a.x, a.D, a.out, rec,
+                                                 col.counters);
+      } else if (a.W <= 64) {
+        static int grid = 0;
+        if (!grid) grid = occupancy_grid(ctx, k_mttkrp_walk<2>);
+        k_mttkrp_walk<2><<<grid, kBlock, 0, s>>>(g, L2.rowptr, L2.parent_positions, L1.crd,
+                                                 L2.crd, B->vals, a.x, a.D, a.out, rec,
+                                                 col.counters);
+      } else {
+        static int grid = 0;
+        if (!grid) grid = occupancy_grid(ctx, k_mttkrp_walk<4>);
+        k_mttkrp_walk<4><<<grid, kBlock, 0, s>>>(g, L2.rowptr, L2.parent_positions, L1.crd,
+                                                 L2.crd, B->vals, a.x, a.D, a.out, rec,
+                                                 col.counters);
+      }
+      break;
+    }
+  }
+  SPD_CHECK_LAUNCH();
+  launches++;
+  {
+    static int grid = 0;
+    if (!grid) grid = occupancy_grid(ctx, k_chunk_fixup);
+    k_chunk_fixup<<<grid, kBlock, 0, s>>>(g, rec, col, a.out);
+    SPD_CHECK_LAUNCH();
+    launches++;
+  }
+  if (ctx->comm && count == 1 && P > 1) {
+    const size_t bytes = sizeof(int64_t) * (W + 2);
+    SPD_NCCL(ncclAllGather(col.head_pack + first * (W + 2), col.head_pack, bytes, ncclUint8,
+                           ctx->comm, s));
+  }
+  k_colour_combine<<<(unsigned)ceil_div(P * 32, 256), 256, 0, s>>>(
+      col, (const DevColor*)ctx->colors_dev.ptr, P, W, first, count, a.out);
+  SPD_CHECK_LAUNCH();
+  launches++;
+  if (stats) {
+    SPD_CUDA(cudaEventRecord(ctx->ev1, s));
+    SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters, col.counters, sizeof(int64_t) * 4,
+                             cudaMemcpyDeviceToHost, s));
+    const auto& hc = host_colors(ctx);  // synchronises the stream
+    std::vector<int64_t> work(P);
+    const int64_t inner = a.op == Op::SpMV || a.op == Op::SpTTV ? 1 : a.W;
+    for (int64_t c = 0; c < P; c++)
+      work[c] = hc[c].q.lo <= hc[c].q.hi ? (hc[c].q.hi - hc[c].q.lo + 1) * inner : 0;
+    fill_stats(ctx, stats, ctx->pinned_counters[0], work, launches, true);
+  }
+}
+
+}  // namespace spd
+
+using namespace spd;
+
+extern "C" {
+
+int spd_spmv(spd_context* ctx, const spd_tensor* B, const double* c_dev, double* a_dev,
+             int64_t first_color, int64_t ncolors, spd_stats* stats) {
+  return guarded([&] {
+    run_rowwalk(ctx, OpArgs{Op::SpMV, B, c_dev, nullptr, 1, a_dev}, first_color, ncolors, stats);
+  });
+}
+
+int spd_spmm(spd_context* ctx, const spd_tensor* B, const double* C_dev, int64_t N,
+             double* A_dev, int64_t first_color, int64_t ncolors, spd_stats* stats) {
+  return guarded([&] {
+    run_rowwalk(ctx, OpArgs{Op::SpMM, B, C_dev, nullptr, N, A_dev}, first_color, ncolors, stats);
+  });
+}
+
+int spd_spttv(spd_context* ctx, const spd_tensor* B, const double* c_dev, double* Avals_dev,
+              int64_t first_color, int64_t ncolors, spd_stats* stats) {
+  return guarded([&] {
+    run_rowwalk(ctx, OpArgs{Op::SpTTV, B, c_dev, nullptr, 1, Avals_dev}, first_color, ncolors,
+                stats);
+  });
+}
+
+int spd_spmttkrp(spd_context* ctx, const spd_tensor* B, const double* C_dev,
+                 const double* D_dev, int64_t R, double* A_dev, int64_t first_color,
+                 int64_t ncolors, spd_stats* stats) {
+  return guarded([&] {
+    run_rowwalk(ctx, OpArgs{Op::SpMTTKRP, B, C_dev, D_dev, R, A_dev}, first_color, ncolors,
+                stats);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,507 @@
+"""Host-side mirror of the reference's hot-path interface, over the C-ABI.
+
+The reference (dspar, C++) exposes this path as
+
+  * SparseTensor::from_parts / pack         tensor.hpp:62-72, tensor.cpp:94-197
+  * LevelPartitioner universe / nonzero     level_partition.hpp:23-58
+  * plan(...) -> Plan                        planner.hpp:42
+  * execute(plan, tensors, machine, ...)     sim.hpp:121-122 -> ExecResult{output, Stats}
+
+This module keeps the same names, argument meaning and error classes
+(ValidationError -> SpdValidationError, runtime errors -> SpdError) so the
+parity tests read like the reference's own tests, while every computation
+runs in libspdistal_b200.so on the GPU.  PyTorch is only used for device
+memory and streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from . import _native as N
+from ._native import SpdError, SpdValidationError, check
+
+DENSE, COMPRESSED = "d", "s"
+
+
+# ---------------------------------------------------------------- formats ---
+@dataclass(frozen=True)
+class FormatSpec:
+    """FormatSpec (tensor.hpp:19-30): level kind per storage position + mode order."""
+    kinds: tuple
+    mode_order: tuple
+
+    @property
+    def order(self):
+        return len(self.kinds)
+
+
+def parse_format(text: str) -> FormatSpec:
+    """parse_format (format_lang.cpp:13-53): "ds" = CSR, "ds:1,0" = CSC."""
+    body, _, perm = text.strip().partition(":")
+    if not body or any(ch not in "ds" for ch in body):
+        raise SpdValidationError(f"bad format '{text}'")
+    order = tuple(int(x) for x in perm.split(",")) if perm else tuple(range(len(body)))
+    if sorted(order) != list(range(len(body))):
+        raise SpdValidationError("format: mode order is not a permutation")
+    return FormatSpec(tuple(body), order)
+
+
+def level_grouping(fmt: FormatSpec) -> List[List[int]]:
+    """tensor.cpp:30-41: maximal runs of dense modes collapse into one level."""
+    groups: List[List[int]] = []
+    for k, kind in enumerate(fmt.kinds):
+        if kind == DENSE and groups and fmt.kinds[groups[-1][-1]] == DENSE:
+            groups[-1].append(k)
+        else:
+            groups.append([k])
+    return groups
+
+
+# ----------------------------------------------------------- host tensors ---
+@dataclass
+class Level:
+    kind: str                               # "d" or "s"
+    dom: tuple = ()                         # dense extents
+    pos: Optional[np.ndarray] = None        # compressed: int64 [npos, 2] inclusive (lo, hi)
+    crd: Optional[np.ndarray] = None        # compressed: int64 [nnz]
+
+    def rowptr(self) -> np.ndarray:
+        """Lossless pairs -> row pointer (tensor.cpp:258-281)."""
+        npos = self.pos.shape[0]
+        rp = np.empty(npos + 1, dtype=np.int64)
+        rp[:npos] = self.pos[:, 0]
+        rp[npos] = self.pos[-1, 1] + 1 if npos else 0
+        return rp
+
+
+@dataclass
+class SparseTensor:
+    """Host copy of the reference's SparseTensor (coordinate-tree encoding)."""
+    dims: tuple
+    format: FormatSpec
+    levels: List[Level]
+    vals: np.ndarray
+
+    @staticmethod
+    def from_parts(dims, fmt: FormatSpec, levels: List[Level], vals) -> "SparseTensor":
+        t = SparseTensor(tuple(int(d) for d in dims), fmt, levels,
+                         np.ascontiguousarray(vals, dtype=np.float64))
+        return t
+
+    @staticmethod
+    def from_rowptrs(dims, fmt: FormatSpec, rowptrs: Sequence, crds: Sequence, vals) -> "SparseTensor":
+        """Device-format constructor: one row pointer + crd per compressed level."""
+        levels = []
+        ci = 0
+        for g in level_grouping(fmt):
+            if fmt.kinds[g[0]] == DENSE:
+                levels.append(Level(DENSE, dom=tuple(dims[fmt.mode_order[k]] for k in g)))
+            else:
+                rp = np.ascontiguousarray(rowptrs[ci], dtype=np.int64)
+                pos = np.stack([rp[:-1], rp[1:] - 1], axis=1)
+                levels.append(Level(COMPRESSED, pos=np.ascontiguousarray(pos),
+                                    crd=np.ascontiguousarray(crds[ci], dtype=np.int64)))
+                ci += 1
+        return SparseTensor.from_parts(dims, fmt, levels, vals)
+
+    @staticmethod
+    def pack(dims, fmt: FormatSpec, coords, values) -> "SparseTensor":
+        """SparseTensor::pack (tensor.cpp:94-182): sort in storage order, sum
+        duplicates (in input order), keep explicit zeros.  Host-side test and
+        fixture helper (numpy)."""
+        dims = tuple(int(d) for d in dims)
+        coords = np.asarray(coords, dtype=np.int64).reshape(-1, len(dims))
+        values = np.asarray(values, dtype=np.float64).reshape(-1)
+        for k in range(len(dims)):
+            if coords.size and (coords[:, k].min() < 0 or coords[:, k].max() >= dims[k]):
+                raise SpdValidationError("pack: coordinate out of bounds")
+        skeys = coords[:, list(fmt.mode_order)] if coords.size else coords
+        if skeys.shape[0]:
+            order = np.lexsort(skeys.T[::-1])  # stable: duplicates keep input order
+            skeys = skeys[order]
+            values = values[order]
+            diff = np.any(skeys[1:] != skeys[:-1], axis=1)
+            starts = np.concatenate([[True], diff])
+            uniq = skeys[starts]
+            seg = np.cumsum(starts) - 1
+            summed = np.zeros(uniq.shape[0])
+            for i in range(values.shape[0]):  # in-order accumulation (std::map +=)
+                summed[seg[i]] += values[i]
+        else:
+            uniq = skeys.reshape(0, len(dims))
+            summed = np.zeros(0)
+        levels: List[Level] = []
+        entry_pos = np.zeros(uniq.shape[0], dtype=np.int64)
+        parent = 1
+        base = 0
+        for g in level_grouping(fmt):
+            if fmt.kinds[g[0]] == DENSE:
+                ext = tuple(dims[fmt.mode_order[k]] for k in g)
+                local = np.zeros(uniq.shape[0], dtype=np.int64)
+                for j, k in enumerate(g):
+                    local = local * ext[j] + uniq[:, base + j]
+                total = int(np.prod(ext)) if ext else 1
+                entry_pos = entry_pos * total + local
+                parent *= total
+                levels.append(Level(DENSE, dom=ext))
+            else:
+                col = uniq[:, base]
+                key = np.stack([entry_pos, col], axis=1)
+                if key.shape[0]:
+                    newp = np.concatenate([[True], np.any(key[1:] != key[:-1], axis=1)])
+                else:
+                    newp = np.zeros(0, dtype=bool)
+                crd = col[newp]
+                ids = np.cumsum(newp) - 1
+                parents = entry_pos[newp]
+                counts = np.bincount(parents, minlength=parent) if parents.size else np.zeros(parent, np.int64)
+                rp = np.zeros(parent + 1, dtype=np.int64)
+                rp[1:] = np.cumsum(counts)
+                pos = np.stack([rp[:-1], rp[1:] - 1], axis=1)
+                levels.append(Level(COMPRESSED, pos=np.ascontiguousarray(pos), crd=crd.astype(np.int64)))
+                entry_pos = ids.astype(np.int64)
+                parent = int(crd.shape[0])
+            base += len(g)
+        vals = np.zeros(parent)
+        if uniq.shape[0]:
+            vals[entry_pos] = summed
+        return SparseTensor.from_parts(dims, fmt, levels, vals)
+
+    def nnz(self) -> int:
+        return int(self.vals.shape[0])
+
+    def compressed_rowptrs(self):
+        return [lv.rowptr() for lv in self.levels if lv.kind == COMPRESSED]
+
+    def densify(self) -> np.ndarray:
+        """densify (oracle.cpp:39-43) for small tensors."""
+        out = np.zeros(self.dims)
+        for coords, v in self.leaves():
+            out[coords] += v
+        return out
+
+    def leaves(self):
+        """(logical coords, value) per stored path (tensor.cpp:199-206)."""
+        fmt = self.format
+        paths = [((), 0)]  # (storage coords so far, position)
+        for lv in self.levels:
+            nxt = []
+            if lv.kind == DENSE:
+                total = int(np.prod(lv.dom)) if lv.dom else 1
+                for sc, p in paths:
+                    for s in range(total):
+                        pt = np.unravel_index(s, lv.dom) if lv.dom else ()
+                        nxt.append((sc + tuple(int(x) for x in pt), p * total + s))
+            else:
+                for sc, p in paths:
+                    lo, hi = lv.pos[p]
+                    for q in range(lo, hi + 1):
+                        nxt.append((sc + (int(lv.crd[q]),), q))
+            paths = nxt
+        out = []
+        for sc, p in paths:
+            logical = [0] * len(self.dims)
+            for k, c in enumerate(sc):
+                logical[fmt.mode_order[k]] = c
+            out.append((tuple(logical), float(self.vals[p])))
+        return out
+
+
+# ---------------------------------------------------------------- device ---
+def _i64arr(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+class Context:
+    """One GPU (spd_context).  `stream` defaults to torch's current stream so
+    torch-allocated buffers and the backend's kernels are ordered."""
+
+    def __init__(self, device: int = 0, stream: Optional[int] = None, use_torch_stream: bool = True):
+        self.device = device
+        if stream is None and use_torch_stream:
+            import torch
+            torch.cuda.set_device(device)
+            stream = torch.cuda.current_stream(device).cuda_stream
+        h = C.c_void_p()
+        check(N.lib().spd_context_create(device, C.c_void_p(stream) if stream else None, C.byref(h)))
+        self.h = h
+
+    def synchronize(self):
+        check(N.lib().spd_context_synchronize(self.h))
+
+    def init_comm(self, unique_id: bytes, rank: int, world: int):
+        buf = C.create_string_buffer(unique_id, 128)
+        check(N.lib().spd_context_init_comm(self.h, buf, rank, world))
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(N.lib().spd_nccl_unique_id(buf))
+        return buf.raw
+
+    def close(self):
+        if self.h:
+            check(N.lib().spd_context_destroy(self.h))
+            self.h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
+def _format_arrays(dims, fmt: FormatSpec):
+    order = len(dims)
+    d = (C.c_int64 * order)(*[int(x) for x in dims])
+    kinds = (C.c_int * order)(*[N.SPD_DENSE if k == DENSE else N.SPD_COMPRESSED for k in fmt.kinds])
+    mo = (C.c_int * order)(*fmt.mode_order)
+    return d, kinds, mo
+
+
+class DeviceTensor:
+    """A tensor resident in HBM (spd_tensor)."""
+
+    def __init__(self, ctx: Context, handle, dims, fmt: FormatSpec, keep=None):
+        self.ctx, self.h, self.dims, self.format = ctx, handle, tuple(dims), fmt
+        self._keep = keep
+
+    @staticmethod
+    def upload(ctx: Context, t: SparseTensor) -> "DeviceTensor":
+        """spd_tensor_upload: the reference's own (lo,hi) pos pairs; validated on the GPU."""
+        d, kinds, mo = _format_arrays(t.dims, t.format)
+        nl = len(t.levels)
+        keep = []
+        pos = (N.i64p * nl)()
+        crd = (N.i64p * nl)()
+        for l, lv in enumerate(t.levels):
+            if lv.kind == COMPRESSED:
+                p = _i64arr(lv.pos).reshape(-1)
+                c = _i64arr(lv.crd)
+                keep += [p, c]
+                pos[l] = p.ctypes.data_as(N.i64p)
+                crd[l] = c.ctypes.data_as(N.i64p)
+        vals = np.ascontiguousarray(t.vals, dtype=np.float64)
+        h = C.c_void_p()
+        check(N.lib().spd_tensor_upload(ctx.h, len(t.dims), d, kinds, mo, pos, crd,
+                                        vals.ctypes.data_as(N.dblp), C.byref(h)))
+        return DeviceTensor(ctx, h, t.dims, t.format)
+
+    @staticmethod
+    def upload_rowptr(ctx: Context, dims, fmt: FormatSpec, rowptrs, crds, vals,
+                      validate=True) -> "DeviceTensor":
+        """spd_tensor_upload_rowptr: device-format host arrays (one per compressed level)."""
+        d, kinds, mo = _format_arrays(dims, fmt)
+        groups = level_grouping(fmt)
+        nl = len(groups)
+        pos = (N.i64p * nl)()
+        crd = (N.i64p * nl)()
+        keep = []
+        ci = 0
+        for l, g in enumerate(groups):
+            if fmt.kinds[g[0]] == COMPRESSED:
+                rp = _i64arr(rowptrs[ci])
+                c = _i64arr(crds[ci])
+                keep += [rp, c]
+                pos[l] = rp.ctypes.data_as(N.i64p)
+                crd[l] = c.ctypes.data_as(N.i64p)
+                ci += 1
+        v = np.ascontiguousarray(vals, dtype=np.float64)
+        h = C.c_void_p()
+        check(N.lib().spd_tensor_upload_rowptr(ctx.h, len(dims), d, kinds, mo, pos, crd,
+                                               v.ctypes.data_as(N.dblp), int(bool(validate)),
+                                               C.byref(h)))
+        return DeviceTensor(ctx, h, dims, fmt)
+
+    @staticmethod
+    def wrap(ctx: Context, dims, fmt: FormatSpec, rowptr_ptrs, crd_ptrs, vals_ptr, keep=None):
+        """spd_tensor_wrap_device: zero-copy over device arrays (e.g. torch tensors)."""
+        d, kinds, mo = _format_arrays(dims, fmt)
+        groups = level_grouping(fmt)
+        nl = len(groups)
+        rp = (C.c_void_p * nl)()
+        cr = (C.c_void_p * nl)()
+        ci = 0
+        for l, g in enumerate(groups):
+            if fmt.kinds[g[0]] == COMPRESSED:
+                rp[l] = rowptr_ptrs[ci]
+                cr[l] = crd_ptrs[ci]
+                ci += 1
+        h = C.c_void_p()
+        check(N.lib().spd_tensor_wrap_device(ctx.h, len(dims), d, kinds, mo, rp, cr,
+                                             C.c_void_p(vals_ptr), C.byref(h)))
+        return DeviceTensor(ctx, h, dims, fmt, keep)
+
+    def num_levels(self) -> int:
+        n = C.c_int()
+        check(N.lib().spd_tensor_num_levels(self.h, C.byref(n)))
+        return n.value
+
+    def level(self, l):
+        kind, par, pos = C.c_int(), C.c_int64(), C.c_int64()
+        check(N.lib().spd_tensor_level(self.h, l, C.byref(kind), C.byref(par), C.byref(pos)))
+        return kind.value, par.value, pos.value
+
+    def nvals(self) -> int:
+        n = C.c_int64()
+        check(N.lib().spd_tensor_nvals(self.h, C.byref(n)))
+        return n.value
+
+    def vals_ptr(self) -> int:
+        p = C.c_void_p()
+        check(N.lib().spd_tensor_vals_ptr(self.h, C.byref(p)))
+        return p.value
+
+    def download(self) -> SparseTensor:
+        levels = []
+        for l in range(self.num_levels()):
+            kind, par, pos = self.level(l)
+            if kind == N.SPD_DENSE:
+                levels.append(None)
+                continue
+            pairs = np.empty((par, 2), dtype=np.int64)
+            crd = np.empty(pos, dtype=np.int64)
+            check(N.lib().spd_tensor_download_level(self.h, l, pairs.ctypes.data_as(N.i64p),
+                                                    crd.ctypes.data_as(N.i64p)))
+            levels.append(Level(COMPRESSED, pos=pairs, crd=crd))
+        groups = level_grouping(self.format)
+        for l, g in enumerate(groups):
+            if levels[l] is None:
+                levels[l] = Level(DENSE, dom=tuple(self.dims[self.format.mode_order[k]] for k in g))
+        vals = np.empty(self.nvals(), dtype=np.float64)
+        check(N.lib().spd_tensor_download_vals(self.h, vals.ctypes.data_as(N.dblp)))
+        return SparseTensor.from_parts(self.dims, self.format, levels, vals)
+
+    def close(self):
+        if self.h:
+            check(N.lib().spd_tensor_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+# ------------------------------------------------------------ partitions ---
+@dataclass
+class Colour:
+    """One colour of a distributed loop (spd_color), inclusive ranges."""
+    color: tuple
+    q: tuple
+    par: tuple
+    top: tuple
+
+
+def _colours(arr) -> List[Colour]:
+    return [Colour((c.color.lo, c.color.hi), (c.q.lo, c.q.hi), (c.par.lo, c.par.hi),
+                   (c.top.lo, c.top.hi)) for c in arr]
+
+
+def partition_universe(ctx: Context, t: DeviceTensor, pieces: int) -> List[Colour]:
+    arr = (N.spd_color * pieces)()
+    check(N.lib().spd_partition_universe(ctx.h, t.h, pieces, arr))
+    return _colours(arr)
+
+
+def partition_nonzero(ctx: Context, t: DeviceTensor, level: int, pieces: int) -> List[Colour]:
+    arr = (N.spd_color * pieces)()
+    check(N.lib().spd_partition_nonzero(ctx.h, t.h, level, pieces, arr))
+    return _colours(arr)
+
+
+REGION = {"dom": 0, "pos": 1, "crd": 2, "vals": 3}
+
+
+def materialize(ctx: Context, t: DeviceTensor, level: int, region: str, color: int) -> np.ndarray:
+    """K2m: one colour's explicit index set of a bundle region."""
+    count = C.c_int64()
+    check(N.lib().spd_partition_materialize(ctx.h, t.h, level, REGION[region], color, None, 0,
+                                            C.byref(count)))
+    out = np.empty(count.value, dtype=np.int64)
+    check(N.lib().spd_partition_materialize(ctx.h, t.h, level, REGION[region], color,
+                                            out.ctypes.data_as(N.i64p), count.value,
+                                            C.byref(count)))
+    return out
+
+
+# ------------------------------------------------------------------ stats ---
+@dataclass
+class Stats:
+    """Stats (sim.hpp:25-36)."""
+    workers: int
+    work: List[int]
+    imbalance: float
+    combines: int
+    kernel_ms: float = 0.0
+    launches: int = 0
+
+
+def _stats(ctx: Context, st: N.spd_stats, pieces: int) -> Stats:
+    work = (C.c_int64 * pieces)()
+    check(N.lib().spd_last_work(ctx.h, work, pieces))
+    return Stats(st.workers, list(work), st.imbalance, st.combines, st.kernel_ms, st.launches)
+
+
+def _ptr(x) -> C.c_void_p:
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return C.c_void_p(x.data_ptr())
+    return C.c_void_p(int(x))
+
+
+# --------------------------------------------------------------- leaf ops ---
+def spmv(ctx, B: DeviceTensor, c, a, first=0, count=None, pieces=None, stats=True):
+    st = N.spd_stats()
+    count = pieces - first if count is None else count
+    check(N.lib().spd_spmv(ctx.h, B.h, _ptr(c), _ptr(a), first, count, C.byref(st) if stats else None))
+    return _stats(ctx, st, pieces) if stats else None
+
+
+def spmm(ctx, B: DeviceTensor, Cd, n_cols, A, first=0, count=None, pieces=None, stats=True):
+    st = N.spd_stats()
+    count = pieces - first if count is None else count
+    check(N.lib().spd_spmm(ctx.h, B.h, _ptr(Cd), n_cols, _ptr(A), first, count,
+                           C.byref(st) if stats else None))
+    return _stats(ctx, st, pieces) if stats else None
+
+
+def sddmm(ctx, B: DeviceTensor, Cd, Dd, K, dk, dj, Avals, first=0, count=None, pieces=None, stats=True):
+    st = N.spd_stats()
+    count = pieces - first if count is None else count
+    check(N.lib().spd_sddmm(ctx.h, B.h, _ptr(Cd), _ptr(Dd), K, dk, dj, _ptr(Avals), first, count,
+                            C.byref(st) if stats else None))
+    return _stats(ctx, st, pieces) if stats else None
+
+
+def spttv(ctx, B: DeviceTensor, c, Avals, first=0, count=None, pieces=None, stats=True):
+    st = N.spd_stats()
+    count = pieces - first if count is None else count
+    check(N.lib().spd_spttv(ctx.h, B.h, _ptr(c), _ptr(Avals), first, count,
+                            C.byref(st) if stats else None))
+    return _stats(ctx, st, pieces) if stats else None
+
+
+def spmttkrp(ctx, B: DeviceTensor, Cd, Dd, R, A, first=0, count=None, pieces=None, stats=True):
+    st = N.spd_stats()
+    count = pieces - first if count is None else count
+    check(N.lib().spd_spmttkrp(ctx.h, B.h, _ptr(Cd), _ptr(Dd), R, _ptr(A), first, count,
+                               C.byref(st) if stats else None))
+    return _stats(ctx, st, pieces) if stats else None
+
+
+def spadd3(ctx, B: DeviceTensor, Cm: DeviceTensor, D: DeviceTensor, first=0, count=None,
+           pieces=None, stats=True):
+    st = N.spd_stats()
+    count = pieces - first if count is None else count
+    h = C.c_void_p()
+    check(N.lib().spd_spadd3(ctx.h, B.h, Cm.h, D.h, C.byref(h), first, count,
+                             C.byref(st) if stats else None))
+    A = DeviceTensor(ctx, h, B.dims, B.format)
+    return A, (_stats(ctx, st, pieces) if stats else None)
