@@ -199,6 +199,16 @@ int spd_spadd3(spd_context* ctx, const spd_tensor* B, const spd_tensor* C, const
  * entries. */
 int spd_last_work(spd_context* ctx, int64_t* work, int64_t pieces);
 
+/* ---- (5) instrumentation ----------------------------------------------- */
+/* Records a CUDA-event pair around every leaf kernel launched on the
+ * context's stream while enabled (no host synchronisation). */
+int spd_context_timing(spd_context* ctx, int enable);
+/* Synchronises, returns up to `cap` recorded leaf-kernel durations (ms) in
+ * launch order via *n, and clears the record. */
+int spd_context_read_timing(spd_context* ctx, double* leaf_ms, int64_t cap, int64_t* n);
+/* Kernels launched by this context since it was created. */
+int spd_context_launches(const spd_context* ctx, int64_t* count);
+
 #ifdef __cplusplus
 }
 #endif

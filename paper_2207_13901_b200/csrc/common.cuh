@@ -140,6 +140,12 @@ struct spd_context {
   spd::DeviceBuffer scratch[6];
   spd::DeviceBuffer counters;        // small int64 device counters
   int64_t* pinned_counters = nullptr;
+
+  // Instrumentation (spd_context_timing / spd_context_launches).
+  int64_t launches = 0;
+  bool timing = false;
+  std::vector<cudaEvent_t> timing_events;  // pairs, grow-only pool
+  size_t timing_used = 0;                  // events in use (2 per leaf launch)
 };
 
 namespace spd {
@@ -196,5 +202,8 @@ const std::vector<spd_color>& host_colors(spd_context* ctx);  // syncs if needed
 void require_partition(spd_context* ctx, const spd_tensor* t, int64_t first, int64_t count);
 void fill_stats(spd_context* ctx, spd_stats* st, int64_t combines, const std::vector<int64_t>& work,
                 int64_t launches, bool timed);
+// Brackets the leaf kernel of an op with a timing event pair when enabled.
+void leaf_timing_begin(spd_context* ctx);
+void leaf_timing_end(spd_context* ctx);
 
 }  // namespace spd

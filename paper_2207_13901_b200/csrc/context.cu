@@ -291,11 +291,58 @@ void fill_stats(spd_context* ctx, spd_stats* st, int64_t combines, const std::ve
   }
 }
 
+static cudaEvent_t timing_event(spd_context* ctx) {
+  if (ctx->timing_used == ctx->timing_events.size()) {
+    cudaEvent_t e;
+    SPD_CUDA(cudaEventCreate(&e));
+    ctx->timing_events.push_back(e);
+  }
+  return ctx->timing_events[ctx->timing_used++];
+}
+
+void leaf_timing_begin(spd_context* ctx) {
+  if (ctx->timing) SPD_CUDA(cudaEventRecord(timing_event(ctx), ctx->stream));
+}
+
+void leaf_timing_end(spd_context* ctx) {
+  if (ctx->timing) SPD_CUDA(cudaEventRecord(timing_event(ctx), ctx->stream));
+}
+
 }  // namespace spd
 
 using namespace spd;
 
 extern "C" {
+
+int spd_context_timing(spd_context* ctx, int enable) {
+  return guarded([&] {
+    checked(ctx);
+    ctx->timing = enable != 0;
+  });
+}
+
+int spd_context_read_timing(spd_context* ctx, double* leaf_ms, int64_t cap, int64_t* n) {
+  return guarded([&] {
+    checked(ctx);
+    activate(ctx);
+    SPD_CUDA(cudaStreamSynchronize(ctx->stream));
+    int64_t pairs = (int64_t)ctx->timing_used / 2;
+    for (int64_t i = 0; i < pairs && i < cap; i++) {
+      float ms = 0;
+      SPD_CUDA(cudaEventElapsedTime(&ms, ctx->timing_events[2 * i], ctx->timing_events[2 * i + 1]));
+      leaf_ms[i] = ms;
+    }
+    *n = pairs;
+    ctx->timing_used = 0;
+  });
+}
+
+int spd_context_launches(const spd_context* ctx, int64_t* count) {
+  return guarded([&] {
+    if (!ctx) throw ValidationError("null spd_context");
+    *count = ctx->launches;
+  });
+}
 
 const char* spd_last_error(void) { return g_last_error.c_str(); }
 int spd_abi_version(void) { return 100; }
@@ -340,6 +387,7 @@ int spd_context_destroy(spd_context* ctx) {
     for (auto& b : ctx->scratch) b.release();
     ctx->counters.release();
     if (ctx->pinned_counters) cudaFreeHost(ctx->pinned_counters);
+    for (cudaEvent_t e : ctx->timing_events) cudaEventDestroy(e);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);

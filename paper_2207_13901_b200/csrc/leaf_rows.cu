@@ -660,6 +660,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   launches++;
 
   const spd_level_store& leaf = B->levels[nl - 1];
+  leaf_timing_begin(ctx);
   switch (a.op) {
     case Op::SpMV:
     case Op::SpTTV: {
@@ -710,6 +711,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
     }
   }
   SPD_CHECK_LAUNCH();
+  leaf_timing_end(ctx);
   launches++;
   {
     static int grid = 0;
@@ -727,6 +729,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
       col, (const DevColor*)ctx->colors_dev.ptr, P, W, first, count, a.out);
   SPD_CHECK_LAUNCH();
   launches++;
+  ctx->launches += launches;
   if (stats) {
     SPD_CUDA(cudaEventRecord(ctx->ev1, s));
     SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters, col.counters, sizeof(int64_t) * 4,

@@ -182,6 +182,7 @@ static void run_partition(spd_context* ctx, const spd_tensor* t, int level, int6
     k_partition_universe<<<(unsigned)pieces, 32, 0, ctx->stream>>>(v, pieces, cols);
   }
   SPD_CHECK_LAUNCH();
+  ctx->launches++;
   ctx->split = nonzero ? SplitKind::NonZero : SplitKind::Universe;
   ctx->split_tensor = t;
   ctx->split_level = nonzero ? level : 0;

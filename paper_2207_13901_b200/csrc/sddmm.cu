@@ -134,6 +134,7 @@ static void run_sddmm(spd_context* ctx, const spd_tensor* B, const double* C, co
   SPD_CHECK_LAUNCH();
   launches++;
   const int64_t kt = ceil_div(K > 0 ? K : 1, 32);
+  leaf_timing_begin(ctx);
 #define SDDMM_CASE(KT_)                                                                    \
   {                                                                                        \
     static int grid = 0;                                                                   \
@@ -147,7 +148,9 @@ static void run_sddmm(spd_context* ctx, const spd_tensor* B, const double* C, co
   else SDDMM_CASE(8)
 #undef SDDMM_CASE
   SPD_CHECK_LAUNCH();
+  leaf_timing_end(ctx);
   launches++;
+  ctx->launches += launches;
   if (stats) {
     SPD_CUDA(cudaEventRecord(ctx->ev1, s));
     const auto& hc = host_colors(ctx);

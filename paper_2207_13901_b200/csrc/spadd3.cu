@@ -197,6 +197,7 @@ static void run_spadd3(spd_context* ctx, const spd_tensor* B, const spd_tensor* 
   SPD_CUDA(cudaMallocAsync((void**)&Acrd, sizeof(int64_t) * (nnzA > 0 ? nnzA : 1), s));
   SPD_CUDA(cudaMallocAsync((void**)&Avals, sizeof(double) * (nnzA > 0 ? nnzA : 1), s));
   const int64_t np[3] = {nb, nc, nd};
+  leaf_timing_begin(ctx);
   for (int t = 0; t < 3; t++) {
     if (np[t] == 0) continue;
     k_fill<<<grid_n(ctx, np[t]), 256, 0, s>>>(t, b, c, d, n, 0, np[t] - 1, fC, fD, PC, PD, rpA,
@@ -204,6 +205,8 @@ static void run_spadd3(spd_context* ctx, const spd_tensor* B, const spd_tensor* 
     SPD_CHECK_LAUNCH();
     launches++;
   }
+  leaf_timing_end(ctx);
+  ctx->launches += launches;
   auto* A = new spd_tensor();
   A->ctx = ctx;
   A->order = B->order;

@@ -129,8 +129,7 @@ class SparseTensor:
             uniq = skeys[starts]
             seg = np.cumsum(starts) - 1
             summed = np.zeros(uniq.shape[0])
-            for i in range(values.shape[0]):  # in-order accumulation (std::map +=)
-                summed[seg[i]] += values[i]
+            np.add.at(summed, seg, values)  # unbuffered, in input order (std::map +=)
         else:
             uniq = skeys.reshape(0, len(dims))
             summed = np.zeros(0)
@@ -242,6 +241,21 @@ class Context:
         buf = C.create_string_buffer(128)
         check(N.lib().spd_nccl_unique_id(buf))
         return buf.raw
+
+    def timing(self, enable: bool):
+        """Record CUDA events around every leaf kernel (spd_context_timing)."""
+        check(N.lib().spd_context_timing(self.h, int(bool(enable))))
+
+    def read_timing(self, cap: int = 1 << 16) -> List[float]:
+        buf = (C.c_double * cap)()
+        n = C.c_int64()
+        check(N.lib().spd_context_read_timing(self.h, buf, cap, C.byref(n)))
+        return [buf[i] for i in range(min(n.value, cap))]
+
+    def launches(self) -> int:
+        n = C.c_int64()
+        check(N.lib().spd_context_launches(self.h, C.byref(n)))
+        return n.value
 
     def close(self):
         if self.h:
@@ -403,16 +417,17 @@ def _colours(arr) -> List[Colour]:
                    (c.top.lo, c.top.hi)) for c in arr]
 
 
-def partition_universe(ctx: Context, t: DeviceTensor, pieces: int) -> List[Colour]:
-    arr = (N.spd_color * pieces)()
+def partition_universe(ctx: Context, t: DeviceTensor, pieces: int, host=True):
+    """host=False keeps the colours on the device (no synchronisation)."""
+    arr = (N.spd_color * pieces)() if host else None
     check(N.lib().spd_partition_universe(ctx.h, t.h, pieces, arr))
-    return _colours(arr)
+    return _colours(arr) if host else None
 
 
-def partition_nonzero(ctx: Context, t: DeviceTensor, level: int, pieces: int) -> List[Colour]:
-    arr = (N.spd_color * pieces)()
+def partition_nonzero(ctx: Context, t: DeviceTensor, level: int, pieces: int, host=True):
+    arr = (N.spd_color * pieces)() if host else None
     check(N.lib().spd_partition_nonzero(ctx.h, t.h, level, pieces, arr))
-    return _colours(arr)
+    return _colours(arr) if host else None
 
 
 REGION = {"dom": 0, "pos": 1, "crd": 2, "vals": 3}

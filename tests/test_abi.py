@@ -1,0 +1,73 @@
+"""The C-ABI boundary (CPU): the in-tree library loads, exports exactly what
+include/spdistal_b200.h declares, maps errors onto the reference's classes,
+and fails loudly without a GPU (no CPU fallback)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+from paper_2207_13901_b200 import _native as N
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "spdistal_b200.h")
+PKG = os.path.join(ROOT, "paper_2207_13901_b200")
+
+
+def declared_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(spd_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_declares_the_boundary():
+    syms = declared_symbols()
+    for must in ["spd_tensor_upload", "spd_partition_universe", "spd_partition_nonzero",
+                 "spd_spmv", "spd_spmm", "spd_sddmm", "spd_spttv", "spd_spmttkrp", "spd_spadd3",
+                 "spd_context_init_comm", "spd_last_error"]:
+        assert must in syms
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.lib()
+    for s in declared_symbols():
+        assert hasattr(lib, s), s
+    assert set(declared_symbols()) == set(N.SIGNATURES), "bindings out of sync with the header"
+
+
+def test_abi_version():
+    assert N.lib().spd_abi_version() == 100
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    h = C.c_void_p()
+    st = N.lib().spd_context_create(0, None, C.byref(h))
+    assert st == N.SPD_ERR_RUNTIME
+    assert b"no CUDA device" in N.lib().spd_last_error()
+    with pytest.raises(N.SpdError):
+        N.check(st)
+
+
+def test_null_arguments_are_validation_errors():
+    assert N.lib().spd_context_synchronize(None) == N.SPD_ERR_VALIDATION
+    assert N.lib().spd_tensor_destroy(None) == N.SPD_OK
+
+
+def test_product_never_touches_the_oracle():
+    """Only tests/, smoke() and bench's baseline legs may use oracle/."""
+    for dirpath, _, files in os.walk(PKG):
+        if "build" in dirpath:
+            continue
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".c", ".h")):
+                src = open(os.path.join(dirpath, f), errors="replace").read()
+                assert "oracle_bind" not in src and "liboracle" not in src and "libdspar_ref" not in src, f
+
+
+def test_synth_library_loads():
+    s = N.synth()
+    assert s.syn_max_threads() >= 1

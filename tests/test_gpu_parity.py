@@ -1,0 +1,166 @@
+"""GPU parity through the C-ABI: the sm_100a path against the oracle.
+
+  * every reference-generated golden case (tests/golden): partition bounds,
+    bundle subsets (K2m), Stats (work / combines / imbalance) bit-exact;
+    output values bit-exact for integer-valued inputs, within 1e-10 relative
+    (north_star's bound for fp64 reassociation) otherwise; SpAdd3 pattern
+    bit-exact;
+  * seeded random instances against the C restatement at larger sizes;
+  * edge cases the reference tests: empty tensors, P > nnz, hub rows that
+    straddle many colours, invalid pos structures.
+"""
+import numpy as np
+import pytest
+
+import golden_cases as G
+import oracle_bind as ob
+import spd_kernels as K
+from oracle_exec import oracle_execute
+
+pytestmark = pytest.mark.gpu
+
+RTOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2207_13901_b200 import host as H
+
+    c = H.Context(0)
+    yield c
+    c.close()
+
+
+def assert_close(kernel, got, want, exact):
+    if kernel == "spadd3":
+        for g, w in zip(got[:2], want[:2]):
+            assert np.array_equal(np.asarray(g), np.asarray(w)), "SpAdd3 pattern must be bit-exact"
+        got, want = got[2], want[2]
+    got = np.asarray(got, dtype=np.float64).reshape(-1)
+    want = np.asarray(want, dtype=np.float64).reshape(-1)
+    assert got.shape == want.shape
+    if exact:
+        assert np.array_equal(got, want), np.max(np.abs(got - want))
+    else:
+        err = np.abs(got - want)
+        tol = RTOL * np.maximum(np.abs(want), 1e-300)
+        bad = err > tol
+        assert not bad.any(), (err[bad][:5], want[bad][:5])
+
+
+GOLD_INDEX, GOLD_DATA = G.load()
+
+
+@pytest.mark.parametrize("entry", GOLD_INDEX, ids=lambda e: f"{e['key']}-{e['kernel']}-{e['schedule']}-P{e['pieces']}")
+def test_gpu_matches_reference_golden(ctx, entry):
+    from paper_2207_13901_b200 import host as H
+    from paper_2207_13901_b200.execute import execute
+
+    tensors = G.case_tensors(GOLD_DATA, entry)
+    out, st, cols = execute(entry["kernel"], tensors, entry["schedule"], entry["pieces"], ctx)
+    exact = "int" in entry["origin"] or "kat" in entry["origin"]
+    assert_close(entry["kernel"], out, G.expected_out(GOLD_DATA, entry), exact)
+    assert [c.color for c in cols] == [tuple(b) for b in entry["color_bounds"]]
+    if entry["schedule"] == "nonzero" and entry["out_bounds"] is not None:
+        assert [c.top for c in cols] == [tuple(b) for b in entry["out_bounds"]]
+    assert st.work == entry["work"]
+    assert st.combines == entry["combines"]
+    assert st.imbalance == entry["imbalance"]
+    # K2m: the GPU partition materialised exactly as the reference's bundle
+    B = H.DeviceTensor.upload(ctx, tensors["B"])
+    from paper_2207_13901_b200.execute import partition
+
+    partition(ctx, B, entry["schedule"], entry["pieces"])
+    Bt = tensors["B"]
+    key = entry["key"]
+    for c in range(entry["pieces"]):
+        assert list(H.materialize(ctx, B, 0, "vals", c)) == list(GOLD_DATA[f"{key}/B_vals_c{c}"])
+        for l, lv in enumerate(Bt.levels):
+            regions = ["dom"] if lv.kind == "d" else ["pos", "crd"]
+            for r in regions:
+                k = f"{key}/B_{r}{l}_c{c}"
+                if k in GOLD_DATA:
+                    got = H.materialize(ctx, B, l, r, c)
+                    assert list(got) == list(GOLD_DATA[k]), (r, l, c)
+    B.close()
+
+
+@pytest.mark.parametrize("kernel", list(K.KERNELS))
+@pytest.mark.parametrize("schedule", ["row", "nonzero"])
+@pytest.mark.parametrize("pieces", [1, 3, 8])
+def test_gpu_matches_restatement_random(ctx, kernel, schedule, pieces):
+    from paper_2207_13901_b200.execute import execute
+
+    if schedule == "nonzero" and K.KERNELS[kernel]["nonzero"] is None:
+        pytest.skip("position split rejected for union statements")
+    rng = np.random.default_rng(abs(hash((kernel, schedule, pieces))) % 2**32)
+    for integers in (True, False):
+        dims = 300 if kernel not in ("spttv", "spmttkrp") else None
+        t = K.instance(kernel, rng, integers=integers, density=0.05,
+                       max_dim=dims or 40, rank=32 if kernel in ("spmm", "spmttkrp") else None)
+        want = oracle_execute(kernel, t, schedule, pieces)
+        out, st, cols = execute(kernel, t, schedule, pieces, ctx)
+        assert_close(kernel, out, want["out"], integers)
+        assert st.work == want["work"] and st.combines == want["combines"]
+
+
+def test_upload_rejects_broken_pos(ctx):
+    from paper_2207_13901_b200 import host as H
+    from paper_2207_13901_b200._native import SpdValidationError
+
+    B = K.random_sparse(np.random.default_rng(3), (5, 5), "ds", 0.4)
+    B.levels[1].pos = B.levels[1].pos.copy()
+    B.levels[1].pos[2, 0] += 1  # gap in the tiling of [0, nnz)
+    with pytest.raises(SpdValidationError):
+        H.DeviceTensor.upload(ctx, B)
+    C = K.random_sparse(np.random.default_rng(4), (5, 5), "ds", 0.6)
+    C.levels[1].crd = C.levels[1].crd[::-1].copy()  # crd not increasing
+    with pytest.raises(SpdValidationError):
+        H.DeviceTensor.upload(ctx, C)
+
+
+@pytest.mark.parametrize("pieces", [1, 4, 9])
+def test_empty_and_degenerate(ctx, pieces):
+    from paper_2207_13901_b200.execute import execute
+    from paper_2207_13901_b200.host import SparseTensor, parse_format
+
+    empty = SparseTensor.pack((7, 5), parse_format("ds"), np.zeros((0, 2)), [])
+    c = K.dense(np.random.default_rng(0), (5,), "d")
+    for sched in ("row", "nonzero"):
+        out, st, cols = execute("spmv", {"B": empty, "c": c}, sched, pieces, ctx)
+        assert np.array_equal(out, np.zeros(7))
+        assert st.combines == 0
+    # one hub row spanning every colour, P > nnz
+    hub = SparseTensor.pack((3, 50), parse_format("ds"), [[1, j] for j in range(6)], np.arange(1, 7.0))
+    cc = K.dense(np.random.default_rng(1), (50,), "d")
+    want = oracle_execute("spmv", {"B": hub, "c": cc}, "nonzero", pieces)
+    out, st, cols = execute("spmv", {"B": hub, "c": cc}, "nonzero", pieces, ctx)
+    assert np.array_equal(out, want["out"])
+    assert st.combines == want["combines"] and st.work == want["work"]
+
+
+@pytest.mark.parametrize("kernel", ["spmv", "spmm"])
+def test_long_hub_rows_cross_many_chunks(ctx, kernel):
+    """Rows far longer than a warp chunk exercise the carry chains."""
+    from paper_2207_13901_b200.execute import execute
+    from paper_2207_13901_b200.host import SparseTensor, parse_format
+
+    rng = np.random.default_rng(11)
+    n, m = 64, 200000
+    rows = np.concatenate([np.zeros(150000, np.int64), rng.integers(0, n, 20000)])
+    cols = rng.integers(0, m, rows.shape[0])
+    vals = rng.integers(1, 4, rows.shape[0]).astype(float)
+    B = SparseTensor.pack((n, m), parse_format("ds"), np.stack([rows, cols], 1), vals)
+    t = {"B": B}
+    if kernel == "spmv":
+        t["c"] = K.dense(rng, (m,), "d")
+    else:
+        t["C"] = K.dense(rng, (m, 8), "dd")
+    for pieces in (1, 5):
+        want = oracle_execute(kernel, t, "nonzero", pieces)
+        out, st, _ = execute(kernel, t, "nonzero", pieces, ctx)
+        assert_close(kernel, out, want["out"], True)
+        assert st.combines == want["combines"]
