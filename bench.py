@@ -108,6 +108,11 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_first(self, timeout=10.0):
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.05)
+
     def __exit__(self, *exc):
         if self.proc:
             self.proc.terminate()
@@ -266,27 +271,37 @@ def main():
         H.partition_nonzero(ctx, B, 1, pieces, host=False)
         H.spmm(ctx, B, C_d, N, A_d, first=first, count=count, pieces=pieces, stats=False)
 
-    for _ in range(max(args.warmup, 3)):
-        step()
-    torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    launches0 = ctx.launches()
-    ctx.timing(True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
+    # Clocks are sampled (nvidia-smi, 100 ms) over a loaded window that
+    # brackets the timed region: >= W warm-up steps and >= 1.5 s of load
+    # before it, 0.5 s after it.
     with ClockSampler(local) as clocks:
+        clocks.wait_first()
+        t_end, nw = time.time() + 1.5, 0
+        while nw < max(args.warmup, 3) or time.time() < t_end:
+            step()
+            torch.cuda.synchronize()
+            nw += 1
+        launches0 = ctx.launches()
+        ctx.timing(True)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(args.steps):
             step()
         ev1.record(stream)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ctx.timing(False)
+        if world > 1:
+            dist.barrier()
+        ctx.timing(False)
+        launches = ctx.launches() - launches0
+        t_end = time.time() + 0.5
+        while time.time() < t_end:
+            step()
+            torch.cuda.synchronize()
     leaf_ms = ctx.read_timing()
-    launches = ctx.launches() - launches0
     ms = ev0.elapsed_time(ev1) / args.steps
     ms_t = torch.tensor([ms, float(np.mean(leaf_ms)) if leaf_ms else 0.0], dtype=torch.float64, device=dev)
     if world > 1:

@@ -93,8 +93,9 @@ const char* spd_last_error(void);
 int spd_abi_version(void);
 
 /* ---- (1) context: one per GPU (one process per GPU) -------------------- */
-/* device: CUDA ordinal.  stream: a cudaStream_t to enqueue on, or NULL for a
- * context-owned non-blocking stream. */
+/* device: CUDA ordinal.  stream: a cudaStream_t to enqueue on (cudaStreamLegacy
+ * (0x1) selects the legacy default stream), or NULL for a context-owned
+ * non-blocking stream. */
 int spd_context_create(int device, void* stream, spd_context** out);
 int spd_context_destroy(spd_context* ctx);
 int spd_context_synchronize(spd_context* ctx);

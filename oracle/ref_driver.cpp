@@ -28,6 +28,13 @@
 
 using namespace dspar;
 
+#ifdef WITH_GPU_EXEC
+// integration/gpu_execute.cpp: the ExecMode::Gpu adapter under test.
+namespace dspar_gpu {
+ExecResult execute_gpu(const Plan& plan, const TensorSet& tensors, const MachineGrid& machine);
+}
+#endif
+
 extern "C" {
 
 // One tensor as the reference stores it: per-level pos as inclusive (lo,hi)
@@ -193,7 +200,12 @@ void* ref_run(const char* expr, const char* schedule, const char* grid, const ch
     }
     if (do_execute) {
       double t1 = now();
-      r->result = execute(r->compute, r->tensors, r->machine, residency, parse_exec_mode(mode));
+#ifdef WITH_GPU_EXEC
+      if (std::string(mode) == "gpu")
+        r->result = dspar_gpu::execute_gpu(r->compute, r->tensors, r->machine);
+      else
+#endif
+        r->result = execute(r->compute, r->tensors, r->machine, residency, parse_exec_mode(mode));
       r->exec_seconds = now() - t1;
       r->has_result = true;
       r->stats_json = r->result.stats.to_json();

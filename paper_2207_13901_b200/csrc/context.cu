@@ -170,14 +170,18 @@ static spd_tensor* upload_impl(spd_context* ctx, int order, const int64_t* dims,
         continue;
       }
       L.kind = SPD_COMPRESSED;
-      if (!pos || !pos[l] || (!crd || (!crd[l] && parent > 0)))
-        throw ValidationError("compressed level " + std::to_string(l) + " needs pos and crd");
+      if (!pos || (!pos[l] && parent > 0))
+        throw ValidationError("compressed level " + std::to_string(l) + " needs pos");
       int64_t nnz;
-      if (pairs)
-        nnz = parent == 0 ? 0 : pos[l][2 * (parent - 1) + 1] + 1;
+      if (parent == 0)
+        nnz = 0;
+      else if (pairs)
+        nnz = pos[l][2 * (parent - 1) + 1] + 1;
       else
         nnz = pos[l][parent];
       if (nnz < 0) throw ValidationError("tensor: pos ranges must cover exactly [0, nnz)");
+      if (nnz > 0 && (!crd || !crd[l]))
+        throw ValidationError("compressed level " + std::to_string(l) + " needs crd");
       L.positions = nnz;
       L.rowptr = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (parent + 1));
       L.crd = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (nnz > 0 ? nnz : 1));
@@ -193,6 +197,8 @@ static spd_tensor* upload_impl(spd_context* ctx, int order, const int64_t* dims,
           SPD_CUDA(cudaMemsetAsync(L.rowptr, 0, sizeof(int64_t), ctx->stream));
         }
         dev_free(ctx, tmp);
+      } else if (parent == 0) {
+        SPD_CUDA(cudaMemsetAsync(L.rowptr, 0, sizeof(int64_t), ctx->stream));
       } else {
         SPD_CUDA(cudaMemcpyAsync(L.rowptr, pos[l], sizeof(int64_t) * (parent + 1),
                                  cudaMemcpyHostToDevice, ctx->stream));

@@ -25,6 +25,7 @@ from . import _native as N
 from ._native import SpdError, SpdValidationError, check
 
 DENSE, COMPRESSED = "d", "s"
+CUDA_STREAM_LEGACY = 0x1  # cudaStreamLegacy
 
 
 # ---------------------------------------------------------------- formats ---
@@ -225,6 +226,8 @@ class Context:
             import torch
             torch.cuda.set_device(device)
             stream = torch.cuda.current_stream(device).cuda_stream
+            if stream == 0:  # torch's default is the legacy NULL stream: order with it
+                stream = CUDA_STREAM_LEGACY
         h = C.c_void_p()
         check(N.lib().spd_context_create(device, C.c_void_p(stream) if stream else None, C.byref(h)))
         self.h = h

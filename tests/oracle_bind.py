@@ -17,6 +17,7 @@ ORACLE = os.path.join(ROOT, "oracle")
 PORT_LIB = os.path.join(ORACLE, "liboracle.so")
 REF_LIB = os.path.join(ORACLE, "_ref", "libdspar_ref.so")
 REF_TESTS = os.path.join(ORACLE, "_ref", "dspar_ref_tests")
+GPU_LIB = os.path.join(ORACLE, "_ref", "libdspar_gpu.so")  # reference + ExecMode::Gpu adapter
 
 i64 = C.c_int64
 i64p = C.POINTER(C.c_int64)
@@ -34,7 +35,7 @@ def colours_to_tuples(arr):
 
 
 _port = None
-_ref = None
+_refs = {}
 
 
 def ensure_built(ref=True):
@@ -220,11 +221,11 @@ class ref_tensor_in(C.Structure):
     ]
 
 
-def ref():
-    global _ref
-    if _ref is None:
-        ensure_built(ref=True)
-        L = C.CDLL(REF_LIB)
+def ref(path=REF_LIB):
+    if path not in _refs:
+        if path == REF_LIB:
+            ensure_built(ref=True)
+        L = C.CDLL(path)
         vp = C.c_void_p
         L.ref_run.restype = vp
         L.ref_run.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p, C.c_int,
@@ -251,8 +252,8 @@ def ref():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
-        _ref = L
-    return _ref
+        _refs[path] = L
+    return _refs[path]
 
 
 def _ref_inputs(tensors):
@@ -293,8 +294,8 @@ class RefRun:
     """One reference pipeline run (cli.cpp:72-195 with in-memory tensors)."""
 
     def __init__(self, expr, schedule, grid, out_format, tensors, mode="seq", execute=True,
-                 use_placements=False, out_tdn=None):
-        L = ref()
+                 use_placements=False, out_tdn=None, lib=REF_LIB):
+        L = ref(lib)
         self._arr, self._keep = _ref_inputs(tensors)
         self.h = L.ref_run(expr.encode(), schedule.encode() if schedule else b"", str(grid).encode(),
                            out_format.encode(), out_tdn.encode() if out_tdn else None,

@@ -142,8 +142,8 @@ def test_empty_and_degenerate(ctx, pieces):
     assert st.combines == want["combines"] and st.work == want["work"]
 
 
-@pytest.mark.parametrize("kernel", ["spmv", "spmm"])
-def test_long_hub_rows_cross_many_chunks(ctx, kernel):
+@pytest.mark.parametrize("kernel,N", [("spmv", 1), ("spmm", 8), ("spmm", 32)])
+def test_long_hub_rows_cross_many_chunks(ctx, kernel, N):
     """Rows far longer than a warp chunk exercise the carry chains."""
     from paper_2207_13901_b200.execute import execute
     from paper_2207_13901_b200.host import SparseTensor, parse_format
@@ -158,9 +158,9 @@ def test_long_hub_rows_cross_many_chunks(ctx, kernel):
     if kernel == "spmv":
         t["c"] = K.dense(rng, (m,), "d")
     else:
-        t["C"] = K.dense(rng, (m, 8), "dd")
-    for pieces in (1, 5):
-        want = oracle_execute(kernel, t, "nonzero", pieces)
-        out, st, _ = execute(kernel, t, "nonzero", pieces, ctx)
+        t["C"] = K.dense(rng, (m, N), "dd")
+    for pieces, sched in ((1, "nonzero"), (5, "nonzero"), (3, "row")):
+        want = oracle_execute(kernel, t, sched, pieces)
+        out, st, _ = execute(kernel, t, sched, pieces, ctx)
         assert_close(kernel, out, want["out"], True)
         assert st.combines == want["combines"]

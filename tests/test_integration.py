@@ -1,0 +1,54 @@
+"""The drop-in: the reference's own pipeline (parse -> validate_schedule ->
+plan) with execute() replaced by the ExecMode::Gpu adapter
+(integration/gpu_execute.cpp, built into oracle/_ref/libdspar_gpu.so against
+the reference headers), compared with the reference's execute()."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle_bind as ob
+import spd_kernels as K
+from spd_kernels import KERNELS, OUTPUT, ROW, ref_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gpu_lib():
+    if not os.path.exists(ob.GPU_LIB):
+        pytest.skip("integration library not built (make -C oracle integration)")
+    return ob.GPU_LIB
+
+
+@pytest.mark.parametrize("kernel", list(KERNELS))
+@pytest.mark.parametrize("schedule", ["row", "nonzero"])
+def test_reference_pipeline_with_gpu_execute(gpu_lib, kernel, schedule):
+    if schedule == "nonzero" and KERNELS[kernel]["nonzero"] is None:
+        pytest.skip("position split rejected for union statements")
+    spec = KERNELS[kernel]
+    sched = ROW if schedule == "row" else spec["nonzero"]
+    rng = np.random.default_rng(99)
+    for pieces in (1, 3, 4):
+        t = K.instance(kernel, rng, integers=True)
+        args = (spec["expr"], sched, pieces, spec["formats"][OUTPUT[kernel]], ref_inputs(kernel, t))
+        want = ob.RefRun(*args, mode="seq").ok()
+        got = ob.RefRun(*args, mode="gpu", lib=gpu_lib).ok()
+        wl, wv = want.output()
+        gl, gv = got.output()
+        assert np.array_equal(wv, gv)
+        for (wk, wp, wc), (gk, gp, gc) in zip(wl, gl):
+            assert wk == gk
+            if wk == "s":
+                assert np.array_equal(wp, gp) and np.array_equal(wc, gc)
+        ws, gs = want.stats(), got.stats()
+        assert ws["work"] == gs["work"] and ws["combines"] == gs["combines"]
+        assert ws["imbalance"] == gs["imbalance"]
+
+
+def test_unsupported_statement_is_a_validation_error(gpu_lib):
+    from paper_2207_13901_b200.host import SparseTensor, parse_format
+
+    B = SparseTensor.pack((4, 4), parse_format("ds"), [[0, 1], [2, 3]], [1.0, 2.0])
+    run = ob.RefRun("A(i, j) = B(i, j)", ROW, 2, "ds", {"B": (B, "ds")}, mode="gpu", lib=gpu_lib)
+    assert run.status == 2 and "unsupported on gpu" in run.error
