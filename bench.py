@@ -271,42 +271,63 @@ def main():
         H.partition_nonzero(ctx, B, 1, pieces, host=False)
         H.spmm(ctx, B, C_d, N, A_d, first=first, count=count, pieces=pieces, stats=False)
 
-    stream = torch.cuda.current_stream()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    # Clocks are sampled (nvidia-smi, 100 ms) over a loaded window that
-    # brackets the timed region: >= W warm-up steps and >= 1.5 s of load
-    # before it, 0.5 s after it.
-    with ClockSampler(local) as clocks:
-        clocks.wait_first()
-        t_end, nw = time.time() + 1.5, 0
-        while nw < max(args.warmup, 3) or time.time() < t_end:
-            step()
+    def measure(step_fn, steps, warmup, with_clocks):
+        """W warm-up steps, then exactly `steps` steps bracketed by barrier +
+        synchronize, CUDA events on the launching stream; max over ranks.
+        Clocks are sampled (nvidia-smi, 100 ms) over a loaded window that
+        brackets the timed region (>= 1.5 s of load before it, 0.5 s after)."""
+        stream = torch.cuda.current_stream()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sampler = ClockSampler(local) if with_clocks else None
+        if sampler:
+            sampler.__enter__()
+            sampler.wait_first()
+        t_end, nw = time.time() + (1.5 if with_clocks else 0.0), 0
+        while nw < max(warmup, 3) or time.time() < t_end:
+            step_fn()
             torch.cuda.synchronize()
             nw += 1
-        launches0 = ctx.launches()
+        l0 = ctx.launches()
         ctx.timing(True)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
-        for _ in range(args.steps):
-            step()
+        for _ in range(steps):
+            step_fn()
         ev1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         ctx.timing(False)
-        launches = ctx.launches() - launches0
-        t_end = time.time() + 0.5
-        while time.time() < t_end:
-            step()
-            torch.cuda.synchronize()
-    leaf_ms = ctx.read_timing()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    ms_t = torch.tensor([ms, float(np.mean(leaf_ms)) if leaf_ms else 0.0], dtype=torch.float64, device=dev)
+        nl = ctx.launches() - l0
+        if sampler:
+            t_end = time.time() + 0.5
+            while time.time() < t_end:
+                step_fn()
+                torch.cuda.synchronize()
+            sampler.__exit__(None, None, None)
+        lm = ctx.read_timing()
+        m = ev0.elapsed_time(ev1) / steps
+        t = torch.tensor([m, float(np.mean(lm)) if lm else 0.0], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t[0]), float(t[1]), nl, (sampler.summary() if sampler else None)
+
+    ms, leaf_avg, launches, clock_summary = measure(step, args.steps, args.warmup, True)
+
+    # Secondary: SpMV on the same R-MAT (the metric names SpMV and SpMM).
+    x_d = torch.from_numpy(dense_vals(n, args.seed + 2)).to(dev) if rank == 0 else torch.empty(n, dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms, leaf_avg = float(ms_t[0]), float(ms_t[1])
+        dist.broadcast(x_d, 0)
+    y_d = torch.empty(n, dtype=torch.float64, device=dev)
+
+    def step_spmv():
+        H.partition_nonzero(ctx, B, 1, pieces, host=False)
+        H.spmv(ctx, B, x_d, y_d, first=first, count=count, pieces=pieces, stats=False)
+
+    ms_v, leaf_v, _, _ = measure(step_spmv, args.steps, args.warmup, False)
+    spmv_bytes = 8 * (n + 1) + 16 * nnz + 8 * n + 8 * n
     flops = 2.0 * nnz * N
     value = flops / (ms * 1e-3) / 1e9
 
@@ -335,7 +356,7 @@ def main():
 
     # ---- e2e through the C-ABI with host buffers ----
     e2e = None
-    if args.e2e_steps > 0 and world == 1:
+    if args.e2e_steps > 0:
         e2e = run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, C_d, N)
 
     # ---- CPU baseline (rank 0, N=1) ----
@@ -366,8 +387,15 @@ def main():
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": "k_spmm_walk<1>", "peak_source": peak_src,
                          "bytes_per_launch": per_launch, "leaf_ms": leaf_avg},
-            "clocks": clocks.summary(),
+            "clocks": clock_summary,
             "gpu_launches": launches,
+            "spmv": {"workload": "SpMV a(i)=B(i,j)*c(j) on the same R-MAT, nonzero split",
+                     "value": 2.0 * nnz / (ms_v * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms_v,
+                     "effective_gbs": spmv_bytes / (ms_v * 1e-3) / 1e9,
+                     "roofline": {"bound": "hbm", "achieved": (spmv_bytes / world) / (leaf_v * 1e-3) / 1e9 if leaf_v else None,
+                                  "peak": peak, "unit": "GB/s",
+                                  "frac": (spmv_bytes / world) / (leaf_v * 1e-3) / 1e9 / peak if leaf_v else None,
+                                  "kernel": "k_spmv_nz", "leaf_ms": leaf_v}},
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
@@ -378,54 +406,55 @@ def main():
 
 
 def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, C_d, N):
-    """Per step: host (pinned) -> device upload of this GPU's inputs through
-    spd_tensor_upload (the reference's pos pairs), partition, leaf + combine,
-    device -> host of this GPU's output rows."""
-    import torch.distributed as dist
-
-    # This GPU's share: rows of its colour (plus the whole C, replicated).
-    cols = H.partition_nonzero(ctx, H.DeviceTensor.wrap(ctx, (n, n), H.parse_format("ds"), [rp_d.data_ptr()],
-                                                         [crd_d.data_ptr()], vals_d.data_ptr()), 1, world)
-    mine = cols[rank]
-    r0, r1 = (0, n - 1) if world == 1 else mine.par
-    q0 = int(rp_d[r0].item())
-    q1 = int(rp_d[r1 + 1].item())
-    rows = r1 - r0 + 1
-    # host copies of the slice, pinned; pos as the reference's (lo, hi) pairs
-    rp_h = (rp_d[r0:r1 + 2] - q0).cpu()
-    pairs = torch.stack([rp_h[:-1], rp_h[1:] - 1], dim=1).contiguous().pin_memory()
-    crd_h = crd_d[q0:q1].cpu().pin_memory()
-    vals_h = vals_d[q0:q1].cpu().pin_memory()
-    C_h = C_d.cpu().pin_memory()
-    A_h = torch.empty(rows * N, dtype=torch.float64).pin_memory()
-    C_dev = torch.empty_like(C_d)
-    A_dev = torch.empty(rows * N, dtype=torch.float64, device=dev)
-    fmt = H.parse_format("ds")
+    """The metric through the C-ABI with HOST buffers, every step:
+    H2D of B as the reference stores it (inclusive pos pairs + crd + vals,
+    spd_tensor_upload validates and converts on the GPU) and of this GPU's
+    1/N block of C from pinned memory, NCCL all-gather of C over NVLink
+    (spd_allgather), the partition step, the leaf + boundary combine, and D2H
+    of the output rows this GPU owns."""
     import ctypes as Cc
 
+    import torch.distributed as dist
+
     from paper_2207_13901_b200 import _native as NN
-    dims = (Cc.c_int64 * 2)(rows, n)
+    from paper_2207_13901_b200.distributed import owned_rows
+
+    rp_h = rp_d.cpu()
+    pairs = torch.stack([rp_h[:-1], rp_h[1:] - 1], dim=1).contiguous().pin_memory()
+    crd_h = crd_d.cpu().pin_memory()
+    vals_h = vals_d.cpu().pin_memory()
+    per = (n * N) // world
+    C_h = C_d[rank * per:(rank + 1) * per].cpu().pin_memory()
+    C_dev = torch.empty_like(C_d)
+    A_dev = torch.empty(n * N, dtype=torch.float64, device=dev)
+    fmt = H.parse_format("ds")
+    dims = (Cc.c_int64 * 2)(n, n)
     kinds = (Cc.c_int * 2)(0, 1)
     mo = (Cc.c_int * 2)(0, 1)
     pos_pp = (NN.i64p * 2)(None, Cc.cast(pairs.data_ptr(), NN.i64p))
     crd_pp = (NN.i64p * 2)(None, Cc.cast(crd_h.data_ptr(), NN.i64p))
-    h2d = pairs.numel() * 8 + crd_h.numel() * 8 + vals_h.numel() * 8 + C_h.numel() * 8
-    d2h = A_h.numel() * 8
+    state = {}
 
     def one():
         h = Cc.c_void_p()
         NN.check(NN.lib().spd_tensor_upload(ctx.h, 2, dims, kinds, mo, pos_pp, crd_pp,
                                             Cc.cast(vals_h.data_ptr(), NN.dblp), Cc.byref(h)))
-        Bs = H.DeviceTensor(ctx, h, (rows, n), fmt)
-        C_dev.copy_(C_h, non_blocking=True)
-        # the slice is one colour: a one-piece nonzero split of it
-        H.partition_nonzero(ctx, Bs, 1, 1, host=False)
-        H.spmm(ctx, Bs, C_dev, N, A_dev, first=0, count=1, pieces=1, stats=False)
-        A_h.copy_(A_dev, non_blocking=True)
+        Bs = H.DeviceTensor(ctx, h, (n, n), fmt)
+        C_dev[rank * per:(rank + 1) * per].copy_(C_h, non_blocking=True)
+        if world > 1:
+            ctx.allgather(C_dev, per * 8)
+        cols = H.partition_nonzero(ctx, Bs, 1, world)
+        lo, hi = owned_rows(cols, rp_h.numpy(), "nonzero", n)[rank]
+        H.spmm(ctx, Bs, C_dev, N, A_dev, first=rank if world > 1 else 0, count=1, pieces=world, stats=False)
+        if "A_h" not in state:
+            state["A_h"] = torch.empty(max(hi - lo + 1, 0) * N, dtype=torch.float64).pin_memory()
+        A_h = state["A_h"]
+        if hi >= lo:
+            A_h.copy_(A_dev[lo * N:(hi + 1) * N], non_blocking=True)
         torch.cuda.current_stream().synchronize()
         Bs.close()
 
-    one()  # warm
+    one()  # warm (allocator pool, derived indices of the fresh tensor are rebuilt every step)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -438,11 +467,14 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dt = float(t[0])
+    h2d = pairs.numel() * 8 + crd_h.numel() * 8 + vals_h.numel() * 8 + C_h.numel() * 8
+    d2h = state["A_h"].numel() * 8
     flops = 2.0 * nnz * N
     return {"value": flops / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3,
-            "note": "per GPU: B slice as pos pairs + crd + vals and the replicated C uploaded from "
-                    "pinned host memory through spd_tensor_upload each step; output rows copied back"}
+            "note": "per GPU per step: B uploaded as the reference stores it (pos pairs, crd, vals) "
+                    "through spd_tensor_upload, this GPU's 1/N of C H2D + NCCL all-gather, partition, "
+                    "leaf + combine, owned output rows D2H (max over ranks)"}
 
 
 if __name__ == "__main__":

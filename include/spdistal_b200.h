@@ -105,6 +105,12 @@ int spd_context_synchronize(spd_context* ctx);
 int spd_nccl_unique_id(void* out128);
 int spd_context_init_comm(spd_context* ctx, const void* unique_id128, int rank, int world);
 int spd_context_rank(const spd_context* ctx, int* rank, int* world);
+/* In-place all-gather over the context's communicator (NVLink): rank r's
+ * `bytes_per_rank` bytes at dev_buf + r*bytes_per_rank are gathered into every
+ * rank's dev_buf.  Places a replicated dense operand (x / C / D) from a
+ * block-distributed one -- the only data-path collective besides the
+ * boundary-row exchange of the leaf ops. */
+int spd_allgather(spd_context* ctx, void* dev_buf, int64_t bytes_per_rank);
 
 /* ---- (2) tensors: the coordinate-tree encoding (tensor.hpp:54-114) ------ */
 /* Upload from the reference's own host storage, SparseTensor::from_parts

@@ -116,6 +116,19 @@ struct spd_tensor {
   // Derived device index for 3-level trees: rows -> leaf positions
   // (rp2[rp1[i]]), built on first use by SpMTTKRP.
   int64_t* leaf_rowptr = nullptr;
+  // Compacted non-empty-row views (DCSR-style) of row pointers of this
+  // tensor, built on first use by the leaf kernels (leaf_nz.cuh).
+  struct NzCache {
+    const int64_t* R = nullptr;
+    int64_t* ptr = nullptr;
+    int64_t* id = nullptr;
+    int64_t m = 0;
+  } nz[3];
+  // Leaf crd as int32 with bit 31 = "hot column" (its dense row is among the
+  // most referenced ones that fit in L2), for row-gathering kernels; built on
+  // first use for a given dense-row size (crd32h_rowbytes).
+  int32_t* crd32h = nullptr;
+  int64_t crd32h_rowbytes = 0;
 };
 
 struct spd_context {

@@ -432,6 +432,18 @@ int spd_context_init_comm(spd_context* ctx, const void* unique_id128, int rank, 
   });
 }
 
+int spd_allgather(spd_context* ctx, void* dev_buf, int64_t bytes_per_rank) {
+  return guarded([&] {
+    checked(ctx);
+    if (!ctx->comm) throw ValidationError("spd_allgather needs a communicator (spd_context_init_comm)");
+    if (bytes_per_rank < 0) throw ValidationError("negative size");
+    activate(ctx);
+    char* b = static_cast<char*>(dev_buf);
+    SPD_NCCL(ncclAllGather(b + (size_t)ctx->rank * bytes_per_rank, b, (size_t)bytes_per_rank, ncclUint8,
+                           ctx->comm, ctx->stream));
+  });
+}
+
 int spd_context_rank(const spd_context* ctx, int* rank, int* world) {
   return guarded([&] {
     if (!ctx) throw ValidationError("null spd_context");
@@ -513,6 +525,11 @@ int spd_tensor_destroy(spd_tensor* t) {
       dev_free(ctx, t->vals);
     }
     dev_free(ctx, t->leaf_rowptr);
+    dev_free(ctx, t->crd32h);
+    for (auto& z : t->nz) {
+      dev_free(ctx, z.ptr);
+      dev_free(ctx, z.id);
+    }
     delete t;
   });
 }

@@ -11,6 +11,7 @@
 // colour partials), which north_star allows within 1e-10 relative.
 #include <algorithm>
 #include <cstdlib>
+#include <cub/cub.cuh>
 
 #include "rowwalk.cuh"
 
@@ -254,6 +255,11 @@ __device__ __forceinline__ double2 ld_f64x2_hint(const double* ptr, uint64_t pol
   asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
                : "=d"(v.x), "=d"(v.y)
                : "l"(ptr), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int ld_i32_hint(const int32_t* ptr, uint64_t pol) {
+  int v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(ptr), "l"(pol));
   return v;
 }
 __device__ __forceinline__ int64_t ld_i64_hint(const int64_t* ptr, uint64_t pol) {
@@ -1016,6 +1022,10 @@ __global__ void __launch_bounds__(kBlock) k_spmv_walk(WalkGeom g, const int64_t*
   }
 }
 
+}  // namespace spd
+#include "leaf_nz.cuh"
+namespace spd {
+
 // ---------------------------------------------------------------------------
 // Chunk fixup: sums each cut row's records in chunk order.  Rows cut by the
 // end of a colour become colour tail records; the head chain at the start of
@@ -1140,7 +1150,7 @@ static int spmm32_variant() {
   static int v = [] {
     const char* e = getenv("SPD_SPMM32_VARIANT");
     int x = e ? atoi(e) : 1;
-    return x < 1 || x > 9 ? 1 : x;
+    return x < 1 || x > 13 ? 1 : x;
   }();
   return v;
 }
@@ -1179,6 +1189,126 @@ static void launch_spmm32_bulk(spd_context* ctx, int S, const WalkGeom& g, const
   if (S == 2) launch_bulk_s<2>(ctx, g, crd, vals, C, A, rec, counters);
   else if (S == 3) launch_bulk_s<3>(ctx, g, crd, vals, C, A, rec, counters);
   else launch_bulk_s<4>(ctx, g, crd, vals, C, A, rec, counters);
+}
+
+template <int S>
+static void launch_nz_async(spd_context* ctx, const WalkGeom& g, const NzView& z, const int64_t* crd,
+                            const double* vals, const double* C, double* A, const ChunkRecs& rec,
+                            const int64_t* counters) {
+  const size_t smem = (size_t)kAsyncWarps * S * (kBulkStageBytes + 256);
+  static int grid = 0;
+  if (!grid) {
+    SPD_CUDA(cudaFuncSetAttribute(k_spmm32_nz_async<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmm32_nz_async<S>, kAsyncWarps * 32, smem));
+    grid = ctx->num_sms * (per_sm > 0 ? per_sm : 1);
+  }
+  k_spmm32_nz_async<S><<<grid, kAsyncWarps * 32, smem, ctx->stream>>>(g, z, crd, vals, C, A, rec, counters);
+}
+
+// Compacted non-empty-row view of row pointer R of tensor t (cached on t).
+static NzView nz_view(spd_context* ctx, spd_tensor* t, const int64_t* R, int64_t nrows) {
+  for (auto& e : t->nz)
+    if (e.R == R) return NzView{e.ptr, e.id, e.m};
+  spd_tensor::NzCache* slot = nullptr;
+  for (auto& e : t->nz)
+    if (!e.R) slot = &e;
+  if (!slot) {
+    slot = &t->nz[0];
+    cudaFreeAsync(slot->ptr, ctx->stream);
+    cudaFreeAsync(slot->id, ctx->stream);
+  }
+  cudaStream_t s = ctx->stream;
+  unsigned char* flags = nullptr;
+  int64_t* m_dev = nullptr;
+  SPD_CUDA(cudaMallocAsync((void**)&flags, nrows > 0 ? nrows : 1, s));
+  SPD_CUDA(cudaMallocAsync((void**)&m_dev, sizeof(int64_t), s));
+  SPD_CUDA(cudaMallocAsync((void**)&slot->id, sizeof(int64_t) * (nrows > 0 ? nrows : 1), s));
+  SPD_CUDA(cudaMemsetAsync(m_dev, 0, sizeof(int64_t), s));
+  if (nrows > 0) {
+    k_nz_flags<<<(unsigned)std::min<int64_t>(ceil_div(nrows, 256), ctx->num_sms * 16), 256, 0, s>>>(R, nrows, flags);
+    SPD_CHECK_LAUNCH();
+    cub::CountingInputIterator<int64_t> it(0);
+    size_t bytes = 0;
+    SPD_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, slot->id, m_dev, nrows, s));
+    void* tmp = ctx->scratch[5].reserve(bytes);
+    SPD_CUDA(cub::DeviceSelect::Flagged(tmp, bytes, it, flags, slot->id, m_dev, nrows, s));
+  }
+  SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters + 8, m_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SPD_CUDA(cudaStreamSynchronize(s));
+  slot->m = ctx->pinned_counters[8];
+  SPD_CUDA(cudaMallocAsync((void**)&slot->ptr, sizeof(int64_t) * (slot->m + 1), s));
+  k_nz_ptr<<<(unsigned)std::min<int64_t>(ceil_div(slot->m + 1, 256), ctx->num_sms * 16), 256, 0, s>>>(
+      R, nrows, slot->id, m_dev, slot->ptr);
+  SPD_CHECK_LAUNCH();
+  cudaFreeAsync(flags, s);
+  cudaFreeAsync(m_dev, s);
+  slot->R = R;
+  ctx->launches += 3;
+  return NzView{slot->ptr, slot->id, slot->m};
+}
+
+// Minimum resident CTAs requested for k_spmm32_nz (register budget); tuning knob.
+static int nz_minblocks() {
+  static int v = [] {
+    const char* e = getenv("SPD_NZ_MINB");
+    return e ? atoi(e) : 4;
+  }();
+  return v;
+}
+
+// int32 leaf crd with hot-column bit for dense rows of `rowbytes` (cached on
+// t): the most referenced columns whose rows fit in ~70% of L2 are hot and
+// gathered with L2 evict_last, the rest with evict_first -- an LFU-like L2
+// policy for the power-law column distribution.
+static const int32_t* hot_crd(spd_context* ctx, spd_tensor* t, int64_t rowbytes) {
+  if (t->crd32h && t->crd32h_rowbytes == rowbytes) return t->crd32h;
+  const spd_level_store& L = t->levels.back();
+  const int64_t nnz = L.positions;
+  const int64_t ncols = t->dims[t->mode_order[t->groups.back()[0]]];
+  cudaStream_t s = ctx->stream;
+  int l2 = 0;
+  SPD_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
+  const int64_t k = std::max<int64_t>(1, (int64_t)(0.7 * l2) / rowbytes);
+  int32_t *counts = nullptr, *sorted = nullptr;
+  SPD_CUDA(cudaMallocAsync((void**)&counts, sizeof(int32_t) * (ncols > 0 ? ncols : 1), s));
+  SPD_CUDA(cudaMallocAsync((void**)&sorted, sizeof(int32_t) * (ncols > 0 ? ncols : 1), s));
+  SPD_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (ncols > 0 ? ncols : 1), s));
+  if (!t->crd32h) SPD_CUDA(cudaMallocAsync((void**)&t->crd32h, sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
+  const unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(nnz, 256), 1), ctx->num_sms * 16);
+  if (nnz > 0) {
+    k_col_count<<<grid, 256, 0, s>>>(L.crd, nnz, counts);
+    SPD_CHECK_LAUNCH();
+    size_t bytes = 0;
+    SPD_CUDA(cub::DeviceRadixSort::SortKeysDescending(nullptr, bytes, counts, sorted, ncols, 0, 32, s));
+    void* tmp = ctx->scratch[5].reserve(bytes);
+    SPD_CUDA(cub::DeviceRadixSort::SortKeysDescending(tmp, bytes, counts, sorted, ncols, 0, 32, s));
+    k_crd32h<<<grid, 256, 0, s>>>(L.crd, nnz, counts, sorted, k, ncols, t->crd32h);
+    SPD_CHECK_LAUNCH();
+    ctx->launches += 3;
+  }
+  cudaFreeAsync(counts, s);
+  cudaFreeAsync(sorted, s);
+  t->crd32h_rowbytes = rowbytes;
+  return t->crd32h;
+}
+
+static bool hot_enabled() {
+  static int v = [] {
+    const char* e = getenv("SPD_HOT");
+    return e ? atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
+// Whether an op walks the compacted view (default) -- SPD_NZ=0 selects the
+// direct row-pointer walks (kept for comparison).
+static bool nz_enabled() {
+  static int v = [] {
+    const char* e = getenv("SPD_NZ");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
 }
 
 static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_t count,
@@ -1269,7 +1399,56 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   launches++;
 
   const spd_level_store& leaf = B->levels[nl - 1];
+  const bool use_nz = nz_enabled() && (a.op == Op::SpMV || a.op == Op::SpTTV || (spmm32 && (variant == 1 || variant >= 10)));
+  NzView z{nullptr, nullptr, 0};
+  if (use_nz) {
+    z = nz_view(ctx, const_cast<spd_tensor*>(B), g.R, g.nrows);
+    static int zgrid = 0;
+    if (!zgrid) zgrid = occupancy_grid(ctx, k_zero_empty);
+    k_zero_empty<<<zgrid, kBlock, 0, s>>>(g.R, g.nrows, (const DevColor*)ctx->colors_dev.ptr, first, count,
+                                         a.W, a.out);
+    SPD_CHECK_LAUNCH();
+    launches++;
+  }
   leaf_timing_begin(ctx);
+  if (use_nz) {
+    if (a.op == Op::SpMM && variant >= 10) {
+      if (variant == 10) launch_nz_async<2>(ctx, g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      else if (variant == 11) launch_nz_async<3>(ctx, g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      else if (variant == 12) launch_nz_async<4>(ctx, g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      else launch_nz_async<6>(ctx, g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+    } else if (a.op == Op::SpMM && hot_enabled()) {
+      const int32_t* h = hot_crd(ctx, const_cast<spd_tensor*>(B), 256);
+      static int grid = 0;
+      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, true>);
+      k_spmm32_nz<4, 4, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, h, B->vals, a.x, a.out, rec,
+                                                      col.counters);
+    } else if (a.op == Op::SpMM && nz_minblocks() == 83) {
+      static int grid = 0;
+      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<8, 3, false>);
+      k_spmm32_nz<8, 3, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
+                                                       col.counters);
+    } else if (a.op == Op::SpMM && nz_minblocks() == 84) {
+      static int grid = 0;
+      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<8, 4, false>);
+      k_spmm32_nz<8, 4, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
+                                                       col.counters);
+    } else if (a.op == Op::SpMM && nz_minblocks() == 4) {
+      static int grid = 0;
+      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, false>);
+      k_spmm32_nz<4, 4, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
+                                                       col.counters);
+    } else if (a.op == Op::SpMM) {
+      static int grid = 0;
+      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 1, false>);
+      k_spmm32_nz<4, 1, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
+                                                       col.counters);
+    } else {
+      static int grid = 0;
+      if (!grid) grid = occupancy_grid(ctx, k_spmv_nz);
+      k_spmv_nz<<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+    }
+  } else
   switch (a.op) {
     case Op::SpMV:
     case Op::SpTTV: {

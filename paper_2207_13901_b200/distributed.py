@@ -1,0 +1,71 @@
+"""Host-side plumbing for one process per GPU (torch.distributed bootstrap).
+
+The data path between GPUs is inside libspdistal_b200.so (NCCL all-gather of
+boundary records, rowwalk.cuh); this module only
+  * bootstraps the backend's NCCL communicator from a torch.distributed group
+    (the 128-byte ncclUniqueId travels over whatever backend the group uses);
+  * states the output-ownership rule the device code applies (k_setup,
+    leaf_rows.cu): colour c stores rows W_c, and the W_c tile [0, rows);
+  * assembles a distributed dense output on one rank for checking/download.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def init_comm(ctx, dist, rank: int, world: int, device=None):
+    """Create the backend communicator of `ctx` for this rank."""
+    import torch
+
+    from .host import Context
+
+    dev = device if device is not None else "cpu"
+    uid = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        uid.copy_(torch.frombuffer(bytearray(Context.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(uid, 0)
+    ctx.init_comm(bytes(uid.cpu().numpy().tobytes()), rank, world)
+
+
+def owned_rows(colours, rowptr, schedule: str, nrows: int):
+    """W_c for every colour: its row block for a universe ("row") split; for a
+    nonzero split, from the first row starting inside the colour up to the row
+    before the next colour's first such row (the first non-empty colour starts
+    at row 0; with no positions at all the last colour owns every row).
+    `colours` are host.Colour-like objects with `.q` and `.top` spans."""
+    P = len(colours)
+    if schedule == "row":
+        return [tuple(c.top) for c in colours]
+    rowptr = np.asarray(rowptr)
+    starts = []
+    for c in colours:
+        lo, hi = c.q
+        if lo > hi:
+            starts.append(None)
+            continue
+        o = int(np.searchsorted(rowptr, lo, side="right") - 1)
+        starts.append(o if rowptr[o] == lo else o + 1)
+    W = [None] * P
+    nxt, first = nrows, None
+    for c in range(P - 1, -1, -1):
+        if starts[c] is None:
+            W[c] = (nxt, nxt - 1)
+        else:
+            W[c] = (starts[c], nxt - 1)
+            nxt = starts[c]
+            first = c
+    if first is not None:
+        W[first] = (0, W[first][1])
+    else:
+        W[P - 1] = (0, nrows - 1)
+    return W
+
+
+def assemble(parts, W, width: int, nrows: int):
+    """Dense output from every rank's (full-size) buffer, keeping W_c rows of
+    rank c."""
+    out = np.zeros((nrows, width))
+    for r, (lo, hi) in enumerate(W):
+        if lo <= hi:
+            out[lo:hi + 1] = np.asarray(parts[r]).reshape(nrows, width)[lo:hi + 1]
+    return out

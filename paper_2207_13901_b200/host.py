@@ -239,6 +239,10 @@ class Context:
         buf = C.create_string_buffer(unique_id, 128)
         check(N.lib().spd_context_init_comm(self.h, buf, rank, world))
 
+    def allgather(self, dev_buf, bytes_per_rank: int):
+        """In-place NCCL all-gather of a device buffer (spd_allgather)."""
+        check(N.lib().spd_allgather(self.h, _ptr(dev_buf), int(bytes_per_rank)))
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = C.create_string_buffer(128)
