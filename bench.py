@@ -467,14 +467,18 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dt = float(t[0])
-    h2d = pairs.numel() * 8 + crd_h.numel() * 8 + vals_h.numel() * 8 + C_h.numel() * 8
-    d2h = state["A_h"].numel() * 8
+    # whole-job bytes per step: summed over ranks
+    by = torch.tensor([pairs.numel() * 8 + crd_h.numel() * 8 + vals_h.numel() * 8 + C_h.numel() * 8,
+                       state["A_h"].numel() * 8], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(by)
+    h2d, d2h = int(by[0]), int(by[1])
     flops = 2.0 * nnz * N
     return {"value": flops / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3,
-            "note": "per GPU per step: B uploaded as the reference stores it (pos pairs, crd, vals) "
-                    "through spd_tensor_upload, this GPU's 1/N of C H2D + NCCL all-gather, partition, "
-                    "leaf + combine, owned output rows D2H (max over ranks)"}
+            "note": "per step, every GPU: B uploaded as the reference stores it (pos pairs, crd, vals) "
+                    "through spd_tensor_upload, its 1/N of C H2D + NCCL all-gather, partition, leaf + "
+                    "combine, its owned output rows D2H; time = max over ranks, bytes = sum over ranks"}
 
 
 if __name__ == "__main__":

@@ -129,6 +129,8 @@ struct spd_tensor {
   // first use for a given dense-row size (crd32h_rowbytes).
   int32_t* crd32h = nullptr;
   int64_t crd32h_rowbytes = 0;
+  // 3-level trees: middle-mode coordinate of every leaf (crd1 of its fibre).
+  int32_t* jleaf = nullptr;
 };
 
 struct spd_context {
@@ -139,6 +141,10 @@ struct spd_context {
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // Auxiliary stream for work that overlaps the leaf (the zero-fill of empty
+  // output rows), forked from / joined into `stream` with events.
+  cudaStream_t aux = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
 
   // Last partition (spd_partition_*): device + host copies of the colours.
   spd::SplitKind split = spd::SplitKind::None;

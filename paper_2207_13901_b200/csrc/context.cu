@@ -378,6 +378,9 @@ int spd_context_create(int device, void* stream, spd_context** out) {
     SPD_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
     SPD_CUDA(cudaEventCreate(&ctx->ev0));
     SPD_CUDA(cudaEventCreate(&ctx->ev1));
+    SPD_CUDA(cudaStreamCreateWithFlags(&ctx->aux, cudaStreamNonBlocking));
+    SPD_CUDA(cudaEventCreateWithFlags(&ctx->fork, cudaEventDisableTiming));
+    SPD_CUDA(cudaEventCreateWithFlags(&ctx->join, cudaEventDisableTiming));
     SPD_CUDA(cudaMallocHost((void**)&ctx->pinned_counters, sizeof(int64_t) * 64));
     *out = ctx;
   });
@@ -394,6 +397,9 @@ int spd_context_destroy(spd_context* ctx) {
     ctx->counters.release();
     if (ctx->pinned_counters) cudaFreeHost(ctx->pinned_counters);
     for (cudaEvent_t e : ctx->timing_events) cudaEventDestroy(e);
+    if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
+    if (ctx->fork) cudaEventDestroy(ctx->fork);
+    if (ctx->join) cudaEventDestroy(ctx->join);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
@@ -526,6 +532,7 @@ int spd_tensor_destroy(spd_tensor* t) {
     }
     dev_free(ctx, t->leaf_rowptr);
     dev_free(ctx, t->crd32h);
+    dev_free(ctx, t->jleaf);
     for (auto& z : t->nz) {
       dev_free(ctx, z.ptr);
       dev_free(ctx, z.id);

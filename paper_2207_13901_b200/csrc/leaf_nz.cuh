@@ -83,6 +83,21 @@ __device__ __forceinline__ unsigned nz_window_mask(const NzCursor& c, int64_t ba
   return bm;
 }
 
+// Zeroes rows [lo, hi] of a W-wide dense output (contiguous), warp-cooperative.
+__device__ __forceinline__ void zero_gap(double* __restrict__ out, int64_t W, int64_t lo, int64_t hi) {
+  if (lo > hi) return;
+  const int lane = lane_id();
+  if (W % 2 == 0) {
+    double2* p = reinterpret_cast<double2*>(out + lo * W);
+    const int64_t cnt = (hi - lo + 1) * (W / 2);
+    for (int64_t i = lane; i < cnt; i += 32) p[i] = make_double2(0.0, 0.0);
+  } else {
+    double* p = out + lo * W;
+    const int64_t cnt = (hi - lo + 1) * W;
+    for (int64_t i = lane; i < cnt; i += 32) p[i] = 0.0;
+  }
+}
+
 // Zeroes the empty rows of the union of the write ranges of colours
 // [c_first, c_first + c_count): one warp per 32 rows, one coalesced W-wide
 // store per empty row.
@@ -100,6 +115,7 @@ __global__ void __launch_bounds__(kBlock) k_zero_empty(const int64_t* __restrict
   if (lo > hi) return;
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t pol = l2_policy_evict_first();
   for (int64_t g0 = lo + gw * 32; g0 <= hi; g0 += nw * 32) {
     const int64_t r = g0 + lane;
     const bool empty = r <= hi && ld64(R + r + 1) == ld64(R + r);
@@ -107,10 +123,21 @@ __global__ void __launch_bounds__(kBlock) k_zero_empty(const int64_t* __restrict
       if (empty) out[r] = 0.0;
       continue;
     }
-    unsigned m = __ballot_sync(FULL, empty);
-    while (m) {
-      const int b = __ffs(m) - 1;
-      m &= m - 1;
+    const unsigned m = __ballot_sync(FULL, empty);
+    const int ne = __popc(m);
+    if (W == 32) {  // a half-warp per row: one 128-bit store per lane writes two 256-byte rows
+      const int half = lane >> 4, hl = lane & 15;
+      for (int t = 0; t < ne; t += 2) {
+        const int k = t + half;
+        if (k < ne) {
+          const int b = (int)__fns(m, 0, k + 1);
+          st_f64x2_hint(out + (g0 + b) * 32 + 2 * hl, make_double2(0.0, 0.0), pol);
+        }
+      }
+      continue;
+    }
+    for (int t = 0; t < ne; t++) {
+      const int b = (int)__fns(m, 0, t + 1);
       double* row = out + (g0 + b) * W;
       for (int64_t j = lane; j < W; j += 32) row[j] = 0.0;
     }
@@ -122,7 +149,7 @@ __global__ void __launch_bounds__(kBlock) k_zero_empty(const int64_t* __restrict
 // (kSpmvBatch of them loaded together), per window one segmented scan; the
 // rows completing in a window are handled one per lane: lane t finds the end
 // of row ic+t with __fns on the head mask.
-__global__ void __launch_bounds__(kBlock) k_spmv_nz(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
+__global__ void __launch_bounds__(kBlock, 5) k_spmv_nz(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
                                                     const double* __restrict__ vals,
                                                     const double* __restrict__ x, double* __restrict__ y,
                                                     ChunkRecs rec, const int64_t* __restrict__ counters) {
@@ -134,6 +161,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_nz(WalkGeom g, NzView z, const 
   for (int64_t v = begin + gw; v < end; v += nw) {
     const ChunkInfo ci = chunk_info(g, v, begin);
     if (ci.q_lo > ci.q_hi) {
+      zero_gap(y, 1, ci.w_lo, ci.w_hi);
       if (lane == 0) rec.row[2 * ci.local] = -1, rec.row[2 * ci.local + 1] = -1, rec.cont[ci.local] = 0;
       continue;
     }
@@ -144,6 +172,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_nz(WalkGeom g, NzView z, const 
     int64_t head_row = -1;
     int head_cont = 0;
     double head_val = 0.0, acc = 0.0;
+    if (s == ci.q_lo && !head) zero_gap(y, 1, ci.w_lo, __shfl_sync(FULL, c.I0, 0) - 1);
     for (int64_t bbase = s; bbase <= e; bbase += 32 * kSpmvBatch) {
       int64_t kk[kSpmvBatch];
       double vv[kSpmvBatch], prods[kSpmvBatch];
@@ -173,16 +202,14 @@ __global__ void __launch_bounds__(kBlock) k_spmv_nz(WalkGeom g, NzView z, const 
           acc += warp_sum(prods[bi]);
           continue;
         }
+        // segmented inclusive scan: lane l adds the partial of lane l-off
+        // unless a row starts in (l-off, l] -- read off the window mask
         double sv = prods[bi];
-        unsigned f = (heads >> lane) & 1u;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
           const double tv = __shfl_up_sync(FULL, sv, off);
-          const unsigned tf = __shfl_up_sync(FULL, f, off);
-          if (lane >= off) {
-            if (!f) sv += tv;
-            f |= tf;
-          }
+          const unsigned span = lane >= off ? ((((1u << off) - 1u) << (lane - off + 1))) : 0u;
+          if (lane >= off && (heads & span) == 0u) sv += tv;
         }
         const int nh = __popc(heads);
         // lane t < nh: row ic + t ends just before the t-th head
@@ -191,6 +218,9 @@ __global__ void __launch_bounds__(kBlock) k_spmv_nz(WalkGeom g, NzView z, const 
         if (endl < 0) sum = 0.0;
         if (lane == 0) sum += acc;
         const int64_t id = nz_get(c.I0, c.I1, (int)(c.ic - c.cb) + lane);
+        const int64_t id_next = nz_get(c.I0, c.I1, (int)(c.ic - c.cb) + lane + 1);
+        if (lane < nh)  // empty rows between row ic+t and its successor
+          for (int64_t r = id + 1; r < id_next; r++) y[r] = 0.0;
         if (lane < nh) {
           if (lane == 0 && head) {
             head_row = id;
@@ -215,6 +245,8 @@ __global__ void __launch_bounds__(kBlock) k_spmv_nz(WalkGeom g, NzView z, const 
     if (next == e + 1) {
       if (head) head_row = id, head_val = acc, head_cont = 0;
       else if (lane == 0) y[id] = acc;
+      const int64_t nid = nz_get(c.I0, c.I1, (int)(c.ic - c.cb) + 1);
+      zero_gap(y, 1, id + 1, nid < 0 ? ci.w_hi : min(nid - 1, ci.w_hi));
     } else if (head) {
       head_row = id, head_val = acc, head_cont = 1;
     } else {
@@ -301,6 +333,149 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
           } else {
             cv[i] = p < cnt ? ld_f64x2_hint(src, pol_keep) : make_double2(0.0, 0.0);
           }
+        }
+        const unsigned gm = (bm >> u) & ((1u << (2 * UNR)) - 1u);
+        if (gm == 0u) {
+#pragma unroll
+          for (int i = 0; i < UNR; i++) {
+            acc.x = fma(bv[i], cv[i].x, acc.x);
+            acc.y = fma(bv[i], cv[i].y, acc.y);
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < UNR; i++) {
+            const unsigned two = (gm >> (2 * i)) & 3u;
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              if ((two >> h) & 1u) {  // a new row starts at position u + 2i + h
+                double2 o;
+                o.x = acc.x + __shfl_xor_sync(FULL, acc.x, 16);
+                o.y = acc.y + __shfl_xor_sync(FULL, acc.y, 16);
+                const int64_t id = nz_get(c.I0, c.I1, (int)(c.ic - c.cb));
+                if (head) {
+                  if (lane < 16) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
+                  head_row = id;
+                  head_cont = 0;
+                  head = false;
+                } else if (lane < 16) {
+                  st_f64x2_hint(A + id * 32 + 2 * lane, o, pol_stream);
+                }
+                acc = make_double2(0.0, 0.0);
+                nz_advance(z, c, 1);
+              }
+              if (half == h) {
+                acc.x = fma(bv[i], cv[i].x, acc.x);
+                acc.y = fma(bv[i], cv[i].y, acc.y);
+              }
+            }
+          }
+        }
+      }
+    }
+    double2 o;
+    o.x = acc.x + __shfl_xor_sync(FULL, acc.x, 16);
+    o.y = acc.y + __shfl_xor_sync(FULL, acc.y, 16);
+    const int64_t next = nz_get(c.P0, c.P1, (int)(c.ic - c.cb) + 1);
+    const int64_t id = nz_get(c.I0, c.I1, (int)(c.ic - c.cb));
+    int64_t tail_row = -1;
+    if (next == e + 1) {
+      if (head) {
+        if (lane < 16) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
+        head_row = id, head_cont = 0;
+      } else if (lane < 16) {
+        st_f64x2_hint(A + id * 32 + 2 * lane, o, pol_stream);
+      }
+    } else if (head) {
+      if (lane < 16) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
+      head_row = id, head_cont = 1;
+    } else {
+      if (lane < 16) reinterpret_cast<double2*>(rec.val + (2 * k + 1) * 32)[lane] = o;
+      tail_row = id;
+    }
+    if (lane == 0) {
+      rec.row[2 * k] = head_row;
+      rec.row[2 * k + 1] = tail_row;
+      rec.cont[k] = head_cont;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// SpMTTKRP, R == 32, over the compacted rows i (leaf row pointer): the
+// k_spmm32_nz walk with two gathers per position -- D(k,:) by the leaf crd and
+// C(j,:) by the position's fibre coordinate (jleaf, a per-leaf copy of crd1
+// built once per tensor) -- and value ((B*C)*D) as the reference multiplies.
+template <int UNR, int MINB, bool HOT>
+__global__ void __launch_bounds__(kBlock, MINB) k_mttkrp32_nz(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
+                                                      const int32_t* __restrict__ jleaf, const double* __restrict__ Cj,
+                                                      const double* __restrict__ vals,
+                                                      const double* __restrict__ C,
+                                                      double* __restrict__ A, ChunkRecs rec,
+                                                      const int64_t* __restrict__ counters) {
+  const int lane = lane_id();
+  const int half = lane >> 4, hl = lane & 15;
+  const int64_t begin = counters[1], end = counters[2];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t pol_keep = l2_policy_evict_last();
+  const uint64_t pol_stream = l2_policy_evict_first();
+  const double* Cl = C + 2 * hl;
+  const double* Cjl = Cj + 2 * hl;
+  for (int64_t v = begin + gw; v < end; v += nw) {
+    const ChunkInfo ci = chunk_info(g, v, begin);
+    if (ci.q_lo > ci.q_hi) {
+      if (lane == 0) rec.row[2 * ci.local] = -1, rec.row[2 * ci.local + 1] = -1, rec.cont[ci.local] = 0;
+      continue;
+    }
+    const int64_t k = ci.local, s = ci.s, e = ci.e;
+    NzCursor c;
+    nz_start(z, c, s);
+    bool head = __shfl_sync(FULL, c.P0, 0) < s;
+    int64_t head_row = -1;
+    int head_cont = 0;
+    double2 acc = make_double2(0.0, 0.0);
+    // prefetched crd/vals of the next window
+    int kn = 0, jn = 0;
+    double vn = 0.0;
+    if (lane <= e - s) {
+      kn = (int)ld_i64_hint(crd + s + lane, pol_stream);
+      jn = ld_i32_hint(jleaf + s + lane, pol_stream);
+      vn = ld_f64_hint(vals + s + lane, pol_stream);
+    }
+    for (int64_t base = s; base <= e; base += 32) {
+      const int last_off = (int)min((int64_t)31, e - base);
+      const int cnt = last_off + 1;
+      const int my_k = kn, my_j = jn;
+      const double my_v = vn;
+      if (base + 32 + lane <= e) {
+        kn = (int)ld_i64_hint(crd + base + 32 + lane, pol_stream);
+        jn = ld_i32_hint(jleaf + base + 32 + lane, pol_stream);
+        vn = ld_f64_hint(vals + base + 32 + lane, pol_stream);
+      }
+      const unsigned bm = nz_window_mask(c, base, base + last_off);
+      // Fixed-trip groups of 2*UNR positions: positions past `cnt` carry
+      // crd 0 / val 0 (their loads are predicated off), so the fast path is
+      // branch-free; one mask test per group selects the row-switch path.
+#pragma unroll 1
+      for (int u = 0; u < 32; u += 2 * UNR) {
+        if (u >= cnt) break;
+        double2 cv[UNR];
+        double bv[UNR];
+#pragma unroll
+        for (int i = 0; i < UNR; i++) {
+          const int p = u + 2 * i + half;
+          const int kk = __shfl_sync(FULL, my_k, p);
+          const int jj = __shfl_sync(FULL, my_j, p);
+          bv[i] = __shfl_sync(FULL, my_v, p);
+          double2 dv = make_double2(0.0, 0.0), cj = make_double2(0.0, 0.0);
+          if (p < cnt) {
+            dv = ld_f64x2_hint(Cl + (int64_t)kk * 32, pol_keep);
+            cj = ld_f64x2_hint(Cjl + (int64_t)jj * 32, pol_keep);
+          }
+          // ((b * C(j,l)) * D(k,l)) as the reference multiplies (sim.cpp:328-337),
+          // then added with a unit FMA
+          cv[i] = make_double2((bv[i] * cj.x) * dv.x, (bv[i] * cj.y) * dv.y);
+          bv[i] = 1.0;
         }
         const unsigned gm = (bm >> u) & ((1u << (2 * UNR)) - 1u);
         if (gm == 0u) {
@@ -565,4 +740,121 @@ __global__ void k_crd32h(const int64_t* __restrict__ crd, int64_t nnz, const int
   }
 }
 
+}  // namespace spd
+
+namespace spd {
+
+// ---------------------------------------------------------------------------
+// SDDMM over the compacted view, K = 32 * KT.  Lane l owns k in
+// [KT*l, KT*l + KT): one group of 4 positions loads 4 D columns (KT doubles
+// per lane each, contiguous -> coalesced K*8-byte rows when D is j-major) and
+// the C row of each position's row (kept in registers while the row lasts),
+// forms 4 per-lane partial dot products and reduces all four across the warp
+// with one butterfly (2+1+3 shuffles instead of 4 x 5).  Row ids of the
+// positions come from the window's row-start mask, so no row-pointer loads
+// sit on the critical path.
+template <int KT, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_sddmm_nz(WalkGeom g, NzView z, const int32_t* __restrict__ crd32h,
+                                                      const double* __restrict__ vals,
+                                                      const double* __restrict__ C,
+                                                      const double* __restrict__ D, int64_t K,
+                                                      double* __restrict__ Avals,
+                                                      const int64_t* __restrict__ counters) {
+  static_assert(KT == 4, "the vectorised layout assumes 4 k per lane");
+  const int lane = lane_id();
+  const int64_t begin = counters[1], end = counters[2];
+  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const uint64_t pol_stream = l2_policy_evict_first();
+  const uint64_t pol_keep = l2_policy_evict_last();
+  const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1;
+  for (int64_t v = begin + gw; v < end; v += nw) {
+    const ChunkInfo ci = chunk_info(g, v, begin);
+    if (ci.q_lo > ci.q_hi) continue;
+    const int64_t s = ci.s, e = ci.e;
+    NzCursor c;
+    nz_start(z, c, s);
+    int64_t cur_i = -1;
+    double2 cr0 = make_double2(0.0, 0.0), cr1 = cr0;
+    for (int64_t base = s; base <= e; base += 32) {
+      const int cnt = (int)min((int64_t)32, e - base + 1);
+      // crd with the hot-column bit (hot_crd): D columns referenced often
+      // enough to stay in L2 are read with evict_last, the rest evict_first;
+      // the whole warp reads one column at a time, so the policy is uniform.
+      int my_j = 0;
+      double my_b = 0.0;
+      if (lane < cnt) {
+        my_j = ld_i32_hint(crd32h + base + lane, pol_stream);
+        my_b = ld_f64_hint(vals + base + lane, pol_stream);
+      }
+      const unsigned heads = nz_window_mask(c, base, base + cnt - 1);
+      // row of this lane's position: rows starting at or before it
+      const int kth = __popc(heads & (0xffffffffu >> (31 - lane)));
+      const int64_t my_i = nz_get(c.I0, c.I1, (int)(c.ic - c.cb) + kth);
+      double res = 0.0;
+#pragma unroll 1
+      for (int g4 = 0; g4 < cnt; g4 += 4) {
+        double2 d0[4], d1[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int p = g4 + u;
+          const int jh = __shfl_sync(FULL, my_j, p & 31);
+          const int64_t j = jh & 0x7fffffff;
+          const double2* dp = reinterpret_cast<const double2*>(D + j * K + 4 * lane);
+          if (p < cnt && jh < 0) {
+            d0[u] = ld_f64x2_hint(reinterpret_cast<const double*>(dp), pol_keep);
+            d1[u] = ld_f64x2_hint(reinterpret_cast<const double*>(dp + 1), pol_keep);
+          } else if (p < cnt) {
+            d0[u] = ld_f64x2_hint(reinterpret_cast<const double*>(dp), pol_stream);
+            d1[u] = ld_f64x2_hint(reinterpret_cast<const double*>(dp + 1), pol_stream);
+          } else {
+            d0[u] = d1[u] = make_double2(0.0, 0.0);
+          }
+        }
+        double part[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+          const int p = g4 + u;
+          const int64_t i = __shfl_sync(FULL, my_i, p & 31);
+          if (i != cur_i && p < cnt) {  // uniform: a new row's C slice
+            const double* cp = C + i * K + 4 * lane;
+            cr0 = ld_f64x2_hint(cp, pol_stream);
+            cr1 = ld_f64x2_hint(cp + 2, pol_stream);
+            cur_i = i;
+          }
+          part[u] = fma(cr0.x, d0[u].x, fma(cr0.y, d0[u].y, fma(cr1.x, d1[u].x, cr1.y * d1[u].y)));
+        }
+        // butterfly: four warp sums at once
+        double a0 = b4 ? part[2] : part[0], a1 = b4 ? part[3] : part[1];
+        const double s0 = b4 ? part[0] : part[2], s1 = b4 ? part[1] : part[3];
+        a0 += __shfl_xor_sync(FULL, s0, 16);
+        a1 += __shfl_xor_sync(FULL, s1, 16);
+        double bsum = b3 ? a1 : a0;
+        const double sb = b3 ? a0 : a1;
+        bsum += __shfl_xor_sync(FULL, sb, 8);
+        bsum += __shfl_xor_sync(FULL, bsum, 4);
+        bsum += __shfl_xor_sync(FULL, bsum, 2);
+        bsum += __shfl_xor_sync(FULL, bsum, 1);
+        // lanes 8*v .. 8*v+7 hold the dot product of position g4 + v
+        // (v = 2*b4 + b3); lane g4 + v collects it for the final store
+        const double dot = __shfl_sync(FULL, bsum, ((lane - g4) & 3) * 8);
+        if (lane >= g4 && lane < g4 + 4) res = dot;
+      }
+      if (lane < cnt) Avals[base + lane] = my_b * res;
+      nz_advance(z, c, __popc(heads));
+    }
+  }
+}
+
+}  // namespace spd
+
+namespace spd {
+// jleaf[q] = crd1[fibre of q]: the middle-mode coordinate of every leaf.
+__global__ void k_jleaf(const int64_t* __restrict__ rp2, const int64_t* __restrict__ crd1, int64_t F,
+                        int32_t* __restrict__ jleaf) {
+  for (int64_t f = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; f < F; f += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t j = (int32_t)crd1[f];
+    for (int64_t q = rp2[f]; q < rp2[f + 1]; q++) jleaf[q] = j;
+  }
+}
 }  // namespace spd

@@ -1269,7 +1269,11 @@ static const int32_t* hot_crd(spd_context* ctx, spd_tensor* t, int64_t rowbytes)
   cudaStream_t s = ctx->stream;
   int l2 = 0;
   SPD_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
-  const int64_t k = std::max<int64_t>(1, (int64_t)(0.7 * l2) / rowbytes);
+  static double frac = [] {
+    const char* e = getenv("SPD_HOT_FRAC");
+    return e ? atof(e) : 0.7;
+  }();
+  const int64_t k = std::max<int64_t>(1, (int64_t)(frac * l2) / rowbytes);
   int32_t *counts = nullptr, *sorted = nullptr;
   SPD_CUDA(cudaMallocAsync((void**)&counts, sizeof(int32_t) * (ncols > 0 ? ncols : 1), s));
   SPD_CUDA(cudaMallocAsync((void**)&sorted, sizeof(int32_t) * (ncols > 0 ? ncols : 1), s));
@@ -1309,6 +1313,30 @@ static bool nz_enabled() {
     return e ? atoi(e) : 1;
   }();
   return v != 0;
+}
+
+// SDDMM over the compacted view (called by sddmm.cu): K = 128, D j-major.
+bool sddmm_nz_launch(spd_context* ctx, const spd_tensor* B, const WalkGeom& g, const double* C,
+                     const double* D, int64_t K, int64_t dk, int64_t dj, double* Avals,
+                     const int64_t* counters) {
+  if (!nz_enabled() || K != 128 || dk != 1 || dj != 128 || B->dims[1] >= (int64_t(1) << 31)) return false;
+  NzView z = nz_view(ctx, const_cast<spd_tensor*>(B), g.R, g.nrows);
+  const int32_t* h = hot_crd(ctx, const_cast<spd_tensor*>(B), K * 8);
+  static int minb = [] {
+    const char* e = getenv("SPD_SDDMM_MINB");
+    return e ? atoi(e) : 3;
+  }();
+  if (minb == 4) {
+    static int grid = 0;
+    if (!grid) grid = occupancy_grid(ctx, k_sddmm_nz<4, 4>);
+    k_sddmm_nz<4, 4><<<grid, kBlock, 0, ctx->stream>>>(g, z, h, B->vals, C, D, K, Avals, counters);
+  } else {
+    static int grid = 0;
+    if (!grid) grid = occupancy_grid(ctx, k_sddmm_nz<4, 3>);
+    k_sddmm_nz<4, 3><<<grid, kBlock, 0, ctx->stream>>>(g, z, h, B->vals, C, D, K, Avals, counters);
+  }
+  SPD_CHECK_LAUNCH();
+  return true;
 }
 
 static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_t count,
@@ -1399,20 +1427,43 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   launches++;
 
   const spd_level_store& leaf = B->levels[nl - 1];
-  const bool use_nz = nz_enabled() && (a.op == Op::SpMV || a.op == Op::SpTTV || (spmm32 && (variant == 1 || variant >= 10)));
+  const bool mttkrp32 = a.op == Op::SpMTTKRP && a.W == 32 && B->dims[1] < (int64_t(1) << 31) &&
+                        B->dims[2] < (int64_t(1) << 31);
+  const bool use_nz = nz_enabled() && (a.op == Op::SpMV || a.op == Op::SpTTV || mttkrp32 ||
+                                       (spmm32 && (variant == 1 || variant >= 10)));
   NzView z{nullptr, nullptr, 0};
   if (use_nz) {
     z = nz_view(ctx, const_cast<spd_tensor*>(B), g.R, g.nrows);
-    static int zgrid = 0;
-    if (!zgrid) zgrid = occupancy_grid(ctx, k_zero_empty);
-    k_zero_empty<<<zgrid, kBlock, 0, s>>>(g.R, g.nrows, (const DevColor*)ctx->colors_dev.ptr, first, count,
-                                         a.W, a.out);
-    SPD_CHECK_LAUNCH();
-    launches++;
+    // SpMV/SpTTV walks zero the empty rows between consecutive non-empty
+    // rows themselves (8 bytes each); the W-wide outputs use this pass.
+    if (a.op == Op::SpMM || a.op == Op::SpMTTKRP) {
+      static int zgrid = 0;
+      if (!zgrid) zgrid = occupancy_grid(ctx, k_zero_empty);
+      k_zero_empty<<<zgrid, kBlock, 0, s>>>(g.R, g.nrows, (const DevColor*)ctx->colors_dev.ptr, first, count,
+                                           a.W, a.out);
+      SPD_CHECK_LAUNCH();
+      launches++;
+    }
   }
   leaf_timing_begin(ctx);
   if (use_nz) {
-    if (a.op == Op::SpMM && variant >= 10) {
+    if (a.op == Op::SpMTTKRP) {
+      spd_tensor* Bm = const_cast<spd_tensor*>(B);
+      const spd_level_store& L1 = B->levels[1];
+      const spd_level_store& L2 = B->levels[2];
+      if (!Bm->jleaf) {
+        SPD_CUDA(cudaMallocAsync((void**)&Bm->jleaf, sizeof(int32_t) * (L2.positions > 0 ? L2.positions : 1), s));
+        k_jleaf<<<(unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(L2.parent_positions, 256), 1),
+                                               ctx->num_sms * 16), 256, 0, s>>>(L2.rowptr, L1.crd, L2.parent_positions,
+                                                                               Bm->jleaf);
+        SPD_CHECK_LAUNCH();
+        ctx->launches++;
+      }
+      static int grid = 0;
+      if (!grid) grid = occupancy_grid(ctx, k_mttkrp32_nz<4, 3, false>);
+      k_mttkrp32_nz<4, 3, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->jleaf, a.x, B->vals, a.D, a.out, rec,
+                                                         col.counters);
+    } else if (a.op == Op::SpMM && variant >= 10) {
       if (variant == 10) launch_nz_async<2>(ctx, g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
       else if (variant == 11) launch_nz_async<3>(ctx, g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
       else if (variant == 12) launch_nz_async<4>(ctx, g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);

@@ -22,6 +22,10 @@ __global__ void k_setup(DevColor* __restrict__ cols, int64_t P, int split, int o
                         const int64_t* __restrict__ R, int64_t nrows, int64_t CH,
                         int64_t c_first, int64_t c_count, int64_t* __restrict__ counters);
 
+bool sddmm_nz_launch(spd_context* ctx, const spd_tensor* B, const WalkGeom& g, const double* C,
+                     const double* D, int64_t K, int64_t dk, int64_t dj, double* Avals,
+                     const int64_t* counters);
+
 template <int KT>
 __global__ void __launch_bounds__(kBlock) k_sddmm_walk(WalkGeom g, const int64_t* __restrict__ crd,
                                                        const double* __restrict__ vals,
@@ -135,6 +139,8 @@ static void run_sddmm(spd_context* ctx, const spd_tensor* B, const double* C, co
   launches++;
   const int64_t kt = ceil_div(K > 0 ? K : 1, 32);
   leaf_timing_begin(ctx);
+  if (sddmm_nz_launch(ctx, B, g, C, D, K, dk, dj, Avals, counters)) {
+  } else
 #define SDDMM_CASE(KT_)                                                                    \
   {                                                                                        \
     static int grid = 0;                                                                   \

@@ -219,8 +219,6 @@ if "c5" in configs:
     ops = [(rp, crd, vals)]
     for shift in (1, 2):
         rps = np.empty(n + 1, np.int64)
-        cs = np.empty(len(crd) + 10, np.int64)
-        vs = np.empty(len(crd) + 10)
         # shifted copies: same generator, columns + shift (mod n), re-sorted per row
         e = 10 * n
         cs = np.empty(e, np.int64)
