@@ -198,9 +198,23 @@ int spd_spmttkrp(spd_context* ctx, const spd_tensor* B, const double* C_dev,
                  int64_t ncolors, spd_stats* stats);
 /* A = B + C + D over CSR operands with identical dims, row split: two-phase
  * assembly (count -> scan -> fill, sim.cpp:676-788) producing a new CSR
- * tensor with the structural-union pattern. */
+ * tensor with the structural-union pattern.  With a communicator and one
+ * colour per GPU, each GPU assembles the rows of its colour (other rows are
+ * empty in its piece) and the per-GPU nnz are all-gathered so every piece
+ * knows its global pos offset (spd_tensor_global_span). */
 int spd_spadd3(spd_context* ctx, const spd_tensor* B, const spd_tensor* C, const spd_tensor* D,
                spd_tensor** A_out, int64_t first_color, int64_t ncolors, spd_stats* stats);
+
+/* Row block [row_lo, row_hi], first global position and global nnz of a
+ * tensor piece (a whole tensor: all rows, 0, nnz). */
+int spd_tensor_global_span(const spd_tensor* t, int64_t* row_lo, int64_t* row_hi,
+                           int64_t* pos_base, int64_t* global_positions);
+
+/* Collective: gathers the row-block pieces of a distributed CSR output on
+ * GPU `root` (grouped NCCL send/recv; the reference assembles one Region per
+ * output, sim.cpp:676-788).  *out is the whole tensor on root, NULL on the
+ * other ranks. */
+int spd_gather_rows(spd_context* ctx, const spd_tensor* A, int root, spd_tensor** out);
 
 /* Per-colour Stats::PerWorker::work of the last op (sim.cpp:352), `pieces`
  * entries. */

@@ -131,6 +131,10 @@ struct spd_tensor {
   int64_t crd32h_rowbytes = 0;
   // 3-level trees: middle-mode coordinate of every leaf (crd1 of its fibre).
   int32_t* jleaf = nullptr;
+  // Row block and global pos offset of a distributed (per-GPU) piece of an
+  // assembled output (spd_spadd3 with a communicator); a whole tensor has
+  // rows [0, n) and pos_base 0.  global_positions < 0: not an assembled output.
+  int64_t row_lo = 0, row_hi = -1, pos_base = 0, global_positions = -1;
 };
 
 struct spd_context {
@@ -212,7 +216,7 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 // Host-side helpers implemented in context.cu.
 spd_context* checked(spd_context* ctx);

@@ -12,6 +12,14 @@
 
 namespace spd {
 
+// A whole (non-distributed) tensor: every top-level row, pos base 0.
+static void set_whole_span(spd_tensor* t) {
+  t->row_lo = 0;
+  t->row_hi = (t->levels.size() >= 2 ? t->levels[1].parent_positions : 1) - 1;
+  t->pos_base = 0;
+  t->global_positions = t->nvals;
+}
+
 static thread_local std::string g_last_error;
 void set_last_error(const std::string& msg) { g_last_error = msg; }
 
@@ -224,6 +232,7 @@ static spd_tensor* upload_impl(spd_context* ctx, int order, const int64_t* dims,
       parent = nnz;
     }
     t->nvals = parent;
+    set_whole_span(t);
     t->vals = (double*)dev_alloc(ctx, sizeof(double) * (parent > 0 ? parent : 1));
     if (parent > 0) {
       if (!vals) throw ValidationError("tensor: vals length does not match leaf count");
@@ -509,6 +518,7 @@ int spd_tensor_wrap_device(spd_context* ctx, int order, const int64_t* dims, con
       parent = nnz;
     }
     t->nvals = parent;
+    set_whole_span(t);
     t->vals = vals_dev;
     *out = t;
   });

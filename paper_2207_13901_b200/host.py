@@ -397,6 +397,18 @@ class DeviceTensor:
         check(N.lib().spd_tensor_download_vals(self.h, vals.ctypes.data_as(N.dblp)))
         return SparseTensor.from_parts(self.dims, self.format, levels, vals)
 
+    def global_span(self):
+        """(row_lo, row_hi, pos_base, global_positions) of this piece."""
+        v = [C.c_int64() for _ in range(4)]
+        check(N.lib().spd_tensor_global_span(self.h, *[C.byref(x) for x in v]))
+        return tuple(x.value for x in v)
+
+    def gather_rows(self, root: int = 0):
+        """Collective: the whole tensor on GPU `root` (None elsewhere)."""
+        h = C.c_void_p()
+        check(N.lib().spd_gather_rows(self.ctx.h, self.h, root, C.byref(h)))
+        return DeviceTensor(self.ctx, h, self.dims, self.format) if h.value else None
+
     def close(self):
         if self.h:
             check(N.lib().spd_tensor_destroy(self.h))

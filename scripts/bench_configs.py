@@ -237,7 +237,10 @@ if "c5" in configs:
         op().close()
     torch.cuda.synchronize()
     ts = []
+    last = None
     for _ in range(args.steps):
+        if last is not None:  # the previous output goes back to the pool first
+            last.close()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         A = op()

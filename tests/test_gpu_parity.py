@@ -164,3 +164,36 @@ def test_long_hub_rows_cross_many_chunks(ctx, kernel, N):
         out, st, _ = execute(kernel, t, sched, pieces, ctx)
         assert_close(kernel, out, want["out"], True)
         assert st.combines == want["combines"]
+
+
+@pytest.mark.parametrize("pieces", [1, 3])
+def test_spadd3_hub_and_short_rows(ctx, pieces):
+    """Rows on both sides of the short/long split of the SpAdd3 assembly
+    (thread-per-row merge vs CTA-per-row rank union), heavy overlap between
+    the operands, explicit zeros and -0.0 values (0.0 + v semantics)."""
+    from paper_2207_13901_b200.execute import execute
+    from paper_2207_13901_b200.host import SparseTensor, parse_format
+
+    rng = np.random.default_rng(21)
+    n, m = 400, 6000
+    lens = np.concatenate([rng.integers(0, 8, n - 12), [60, 63, 64, 65, 100, 191, 192, 193, 700, 2000, 5000, 5999]])
+    rng.shuffle(lens)
+    base_r = np.repeat(np.arange(n), lens)
+    base_c = np.concatenate([np.sort(rng.choice(m, L, replace=False)) for L in lens])
+    ops = {}
+    for k, X in enumerate("BCD"):
+        keep = rng.random(base_r.shape[0]) < 0.6  # overlapping subsets of a shared pattern
+        extra_r = rng.integers(0, n, 300)
+        extra_c = rng.integers(0, m, 300)
+        r = np.concatenate([base_r[keep], extra_r])
+        c = np.concatenate([base_c[keep], extra_c])
+        lin = np.unique(r * m + c)
+        v = rng.integers(-3, 4, lin.shape[0]).astype(float)
+        v[rng.random(lin.shape[0]) < 0.05] = -0.0
+        ops[X] = SparseTensor.pack((n, m), parse_format("ds"), np.stack([lin // m, lin % m], 1), v)
+    want = oracle_execute("spadd3", ops, "row", pieces)
+    out, st, _ = execute("spadd3", ops, "row", pieces, ctx)
+    assert_close("spadd3", out, want["out"], True)
+    got_v, want_v = np.asarray(out[2]), np.asarray(want["out"][2])
+    assert np.array_equal(np.signbit(got_v), np.signbit(want_v))
+    assert st.work == want["work"]
