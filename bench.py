@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--ref-scale", type=int, default=17, help="R-MAT scale of the CPU reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--trace", action="store_true",
+                    help="after the timed run, print per-phase device times of the SpMM step (stderr)")
     return ap.parse_args()
 
 
@@ -56,6 +58,7 @@ def rmat_csr(scale, edge_factor, seed, kind=0):
     from paper_2207_13901_b200 import _native as N
 
     S = N.synth()
+    S.syn_set_threads(host_cores())  # torchrun exports OMP_NUM_THREADS=1 to every rank
     n = 1 << scale
     edges = edge_factor * n
     rp = np.empty(n + 1, np.int64)
@@ -282,11 +285,25 @@ def main():
         if sampler:
             sampler.__enter__()
             sampler.wait_first()
-        t_end, nw = time.time() + (1.5 if with_clocks else 0.0), 0
-        while nw < max(warmup, 3) or time.time() < t_end:
+        # Step counts must agree across ranks (every step runs an NCCL
+        # collective inside the backend): time-based loops are converted to
+        # counts that are max-reduced over the ranks.
+        def agreed(count):
+            if world == 1:
+                return count
+            c = torch.tensor([count], dtype=torch.int64, device=dev)
+            dist.all_reduce(c, op=dist.ReduceOp.MAX)
+            return int(c[0])
+
+        t0 = time.time()
+        for _ in range(max(warmup, 3)):
             step_fn()
             torch.cuda.synchronize()
-            nw += 1
+        if with_clocks:  # >= 1.5 s of load before the timed region
+            per = (time.time() - t0) / max(warmup, 3)
+            for _ in range(agreed(int(max(0.0, 1.5 - (time.time() - t0)) / max(per, 1e-4)) + 1)):
+                step_fn()
+                torch.cuda.synchronize()
         l0 = ctx.launches()
         ctx.timing(True)
         if world > 1:
@@ -301,9 +318,9 @@ def main():
             dist.barrier()
         ctx.timing(False)
         nl = ctx.launches() - l0
+        m_est = ev0.elapsed_time(ev1) / steps * 1e-3
         if sampler:
-            t_end = time.time() + 0.5
-            while time.time() < t_end:
+            for _ in range(agreed(int(0.5 / max(m_est, 1e-4)) + 1)):
                 step_fn()
                 torch.cuda.synchronize()
             sampler.__exit__(None, None, None)
@@ -315,6 +332,24 @@ def main():
         return float(t[0]), float(t[1]), nl, (sampler.summary() if sampler else None)
 
     ms, leaf_avg, launches, clock_summary = measure(step, args.steps, args.warmup, True)
+    if args.trace:  # phase breakdown of the step on every rank (outside the timed region)
+        ctx.timing(2)
+        for _ in range(4):
+            step()
+        d = np.asarray(ctx.read_timing())
+        ctx.timing(False)
+        names = ["memset+setup", "zero", "leaf", "fixup", "allgather", "combine", "partition+gaps"]
+        per = d[: (len(d) // 7) * 7].reshape(-1, 7)[:-1].mean(axis=0) if len(d) >= 14 else d
+        t = torch.tensor(per, dtype=torch.float64, device=dev)
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        if world > 1:
+            dist.all_gather(allt, t)
+        else:
+            allt = [t]
+        if rank == 0:
+            for r, v in enumerate(allt):
+                print(f"[trace rank {r}] " + " ".join(f"{k}={x * 1e3:.1f}us" for k, x in zip(names, v.cpu().numpy())),
+                      file=sys.stderr, flush=True)
 
     # Secondary: SpMV on the same R-MAT (the metric names SpMV and SpMM).
     x_d = torch.from_numpy(dense_vals(n, args.seed + 2)).to(dev) if rank == 0 else torch.empty(n, dtype=torch.float64, device=dev)

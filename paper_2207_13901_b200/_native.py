@@ -104,6 +104,7 @@ SYNTH_SIGNATURES = {
         [i64, i64, i64, i64, C.c_uint64, C.c_int, i64p, i64p, i64p, i64p, dblp, i64p],
     ),
     "syn_max_threads": (C.c_int, []),
+    "syn_set_threads": (None, [C.c_int]),
 }
 
 

@@ -166,7 +166,7 @@ struct spd_context {
 
   // Instrumentation (spd_context_timing / spd_context_launches).
   int64_t launches = 0;
-  bool timing = false;
+  int timing = 0;  // 0 off, 1 leaf pairs, 2 phase markers
   std::vector<cudaEvent_t> timing_events;  // pairs, grow-only pool
   size_t timing_used = 0;                  // events in use (2 per leaf launch)
 };
@@ -228,5 +228,7 @@ void fill_stats(spd_context* ctx, spd_stats* st, int64_t combines, const std::ve
 // Brackets the leaf kernel of an op with a timing event pair when enabled.
 void leaf_timing_begin(spd_context* ctx);
 void leaf_timing_end(spd_context* ctx);
+// Phase marker (timing mode 2): per-phase device time of an op.
+void trace_mark(spd_context* ctx);
 
 }  // namespace spd

@@ -316,11 +316,15 @@ static cudaEvent_t timing_event(spd_context* ctx) {
 }
 
 void leaf_timing_begin(spd_context* ctx) {
-  if (ctx->timing) SPD_CUDA(cudaEventRecord(timing_event(ctx), ctx->stream));
+  if (ctx->timing == 1) SPD_CUDA(cudaEventRecord(timing_event(ctx), ctx->stream));
 }
 
 void leaf_timing_end(spd_context* ctx) {
-  if (ctx->timing) SPD_CUDA(cudaEventRecord(timing_event(ctx), ctx->stream));
+  if (ctx->timing == 1) SPD_CUDA(cudaEventRecord(timing_event(ctx), ctx->stream));
+}
+
+void trace_mark(spd_context* ctx) {
+  if (ctx->timing == 2) SPD_CUDA(cudaEventRecord(timing_event(ctx), ctx->stream));
 }
 
 }  // namespace spd
@@ -332,7 +336,8 @@ extern "C" {
 int spd_context_timing(spd_context* ctx, int enable) {
   return guarded([&] {
     checked(ctx);
-    ctx->timing = enable != 0;
+    if (enable < 0 || enable > 2) throw ValidationError("timing mode must be 0, 1 or 2");
+    ctx->timing = enable;
   });
 }
 
@@ -341,13 +346,18 @@ int spd_context_read_timing(spd_context* ctx, double* leaf_ms, int64_t cap, int6
     checked(ctx);
     activate(ctx);
     SPD_CUDA(cudaStreamSynchronize(ctx->stream));
-    int64_t pairs = (int64_t)ctx->timing_used / 2;
-    for (int64_t i = 0; i < pairs && i < cap; i++) {
+    // mode 1: (begin, end) pairs around leaf kernels; mode 2: consecutive
+    // phase markers, returned as the deltas between them.
+    const bool pairs_mode = ctx->timing != 2;
+    const int64_t used = (int64_t)ctx->timing_used;
+    const int64_t cnt = pairs_mode ? used / 2 : std::max<int64_t>(used - 1, 0);
+    for (int64_t i = 0; i < cnt && i < cap; i++) {
       float ms = 0;
-      SPD_CUDA(cudaEventElapsedTime(&ms, ctx->timing_events[2 * i], ctx->timing_events[2 * i + 1]));
+      const int64_t a = pairs_mode ? 2 * i : i;
+      SPD_CUDA(cudaEventElapsedTime(&ms, ctx->timing_events[a], ctx->timing_events[a + 1]));
       leaf_ms[i] = ms;
     }
-    *n = pairs;
+    *n = cnt;
     ctx->timing_used = 0;
   });
 }

@@ -1418,6 +1418,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   cudaStream_t s = ctx->stream;
   int64_t launches = 0;
   if (stats) SPD_CUDA(cudaEventRecord(ctx->ev0, s));
+  trace_mark(ctx);
   SPD_CUDA(cudaMemsetAsync(col.head_pack, 0xff, sizeof(int64_t) * P * (W + 2), s));
   SPD_CUDA(cudaMemsetAsync(col.counters, 0, sizeof(int64_t) * 4, s));
   SPD_CUDA(cudaMemsetAsync(col.tail_row, 0xff, sizeof(int64_t) * P, s));
@@ -1439,12 +1440,14 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
     if (a.op == Op::SpMM || a.op == Op::SpMTTKRP) {
       static int zgrid = 0;
       if (!zgrid) zgrid = occupancy_grid(ctx, k_zero_empty);
+      trace_mark(ctx);
       k_zero_empty<<<zgrid, kBlock, 0, s>>>(g.R, g.nrows, (const DevColor*)ctx->colors_dev.ptr, first, count,
                                            a.W, a.out);
       SPD_CHECK_LAUNCH();
       launches++;
     }
   }
+  trace_mark(ctx);
   leaf_timing_begin(ctx);
   if (use_nz) {
     if (a.op == Op::SpMTTKRP) {
@@ -1569,6 +1572,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   }
   SPD_CHECK_LAUNCH();
   leaf_timing_end(ctx);
+  trace_mark(ctx);
   launches++;
   {
     static int grid = 0;
@@ -1577,14 +1581,17 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
     SPD_CHECK_LAUNCH();
     launches++;
   }
+  trace_mark(ctx);
   if (ctx->comm && count == 1 && P > 1) {
     const size_t bytes = sizeof(int64_t) * (W + 2);
     SPD_NCCL(ncclAllGather(col.head_pack + first * (W + 2), col.head_pack, bytes, ncclUint8,
                            ctx->comm, s));
   }
+  trace_mark(ctx);
   k_colour_combine<<<(unsigned)ceil_div(P * 32, 256), 256, 0, s>>>(
       col, (const DevColor*)ctx->colors_dev.ptr, P, W, first, count, a.out);
   SPD_CHECK_LAUNCH();
+  trace_mark(ctx);
   launches++;
   ctx->launches += launches;
   if (stats) {

@@ -249,9 +249,10 @@ class Context:
         check(N.lib().spd_nccl_unique_id(buf))
         return buf.raw
 
-    def timing(self, enable: bool):
-        """Record CUDA events around every leaf kernel (spd_context_timing)."""
-        check(N.lib().spd_context_timing(self.h, int(bool(enable))))
+    def timing(self, enable):
+        """spd_context_timing: False/0 off; True/1 CUDA events around every
+        leaf kernel; 2 phase markers (read_timing returns the deltas)."""
+        check(N.lib().spd_context_timing(self.h, int(enable)))
 
     def read_timing(self, cap: int = 1 << 16) -> List[float]:
         buf = (C.c_double * cap)()

@@ -229,4 +229,10 @@ int64_t syn_powerlaw_csf(int64_t I, int64_t J, int64_t K, int64_t samples, uint6
   return nnz;
 }
 
+/* Thread count of the generators (launchers such as torchrun export
+ * OMP_NUM_THREADS=1 to every rank; the rank that generates inputs raises it). */
+void syn_set_threads(int n) {
+  if (n > 0) omp_set_num_threads(n);
+}
+
 int syn_max_threads(void) { return omp_get_max_threads(); }
