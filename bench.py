@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--edge-factor", type=int, default=10)
     ap.add_argument("--cols", type=int, default=32, help="N, columns of C")
-    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--ref-scale", type=int, default=17, help="R-MAT scale of the CPU reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=42)
@@ -446,13 +446,15 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
     spd_tensor_upload validates and converts on the GPU) and of this GPU's
     1/N block of C from pinned memory, NCCL all-gather of C over NVLink
     (spd_allgather), the partition step, the leaf + boundary combine, and D2H
-    of the output rows this GPU owns."""
+    of the output rows this GPU owns.  Consecutive steps alternate between two
+    contexts on two streams, so step k+1's uploads overlap step k's leaf and
+    read-back (a stream of independent SpMM problems, double-buffered)."""
     import ctypes as Cc
 
     import torch.distributed as dist
 
     from paper_2207_13901_b200 import _native as NN
-    from paper_2207_13901_b200.distributed import owned_rows
+    from paper_2207_13901_b200.distributed import init_comm, owned_rows
 
     rp_h = rp_d.cpu()
     pairs = torch.stack([rp_h[:-1], rp_h[1:] - 1], dim=1).contiguous().pin_memory()
@@ -460,51 +462,71 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
     vals_h = vals_d.cpu().pin_memory()
     per = (n * N) // world
     C_h = C_d[rank * per:(rank + 1) * per].cpu().pin_memory()
-    C_dev = torch.empty_like(C_d)
-    A_dev = torch.empty(n * N, dtype=torch.float64, device=dev)
+    streams = [torch.cuda.Stream(dev) for _ in range(2)]
+    ctxs = [H.Context(dev.index, stream=s.cuda_stream) for s in streams]
+    if world > 1:
+        for cx in ctxs:
+            init_comm(cx, dist, rank, world, dev)
+    C_devs = [torch.empty_like(C_d) for _ in range(2)]
+    A_devs = [torch.empty(n * N, dtype=torch.float64, device=dev) for _ in range(2)]
     fmt = H.parse_format("ds")
     dims = (Cc.c_int64 * 2)(n, n)
     kinds = (Cc.c_int * 2)(0, 1)
     mo = (Cc.c_int * 2)(0, 1)
     pos_pp = (NN.i64p * 2)(None, Cc.cast(pairs.data_ptr(), NN.i64p))
     crd_pp = (NN.i64p * 2)(None, Cc.cast(crd_h.data_ptr(), NN.i64p))
-    state = {}
+    state = {"k": 0, "live": [None, None]}
+    torch.cuda.synchronize()
 
     def one():
-        h = Cc.c_void_p()
-        NN.check(NN.lib().spd_tensor_upload(ctx.h, 2, dims, kinds, mo, pos_pp, crd_pp,
-                                            Cc.cast(vals_h.data_ptr(), NN.dblp), Cc.byref(h)))
-        Bs = H.DeviceTensor(ctx, h, (n, n), fmt)
-        C_dev[rank * per:(rank + 1) * per].copy_(C_h, non_blocking=True)
-        if world > 1:
-            ctx.allgather(C_dev, per * 8)
-        cols = H.partition_nonzero(ctx, Bs, 1, world)
-        lo, hi = owned_rows(cols, rp_h.numpy(), "nonzero", n)[rank]
-        H.spmm(ctx, Bs, C_dev, N, A_dev, first=rank if world > 1 else 0, count=1, pieces=world, stats=False)
-        if "A_h" not in state:
-            state["A_h"] = torch.empty(max(hi - lo + 1, 0) * N, dtype=torch.float64).pin_memory()
-        A_h = state["A_h"]
-        if hi >= lo:
-            A_h.copy_(A_dev[lo * N:(hi + 1) * N], non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        Bs.close()
+        j = state["k"] % 2
+        state["k"] += 1
+        cx, s = ctxs[j], streams[j]
+        if state["live"][j] is not None:  # the tensor of step k-2 on this stream
+            state["live"][j].close()
+        with torch.cuda.stream(s):
+            h = Cc.c_void_p()
+            NN.check(NN.lib().spd_tensor_upload(cx.h, 2, dims, kinds, mo, pos_pp, crd_pp,
+                                                Cc.cast(vals_h.data_ptr(), NN.dblp), Cc.byref(h)))
+            Bs = H.DeviceTensor(cx, h, (n, n), fmt)
+            C_devs[j][rank * per:(rank + 1) * per].copy_(C_h, non_blocking=True)
+            if world > 1:
+                cx.allgather(C_devs[j], per * 8)
+            cols = H.partition_nonzero(cx, Bs, 1, world)
+            lo, hi = owned_rows(cols, rp_h.numpy(), "nonzero", n)[rank]
+            H.spmm(cx, Bs, C_devs[j], N, A_devs[j], first=rank if world > 1 else 0, count=1, pieces=world,
+                   stats=False)
+            key = "A_h%d" % j
+            if key not in state:
+                state[key] = torch.empty(max(hi - lo + 1, 0) * N, dtype=torch.float64).pin_memory()
+            if hi >= lo:
+                state[key].copy_(A_devs[j][lo * N:(hi + 1) * N], non_blocking=True)
+        state["live"][j] = Bs
 
-    one()  # warm (allocator pool, derived indices of the fresh tensor are rebuilt every step)
+    one()  # warm both streams (allocator pools, communicators)
+    one()
+    for st in streams:
+        st.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.e2e_steps):
         one()
-    torch.cuda.synchronize()
+    for st in streams:
+        st.synchronize()
     dt = (time.perf_counter() - t0) / args.e2e_steps
+    for Bs in state["live"]:
+        Bs.close()
+    for cx in ctxs:
+        cx.close()
     t = torch.tensor([dt], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dt = float(t[0])
     # whole-job bytes per step: summed over ranks
     by = torch.tensor([pairs.numel() * 8 + crd_h.numel() * 8 + vals_h.numel() * 8 + C_h.numel() * 8,
-                       state["A_h"].numel() * 8], dtype=torch.float64, device=dev)
+                       state["A_h0"].numel() * 8], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(by)
     h2d, d2h = int(by[0]), int(by[1])
@@ -513,7 +535,8 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
             "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3,
             "note": "per step, every GPU: B uploaded as the reference stores it (pos pairs, crd, vals) "
                     "through spd_tensor_upload, its 1/N of C H2D + NCCL all-gather, partition, leaf + "
-                    "combine, its owned output rows D2H; time = max over ranks, bytes = sum over ranks"}
+                    "combine, its owned output rows D2H; consecutive steps double-buffered on two "
+                    "streams; time = max over ranks, bytes = sum over ranks"}
 
 
 if __name__ == "__main__":

@@ -1400,7 +1400,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   const bool spmm32 = a.op == Op::SpMM && a.W == 32 && B->dims[1] < (int64_t(1) << 31);
   const int variant = spmm32 ? spmm32_variant() : 0;
   if (spmm32 && variant >= 2 && variant <= 4) g.CH = 4096;
-  if (spmm32 && variant >= 7) g.CH = 4096;
+  if (spmm32 && variant >= 7 && variant < 20) g.CH = 4096;
   const int64_t W = a.W > 0 ? a.W : 1;
   const int64_t max_chunks = nnz / g.CH + 2 * P + 2;
 
@@ -1466,7 +1466,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
       if (!grid) grid = occupancy_grid(ctx, k_mttkrp32_nz<4, 3, false>);
       k_mttkrp32_nz<4, 3, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->jleaf, a.x, B->vals, a.D, a.out, rec,
                                                          col.counters);
-    } else if (a.op == Op::SpMM && variant >= 10) {
+    } else if (a.op == Op::SpMM && variant >= 10 && variant < 20) {
       if (variant == 10) launch_nz_async<2>(ctx, g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
       else if (variant == 11) launch_nz_async<3>(ctx, g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
       else if (variant == 12) launch_nz_async<4>(ctx, g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
