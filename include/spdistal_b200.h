@@ -144,6 +144,29 @@ int spd_tensor_nvals(const spd_tensor* t, int64_t* nvals);
 /* Device pointers of a level / of vals (NULL where the level stores nothing). */
 int spd_tensor_device_ptrs(const spd_tensor* t, int level, int64_t** rowptr, int64_t** crd);
 int spd_tensor_vals_ptr(const spd_tensor* t, double** vals);
+/* SparseTensor::pack (tensor.cpp:94-182) on the GPU: `nentries` COO entries
+ * (coords[m] = the coordinates of logical mode m, values) -> the coordinate
+ * tree of the format.  Duplicates are summed in input order from 0.0 and
+ * kept when zero; out-of-range coordinates return SPD_ERR_VALIDATION.
+ * on_device: 0 host pointers (staged with cudaMemcpyAsync), 1 device pointers.
+ * Device-side construction is SURVEY 8f row 1 (the reference's pack runs on
+ * one CPU thread through a std::map). */
+int spd_tensor_pack(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
+                    const int* mode_order, int64_t nentries, const int64_t* const* coords,
+                    const double* values, int on_device, spd_tensor** out);
+
+/* load_tensor (tensor_io.cpp:136-142): a .tns or MatrixMarket file parsed on
+ * all host threads into pinned staging, then spd_tensor_pack.  dims NULL:
+ * from the MatrixMarket header, or the per-mode maximum of a .tns file;
+ * dims_out (order entries, may be NULL) receives the dimensions used.
+ * Malformed files return SPD_ERR_VALIDATION with the reference's message. */
+int spd_tensor_load(spd_context* ctx, const char* path, int order, const int* kinds,
+                    const int* mode_order, const int64_t* dims, spd_tensor** out, int64_t* dims_out);
+
+/* write_tensor (tensor_io.cpp:145-155): every stored leaf, sorted by logical
+ * coordinates, 1-indexed, value as %.17g. */
+int spd_tensor_store(const spd_tensor* t, const char* path);
+
 /* Download (synchronises): pos as (lo,hi) pairs, or row pointers. */
 int spd_tensor_download_level(const spd_tensor* t, int level, int64_t* pos_pairs, int64_t* crd);
 int spd_tensor_download_rowptr(const spd_tensor* t, int level, int64_t* rowptr);

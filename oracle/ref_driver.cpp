@@ -24,6 +24,7 @@
 #include "dspar/schedule.hpp"
 #include "dspar/sim.hpp"
 #include "dspar/tensor.hpp"
+#include "dspar/tensor_io.hpp"
 #include "dspar/tin.hpp"
 
 using namespace dspar;
@@ -289,6 +290,51 @@ int ref_bundle_disjoint(void* h, int loop, const char* tensor) {
   return b ? b->vals.disjoint() : -1;
 }
 
+// SparseTensor::pack (tensor.cpp:94-182) of n COO entries (coords row-major,
+// n x order, logical mode order); the packed tensor is read back with the
+// ref_out_* getters.  Pins the device-side pack (spd_tensor_pack).
+void* ref_pack(int order, const int64_t* dims, const char* format, int64_t n, const int64_t* coords,
+               const double* values) {
+  auto* r = new RefRun();
+  guarded(r, [&] {
+    std::vector<int64_t> d(dims, dims + order);
+    std::vector<TensorEntry> entries(static_cast<size_t>(n));
+    for (int64_t e = 0; e < n; e++) {
+      entries[e].coords.assign(coords + e * order, coords + (e + 1) * order);
+      entries[e].value = values[e];
+    }
+    double t0 = now();
+    r->result.output = SparseTensor::pack(d, parse_format(format), std::move(entries));
+    r->exec_seconds = now() - t0;
+    r->has_result = true;
+  });
+  return r;
+}
+
+// load_tensor (tensor_io.cpp:136-142): .tns or MatrixMarket file -> pack.
+// dims may be NULL (inferred / taken from the MatrixMarket header).  Pins the
+// device-side loader (spd_tensor_load).
+void* ref_load(const char* path, const char* format, int order, const int64_t* dims) {
+  auto* r = new RefRun();
+  guarded(r, [&] {
+    std::optional<std::vector<int64_t>> d;
+    if (dims) d = std::vector<int64_t>(dims, dims + order);
+    double t0 = now();
+    r->result.output = load_tensor(path, parse_format(format), d);
+    r->exec_seconds = now() - t0;
+    r->has_result = true;
+  });
+  return r;
+}
+
+// store_tensor (tensor_io.cpp:158-163) of the run's output tensor.
+int ref_store(void* h, const char* path) {
+  auto* r = static_cast<RefRun*>(h);
+  if (!r->has_result) return -1;
+  guarded(r, [&] { store_tensor(r->result.output, path); });
+  return r->status;
+}
+
 // Output tensor access.
 int ref_out_nlevels(void* h) {
   auto* r = static_cast<RefRun*>(h);
@@ -319,6 +365,13 @@ int ref_out_copy_level(void* h, int l, int64_t* pos_pairs, int64_t* crd) {
   for (int64_t p = 0; p < c.pos.size(); p++)
     pos_pairs[2 * p] = c.pos.range_at(p).lo, pos_pairs[2 * p + 1] = c.pos.range_at(p).hi;
   for (int64_t q = 0; q < c.crd.size(); q++) crd[q] = c.crd.coord_at(q);
+  return 0;
+}
+int ref_out_dims(void* h, int64_t* dims) {
+  auto* r = static_cast<RefRun*>(h);
+  if (!r->has_result) return -1;
+  const auto& d = r->result.output.dims();
+  for (size_t k = 0; k < d.size(); k++) dims[k] = d[k];
   return 0;
 }
 int64_t ref_out_nvals(void* h) {

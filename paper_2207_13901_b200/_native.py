@@ -85,6 +85,11 @@ SIGNATURES = {
     "spd_spadd3": (C.c_int, [vp, vp, vp, vp, C.POINTER(vp), i64, i64, C.POINTER(spd_stats)]),
     "spd_tensor_global_span": (C.c_int, [vp, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
     "spd_gather_rows": (C.c_int, [vp, vp, C.c_int, C.POINTER(vp)]),
+    "spd_tensor_load": (C.c_int, [vp, C.c_char_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), i64p,
+                                  C.POINTER(vp), i64p]),
+    "spd_tensor_store": (C.c_int, [vp, C.c_char_p]),
+    "spd_tensor_pack": (C.c_int, [vp, C.c_int, i64p, C.POINTER(C.c_int), C.POINTER(C.c_int), i64,
+                                  C.POINTER(i64p), dblp, C.c_int, C.POINTER(vp)]),
     "spd_last_work": (C.c_int, [vp, i64p, i64]),
     "spd_context_timing": (C.c_int, [vp, C.c_int]),
     "spd_context_read_timing": (C.c_int, [vp, dblp, i64, i64p]),

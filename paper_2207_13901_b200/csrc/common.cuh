@@ -228,6 +228,13 @@ void fill_stats(spd_context* ctx, spd_stats* st, int64_t combines, const std::ve
 // Brackets the leaf kernel of an op with a timing event pair when enabled.
 void leaf_timing_begin(spd_context* ctx);
 void leaf_timing_end(spd_context* ctx);
+// Tensor construction helpers (context.cu): level skeleton from a FormatSpec
+// (tensor.cpp:30-92), whole-tensor span, stream-ordered allocation.
+spd_tensor* make_skeleton(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
+                          const int* mode_order);
+void set_whole_span(spd_tensor* t);
+void* dev_alloc(spd_context* ctx, size_t bytes);
+void dev_free(spd_context* ctx, void* p);
 // Phase marker (timing mode 2): per-phase device time of an op.
 void trace_mark(spd_context* ctx);
 

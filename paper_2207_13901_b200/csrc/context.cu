@@ -13,7 +13,7 @@
 namespace spd {
 
 // A whole (non-distributed) tensor: every top-level row, pos base 0.
-static void set_whole_span(spd_tensor* t) {
+void set_whole_span(spd_tensor* t) {
   t->row_lo = 0;
   t->row_hi = (t->levels.size() >= 2 ? t->levels[1].parent_positions : 1) - 1;
   t->pos_base = 0;
@@ -104,19 +104,19 @@ static int grid_for(spd_context* ctx, int64_t n, int block = 256) {
   return (int)g;
 }
 
-static void* dev_alloc(spd_context* ctx, size_t bytes) {
+void* dev_alloc(spd_context* ctx, size_t bytes) {
   void* p = nullptr;
   if (bytes == 0) bytes = 8;
   SPD_CUDA(cudaMallocAsync(&p, bytes, ctx->stream));
   return p;
 }
 
-static void dev_free(spd_context* ctx, void* p) {
+void dev_free(spd_context* ctx, void* p) {
   if (p) cudaFreeAsync(p, ctx->stream);
 }
 
 // Builds the level skeleton from the FormatSpec (tensor.cpp:30-41, 81-92).
-static spd_tensor* make_skeleton(spd_context* ctx, int order, const int64_t* dims,
+spd_tensor* make_skeleton(spd_context* ctx, int order, const int64_t* dims,
                                  const int* kinds, const int* mode_order) {
   if (order < 0) throw ValidationError("tensor order must be non-negative");
   std::vector<bool> seen(order, false);

@@ -314,6 +314,54 @@ class DeviceTensor:
         return DeviceTensor(ctx, h, t.dims, t.format)
 
     @staticmethod
+    def pack(ctx: Context, dims, fmt: FormatSpec, coords, values) -> "DeviceTensor":
+        """spd_tensor_pack: SparseTensor::pack (tensor.cpp:94-182) on the GPU.
+        `coords`: (nentries, order) host array in logical mode order, or a
+        sequence of `order` equal-length arrays (numpy, or torch CUDA tensors
+        for device-resident input); `values`: nentries."""
+        order = len(dims)
+        d, kinds, mo = _format_arrays(dims, fmt)
+        on_device = False
+        if isinstance(coords, (list, tuple)):
+            cols = list(coords)
+        else:
+            arr = np.asarray(coords, dtype=np.int64).reshape(-1, order)
+            cols = [np.ascontiguousarray(arr[:, k]) for k in range(order)]
+        if cols and hasattr(cols[0], "is_cuda") and cols[0].is_cuda:
+            on_device = True
+            n = int(cols[0].numel())
+            ptrs = (N.i64p * max(order, 1))(*[C.cast(c.data_ptr(), N.i64p) for c in cols])
+            vptr = C.cast(values.data_ptr(), N.dblp)
+            keep = (cols, values)
+        else:
+            cols = [np.ascontiguousarray(np.asarray(c, dtype=np.int64)) for c in cols]
+            vals = np.ascontiguousarray(np.asarray(values, dtype=np.float64).reshape(-1))
+            n = int(vals.shape[0])
+            ptrs = (N.i64p * max(order, 1))(*[c.ctypes.data_as(N.i64p) for c in cols])
+            vptr = vals.ctypes.data_as(N.dblp)
+            keep = (cols, vals)
+        h = C.c_void_p()
+        check(N.lib().spd_tensor_pack(ctx.h, order, d, kinds, mo, n, ptrs, vptr, int(on_device), C.byref(h)))
+        del keep
+        return DeviceTensor(ctx, h, dims, fmt)
+
+    @staticmethod
+    def load(ctx: Context, path, fmt: FormatSpec, dims=None) -> "DeviceTensor":
+        """spd_tensor_load: load_tensor (tensor_io.cpp:136-142) -> device pack."""
+        order = len(fmt.kinds)
+        kinds = (C.c_int * order)(*[N.SPD_DENSE if k == DENSE else N.SPD_COMPRESSED for k in fmt.kinds])
+        mo = (C.c_int * order)(*fmt.mode_order)
+        d = (C.c_int64 * order)(*[int(x) for x in dims]) if dims is not None else None
+        dout = (C.c_int64 * order)()
+        h = C.c_void_p()
+        check(N.lib().spd_tensor_load(ctx.h, str(path).encode(), order, kinds, mo, d, C.byref(h), dout))
+        return DeviceTensor(ctx, h, tuple(dout), fmt)
+
+    def store(self, path):
+        """spd_tensor_store: write_tensor (tensor_io.cpp:145-155)."""
+        check(N.lib().spd_tensor_store(self.h, str(path).encode()))
+
+    @staticmethod
     def upload_rowptr(ctx: Context, dims, fmt: FormatSpec, rowptrs, crds, vals,
                       validate=True) -> "DeviceTensor":
         """spd_tensor_upload_rowptr: device-format host arrays (one per compressed level)."""

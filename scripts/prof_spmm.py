@@ -15,6 +15,7 @@ ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--scale", type=int, default=24)
 ap.add_argument("--cols", type=int, default=32)
 ap.add_argument("--kernel", default="spmm", choices=["spmm", "spmv", "sddmm"])
+ap.add_argument("--slice", default=None, help="q/P: only the rows of nonzero colour q of P (whole rows)")
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -22,15 +23,27 @@ import torch  # noqa: E402
 from paper_2207_13901_b200 import host as H  # noqa: E402
 
 n, rp, crd, vals = bench.rmat_csr(a.scale, 10, 42)
+if a.slice:
+    import numpy as np
+    q, P = (int(x) for x in a.slice.split("/"))
+    nnz = len(crd)
+    lo, hi = q * nnz // P, (q + 1) * nnz // P - 1
+    r0 = int(np.searchsorted(rp, lo, side="right") - 1)
+    r1 = int(np.searchsorted(rp, hi, side="right") - 1)
+    crd, vals = crd[rp[r0]:rp[r1 + 1]], vals[rp[r0]:rp[r1 + 1]]
+    rp = rp[r0:r1 + 2] - rp[r0]
+    print("slice rows", r0, r1, "nnz", len(crd), "non-empty rows", int(np.count_nonzero(np.diff(rp))))
+m = n
+n = len(rp) - 1
 dev = torch.device("cuda", 0)
 rp_d, crd_d, vals_d = (torch.from_numpy(x).to(dev) for x in (rp, crd, vals))
 N = a.cols if a.kernel == "spmm" else (128 if a.kernel == "sddmm" else 1)
-C_d = torch.from_numpy(bench.dense_vals(n * N, 43)).to(dev)
+C_d = torch.from_numpy(bench.dense_vals(m * N, 43)).to(dev)
 A_d = torch.empty(n * N if a.kernel != "sddmm" else len(crd), dtype=torch.float64, device=dev)
 if a.kernel == "sddmm":
-    D_d = torch.from_numpy(bench.dense_vals(n * N, 44)).to(dev)
+    D_d = torch.from_numpy(bench.dense_vals(m * N, 44)).to(dev)
 ctx = H.Context(0)
-B = H.DeviceTensor.wrap(ctx, (n, n), H.parse_format("ds"), [rp_d.data_ptr()], [crd_d.data_ptr()],
+B = H.DeviceTensor.wrap(ctx, (n, m), H.parse_format("ds"), [rp_d.data_ptr()], [crd_d.data_ptr()],
                         vals_d.data_ptr())
 ctx.timing(True)
 for _ in range(a.steps):

@@ -248,6 +248,10 @@ def ref(path=REF_LIB):
             ("ref_stats_imbalance", C.c_double, [vp]), ("ref_stats_work", i64, [vp, i64]),
             ("ref_dense_eval", C.c_int, [C.c_char_p, C.c_int, C.POINTER(ref_tensor_in), C.c_int,
                                           i64p, dblp, C.c_char_p, C.c_int]),
+            ("ref_pack", vp, [C.c_int, i64p, C.c_char_p, i64, i64p, dblp]),
+            ("ref_load", vp, [C.c_char_p, C.c_char_p, C.c_int, i64p]),
+            ("ref_out_dims", C.c_int, [vp, i64p]),
+            ("ref_store", C.c_int, [vp, C.c_char_p]),
         ]:
             f = getattr(L, name)
             f.restype = res
@@ -365,6 +369,43 @@ class RefRun:
         vals = np.empty(L.ref_out_nvals(self.h))
         L.ref_out_copy_vals(self.h, _p(vals, dblp))
         return levels, vals
+
+    @classmethod
+    def pack(cls, dims, fmt: str, coords, values, lib=REF_LIB):
+        """SparseTensor::pack (tensor.cpp:94-182) run by the reference itself;
+        read the result with output()."""
+        self = cls.__new__(cls)
+        L = ref(lib)
+        dims = I64(dims)
+        coords = I64(np.asarray(coords).reshape(-1, len(dims)))
+        values = F64(np.asarray(values, dtype=np.float64).reshape(-1))
+        self._keep = (dims, coords, values)
+        self.h = L.ref_pack(len(dims), _p(dims), fmt.encode(), values.shape[0], _p(coords), _p(values, dblp))
+        self.L = L
+        self.status = L.ref_status(self.h)
+        self.error = L.ref_error(self.h).decode()
+        return self
+
+    @classmethod
+    def load(cls, path, fmt: str, order: int, dims=None, lib=REF_LIB):
+        """load_tensor (tensor_io.cpp:136-142) run by the reference itself."""
+        self = cls.__new__(cls)
+        L = ref(lib)
+        d = I64(dims) if dims is not None else None
+        self._keep = (d,)
+        self.h = L.ref_load(str(path).encode(), fmt.encode(), order, _p(d) if d is not None else None)
+        self.L = L
+        self.status = L.ref_status(self.h)
+        self.error = L.ref_error(self.h).decode()
+        return self
+
+    def store(self, path):
+        return self.L.ref_store(self.h, str(path).encode())
+
+    def out_dims(self, order):
+        d = np.zeros(order, np.int64)
+        self.L.ref_out_dims(self.h, _p(d))
+        return tuple(int(x) for x in d)
 
     def stats(self):
         L = self.L
