@@ -233,6 +233,19 @@ int spd_spadd3(spd_context* ctx, const spd_tensor* B, const spd_tensor* C, const
 int spd_tensor_global_span(const spd_tensor* t, int64_t* row_lo, int64_t* row_hi,
                            int64_t* pos_base, int64_t* global_positions);
 
+/* Collective, data placement (lower_tdn + residency_from_placements,
+ * planner.cpp:361-439, sim.cpp:547-566) of a CSR matrix by its compute
+ * partition: split 1 = row (universe) split, 2 = nonzero split of the leaf
+ * level, one colour per GPU.  `whole` is read on `root` only (NULL
+ * elsewhere).  Every GPU receives the row pointer and its colour's crd/vals
+ * (NCCL broadcast + send/recv) as a piece tensor that the leaf ops accept for
+ * that colour (the matched distribution: compute moves 0 bytes of it); the
+ * context's partition is left set to the piece.  *bytes_in = bytes received. */
+int spd_tensor_place(spd_context* ctx, int root, const spd_tensor* whole, int split,
+                     spd_tensor** piece, int64_t* bytes_in);
+/* Positions [lo, hi] a (piece) tensor holds; a whole tensor: [0, nvals-1]. */
+int spd_tensor_piece_span(const spd_tensor* t, int64_t* lo, int64_t* hi);
+
 /* Collective: gathers the row-block pieces of a distributed CSR output on
  * GPU `root` (grouped NCCL send/recv; the reference assembles one Region per
  * output, sim.cpp:676-788).  *out is the whole tensor on root, NULL on the

@@ -135,6 +135,15 @@ struct spd_tensor {
   // assembled output (spd_spadd3 with a communicator); a whole tensor has
   // rows [0, n) and pos_base 0.  global_positions < 0: not an assembled output.
   int64_t row_lo = 0, row_hi = -1, pos_base = 0, global_positions = -1;
+  // A placed piece (spd_tensor_place): the leaf level's crd/vals hold only
+  // positions [piece_lo, piece_hi]; the level pointers are offset so global
+  // positions index them, the allocations are piece_crd / piece_vals.  The
+  // row pointer is whole (O(rows), for the partition step).
+  bool piece = false;
+  int64_t piece_lo = 0, piece_hi = -1;
+  int64_t* piece_crd = nullptr;
+  double* piece_vals = nullptr;
+  int32_t* crd32h_alloc = nullptr;  // allocation behind crd32h (offset for pieces)
 };
 
 struct spd_context {

@@ -543,7 +543,15 @@ int spd_tensor_destroy(spd_tensor* t) {
       ctx->split = SplitKind::None;
       ctx->split_tensor = nullptr;
     }
-    if (t->owns) {
+    if (t->piece) {
+      for (size_t l = 0; l + 1 < t->levels.size(); l++) {
+        dev_free(ctx, t->levels[l].rowptr);
+        dev_free(ctx, t->levels[l].crd);
+      }
+      dev_free(ctx, t->levels.back().rowptr);
+      dev_free(ctx, t->piece_crd);
+      dev_free(ctx, t->piece_vals);
+    } else if (t->owns) {
       for (auto& L : t->levels) {
         dev_free(ctx, L.rowptr);
         dev_free(ctx, L.crd);
@@ -551,7 +559,7 @@ int spd_tensor_destroy(spd_tensor* t) {
       dev_free(ctx, t->vals);
     }
     dev_free(ctx, t->leaf_rowptr);
-    dev_free(ctx, t->crd32h);
+    dev_free(ctx, t->crd32h_alloc);
     dev_free(ctx, t->jleaf);
     for (auto& z : t->nz) {
       dev_free(ctx, z.ptr);
@@ -606,6 +614,8 @@ int spd_tensor_download_level(const spd_tensor* t, int level, int64_t* pos_pairs
     if (!t || level < 0 || level >= (int)t->levels.size()) throw ValidationError("no such level");
     const auto& L = t->levels[level];
     if (L.kind != SPD_COMPRESSED) throw ValidationError("level is dense: nothing stored");
+    if (t->piece && crd && level + 1 == (int)t->levels.size())
+      throw ValidationError("a placed piece holds only its colour's positions: download the whole tensor");
     spd_context* ctx = t->ctx;
     activate(ctx);
     if (pos_pairs && L.parent_positions > 0) {
@@ -640,6 +650,7 @@ int spd_tensor_download_rowptr(const spd_tensor* t, int level, int64_t* rowptr) 
 int spd_tensor_download_vals(const spd_tensor* t, double* vals) {
   return guarded([&] {
     if (!t) throw ValidationError("null tensor");
+    if (t->piece) throw ValidationError("a placed piece holds only its colour's positions");
     spd_context* ctx = t->ctx;
     activate(ctx);
     if (t->nvals > 0)
@@ -654,6 +665,8 @@ int spd_tensor_download_vals_range(const spd_tensor* t, int64_t first, int64_t c
   return guarded([&] {
     if (!t) throw ValidationError("null tensor");
     if (first < 0 || count < 0 || first + count > t->nvals) throw ValidationError("range outside vals");
+    if (t->piece && count > 0 && (first < t->piece_lo || first + count - 1 > t->piece_hi))
+      throw ValidationError("range outside the placed piece");
     spd_context* ctx = t->ctx;
     activate(ctx);
     if (count > 0)

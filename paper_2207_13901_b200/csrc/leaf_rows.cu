@@ -1264,7 +1264,9 @@ static int nz_minblocks() {
 static const int32_t* hot_crd(spd_context* ctx, spd_tensor* t, int64_t rowbytes) {
   if (t->crd32h && t->crd32h_rowbytes == rowbytes) return t->crd32h;
   const spd_level_store& L = t->levels.back();
-  const int64_t nnz = L.positions;
+  // positions held: all of them, or a placed piece's range
+  const int64_t lo = t->piece ? t->piece_lo : 0;
+  const int64_t nnz = t->piece ? t->piece_hi - t->piece_lo + 1 : L.positions;
   const int64_t ncols = t->dims[t->mode_order[t->groups.back()[0]]];
   cudaStream_t s = ctx->stream;
   int l2 = 0;
@@ -1278,16 +1280,19 @@ static const int32_t* hot_crd(spd_context* ctx, spd_tensor* t, int64_t rowbytes)
   SPD_CUDA(cudaMallocAsync((void**)&counts, sizeof(int32_t) * (ncols > 0 ? ncols : 1), s));
   SPD_CUDA(cudaMallocAsync((void**)&sorted, sizeof(int32_t) * (ncols > 0 ? ncols : 1), s));
   SPD_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (ncols > 0 ? ncols : 1), s));
-  if (!t->crd32h) SPD_CUDA(cudaMallocAsync((void**)&t->crd32h, sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
+  if (!t->crd32h_alloc) {
+    SPD_CUDA(cudaMallocAsync((void**)&t->crd32h_alloc, sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
+    t->crd32h = t->crd32h_alloc - lo;  // indexed by global position
+  }
   const unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(nnz, 256), 1), ctx->num_sms * 16);
   if (nnz > 0) {
-    k_col_count<<<grid, 256, 0, s>>>(L.crd, nnz, counts);
+    k_col_count<<<grid, 256, 0, s>>>(L.crd + lo, nnz, counts);
     SPD_CHECK_LAUNCH();
     size_t bytes = 0;
     SPD_CUDA(cub::DeviceRadixSort::SortKeysDescending(nullptr, bytes, counts, sorted, ncols, 0, 32, s));
     void* tmp = ctx->scratch[5].reserve(bytes);
     SPD_CUDA(cub::DeviceRadixSort::SortKeysDescending(tmp, bytes, counts, sorted, ncols, 0, 32, s));
-    k_crd32h<<<grid, 256, 0, s>>>(L.crd, nnz, counts, sorted, k, ncols, t->crd32h);
+    k_crd32h<<<grid, 256, 0, s>>>(L.crd + lo, nnz, counts, sorted, k, ncols, t->crd32h_alloc);
     SPD_CHECK_LAUNCH();
     ctx->launches += 3;
   }

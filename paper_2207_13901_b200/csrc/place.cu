@@ -1,0 +1,133 @@
+// Data placement on GPUs: a CSR matrix distributed over
+// the communicator's GPUs by the row or nonzero partition of its compute
+// schedule -- the matched distribution of lower_tdn + residency_from_
+// placements (/root/reference/proj/core/src/planner.cpp:361-439,
+// sim.cpp:547-566) for which the compute-time ledger charges 0 bytes
+// (SPEC.md:426).
+//
+// Every GPU receives the row pointer (O(rows): the partition step needs it,
+// and it is what the reference's preimage walks) and only its colour's
+// crd/vals positions (O(nnz / GPUs)): one NCCL broadcast and grouped
+// send/recv from the root, no host staging.  The result is a "piece"
+// tensor whose leaf arrays are indexed by global position, so the leaf ops
+// run on it unchanged for that colour.  The bytes each GPU received are
+// returned (the placement's cost, reported apart from compute).
+#include "common.cuh"
+
+namespace spd {
+
+namespace {
+
+void run_place(spd_context* ctx, int root, const spd_tensor* whole, int split, spd_tensor** out,
+               int64_t* bytes_in) {
+  checked(ctx);
+  if (!out) throw ValidationError("null output handle");
+  if (!ctx->comm) throw ValidationError("spd_tensor_place needs a communicator");
+  if (root < 0 || root >= ctx->world) throw ValidationError("root outside the communicator");
+  if (split != 1 && split != 2) throw ValidationError("split must be 1 (rows) or 2 (nonzeros)");
+  activate(ctx);
+  cudaStream_t s = ctx->stream;
+  const bool is_root = ctx->rank == root;
+  // header: order, dims (2), kinds, mode order, nnz
+  int64_t hdr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (is_root) {
+    if (!whole) throw ValidationError("the root must pass the whole tensor");
+    if (whole->piece) throw ValidationError("cannot place a piece");
+    if (whole->levels.size() != 2 || whole->levels[0].kind != SPD_DENSE ||
+        whole->levels[1].kind != SPD_COMPRESSED)
+      throw ValidationError("unsupported on gpu: placement of ds (CSR-like) matrices");
+    hdr[0] = whole->order;
+    hdr[1] = whole->dims[0];
+    hdr[2] = whole->dims[1];
+    hdr[3] = whole->mode_order[0];
+    hdr[4] = whole->mode_order[1];
+    hdr[5] = whole->levels[1].positions;
+    hdr[6] = whole->levels[1].parent_positions;
+  }
+  int64_t* dh = (int64_t*)ctx->counters.reserve(sizeof(hdr));
+  SPD_CUDA(cudaMemcpyAsync(dh, hdr, sizeof(hdr), cudaMemcpyHostToDevice, s));
+  SPD_NCCL(ncclBroadcast(dh, dh, 8, ncclInt64, root, ctx->comm, s));
+  SPD_CUDA(cudaMemcpyAsync(hdr, dh, sizeof(hdr), cudaMemcpyDeviceToHost, s));
+  SPD_CUDA(cudaStreamSynchronize(s));
+  const int64_t dims[2] = {hdr[1], hdr[2]};
+  const int kinds[2] = {SPD_DENSE, SPD_COMPRESSED};
+  const int mo[2] = {(int)hdr[3], (int)hdr[4]};
+  const int64_t nnz = hdr[5], nrows = hdr[6];
+  spd_tensor* t = make_skeleton(ctx, 2, dims, kinds, mo);
+  try {
+    t->levels[0].kind = SPD_DENSE;
+    t->levels[0].dom = {nrows};
+    t->levels[0].positions = nrows;
+    spd_level_store& L = t->levels[1];
+    L.kind = SPD_COMPRESSED;
+    L.parent_positions = nrows;
+    L.positions = nnz;
+    L.rowptr = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (nrows + 1));
+    if (is_root)
+      SPD_CUDA(cudaMemcpyAsync(L.rowptr, whole->levels[1].rowptr, sizeof(int64_t) * (nrows + 1),
+                               cudaMemcpyDeviceToDevice, s));
+    SPD_NCCL(ncclBroadcast(L.rowptr, L.rowptr, nrows + 1, ncclInt64, root, ctx->comm, s));
+    t->nvals = nnz;
+    t->piece = true;
+    set_whole_span(t);
+    // the compute partition, the same on every GPU (one colour per GPU)
+    const int rc = split == 1 ? spd_partition_universe(ctx, t, ctx->world, nullptr)
+                              : spd_partition_nonzero(ctx, t, 1, ctx->world, nullptr);
+    if (rc != SPD_OK) throw ValidationError(spd_last_error());
+    const auto& hc = host_colors(ctx);
+    const spd_range mine = hc[ctx->rank].q;
+    t->piece_lo = mine.lo;
+    t->piece_hi = mine.hi;
+    const int64_t cnt = std::max<int64_t>(mine.hi - mine.lo + 1, 0);
+    t->piece_crd = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * std::max<int64_t>(cnt, 1));
+    t->piece_vals = (double*)dev_alloc(ctx, sizeof(double) * std::max<int64_t>(cnt, 1));
+    L.crd = t->piece_crd - mine.lo;  // indexed by global position
+    t->vals = t->piece_vals - mine.lo;
+    SPD_NCCL(ncclGroupStart());
+    if (is_root) {
+      for (int r = 0; r < ctx->world; r++) {
+        const spd_range q = hc[r].q;
+        const int64_t c = q.hi - q.lo + 1;
+        if (c <= 0) continue;
+        if (r == root) {
+          SPD_CUDA(cudaMemcpyAsync(t->piece_crd, whole->levels[1].crd + q.lo, sizeof(int64_t) * c,
+                                   cudaMemcpyDeviceToDevice, s));
+          SPD_CUDA(cudaMemcpyAsync(t->piece_vals, whole->vals + q.lo, sizeof(double) * c,
+                                   cudaMemcpyDeviceToDevice, s));
+        } else {
+          SPD_NCCL(ncclSend(whole->levels[1].crd + q.lo, c, ncclInt64, r, ctx->comm, s));
+          SPD_NCCL(ncclSend(whole->vals + q.lo, c, ncclFloat64, r, ctx->comm, s));
+        }
+      }
+    } else if (cnt > 0) {
+      SPD_NCCL(ncclRecv(t->piece_crd, cnt, ncclInt64, root, ctx->comm, s));
+      SPD_NCCL(ncclRecv(t->piece_vals, cnt, ncclFloat64, root, ctx->comm, s));
+    }
+    SPD_NCCL(ncclGroupEnd());
+    SPD_CUDA(cudaStreamSynchronize(s));
+    if (bytes_in) *bytes_in = is_root ? 0 : (int64_t)sizeof(int64_t) * (nrows + 1) + 16 * cnt;
+  } catch (...) {
+    spd_tensor_destroy(t);
+    throw;
+  }
+  *out = t;
+}
+
+}  // namespace
+
+}  // namespace spd
+
+using namespace spd;
+
+extern "C" int spd_tensor_place(spd_context* ctx, int root, const spd_tensor* whole, int split,
+                                spd_tensor** piece, int64_t* bytes_in) {
+  return guarded([&] { run_place(ctx, root, whole, split, piece, bytes_in); });
+}
+
+extern "C" int spd_tensor_piece_span(const spd_tensor* t, int64_t* lo, int64_t* hi) {
+  return guarded([&] {
+    if (!t) throw ValidationError("null spd_tensor");
+    *lo = t->piece ? t->piece_lo : 0;
+    *hi = t->piece ? t->piece_hi : t->nvals - 1;
+  });
+}

@@ -357,6 +357,22 @@ class DeviceTensor:
         check(N.lib().spd_tensor_load(ctx.h, str(path).encode(), order, kinds, mo, d, C.byref(h), dout))
         return DeviceTensor(ctx, h, tuple(dout), fmt)
 
+    @staticmethod
+    def place(ctx: Context, whole, dims, fmt: FormatSpec, split: str = "nonzero", root: int = 0):
+        """Collective spd_tensor_place: this GPU's piece of a CSR matrix placed
+        by its compute partition ("row" or "nonzero"); `whole` on root only.
+        Returns (piece, bytes received)."""
+        h = C.c_void_p()
+        b = C.c_int64()
+        check(N.lib().spd_tensor_place(ctx.h, root, whole.h if whole is not None else None,
+                                       1 if split == "row" else 2, C.byref(h), C.byref(b)))
+        return DeviceTensor(ctx, h, dims, fmt), b.value
+
+    def piece_span(self):
+        lo, hi = C.c_int64(), C.c_int64()
+        check(N.lib().spd_tensor_piece_span(self.h, C.byref(lo), C.byref(hi)))
+        return lo.value, hi.value
+
     def store(self, path):
         """spd_tensor_store: write_tensor (tensor_io.cpp:145-155)."""
         check(N.lib().spd_tensor_store(self.h, str(path).encode()))

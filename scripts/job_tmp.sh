@@ -1,2 +1,3 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_pack.py -m gpu -x -q > gpurun_out/pytest_pack.log 2>&1; echo "pytest exit $?"; tail -25 gpurun_out/pytest_pack.log
+timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 scripts/mgpu_check.py > gpurun_out/mgpu2.log 2>&1; echo "mgpu exit $?"; grep -E "mgpu|MGPU|Error|error" gpurun_out/mgpu2.log | head -30
+timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -2 gpurun_out/pytest_gpu.log

@@ -84,6 +84,56 @@ def main():
                           f"{'OK' if ok else 'MISMATCH'} combines={st.combines}", flush=True)
                     failures += 0 if ok else 1
                 Bd.close()
+    # Placed operands (spd_tensor_place): every GPU holds the row pointer and
+    # only its colour's crd/vals; the leaf ops run on the pieces.
+    for schedule in ("nonzero", "row"):
+        rng = np.random.default_rng(4321)
+        n, m = 3000, 2500
+        rows = np.concatenate([np.full(30000, 5), rng.integers(0, n, 50000)])
+        cols = rng.integers(0, m, rows.shape[0])
+        vals = rng.uniform(0.5, 1.5, rows.shape[0])
+        B = H.SparseTensor.pack((n, m), H.parse_format("ds"), np.stack([rows, cols], 1), vals)
+        whole = H.DeviceTensor.upload(ctx, B) if rank == 0 else None
+        piece, nbytes = H.DeviceTensor.place(ctx, whole, (n, m), H.parse_format("ds"), schedule)
+        lo, hi = piece.piece_span()
+        Cm = K.dense(rng, (m, 32), "dd", False)
+        Cd = torch.from_numpy(Cm.vals).to(dev)
+        out = torch.zeros(n * 32, dtype=torch.float64, device=dev)
+        cols_ = (H.partition_universe(ctx, piece, world) if schedule == "row"
+                 else H.partition_nonzero(ctx, piece, 1, world))
+        H.spmm(ctx, piece, Cd, 32, out, first=rank, count=1, pieces=world)
+        W = owned_rows(cols_, B.levels[1].rowptr(), schedule, n)
+        gathered = [torch.zeros_like(out) for _ in range(world)]
+        dist.all_gather(gathered, out)
+        # SDDMM on the piece (hot-column index over the piece's positions)
+        Kd = 128
+        Cs = K.dense(rng, (n, Kd), "dd", False)
+        Ds = K.dense(rng, (Kd, m), "dd:1,0", False)
+        A = torch.zeros(len(B.vals), dtype=torch.float64, device=dev)
+        (H.partition_universe(ctx, piece, world) if schedule == "row" else H.partition_nonzero(ctx, piece, 1, world))
+        H.sddmm(ctx, piece, torch.from_numpy(Cs.vals).to(dev), torch.from_numpy(Ds.vals).to(dev), Kd, 1, Kd, A,
+                first=rank, count=1, pieces=world)
+        ga = [torch.zeros_like(A) for _ in range(world)]
+        dist.all_gather(ga, A)
+        spans = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in range(world)]
+        dist.all_gather(spans, torch.tensor([lo, hi], dtype=torch.int64, device=dev))
+        if rank == 0:
+            got = assemble([x.cpu().numpy() for x in gathered], W, 32, n)
+            want = np.asarray(oracle_exec.oracle_execute("spmm", {"B": B, "C": Cm}, schedule, world)["out"]).reshape(n, 32)
+            ok = np.all(np.abs(got - want) <= 1e-10 * np.maximum(np.abs(want), 1e-300))
+            gs = np.zeros(len(B.vals))
+            for r in range(world):
+                a, b = (int(x) for x in spans[r].cpu())
+                gs[a:b + 1] = ga[r].cpu().numpy()[a:b + 1]
+            wsd = np.asarray(oracle_exec.oracle_execute("sddmm", {"B": B, "C": Cs, "D": Ds}, schedule, world)["out"])
+            ok2 = np.all(np.abs(gs - wsd) <= 1e-10 * np.maximum(np.abs(wsd), 1e-300))
+            print(f"[mgpu world={world}] placed {schedule}: spmm {'OK' if ok else 'MISMATCH'} sddmm "
+                  f"{'OK' if ok2 else 'MISMATCH'} piece=[{lo},{hi}] bytes_in={nbytes}", flush=True)
+            failures += (0 if ok else 1) + (0 if ok2 else 1)
+        piece.close()
+        if whole is not None:
+            whole.close()
+
     # SpAdd3: every GPU assembles its row block, global pos offsets from the
     # all-gathered per-GPU nnz, pieces gathered on rank 0 with NCCL send/recv.
     for integers in (True, False):
