@@ -263,6 +263,9 @@ def main():
             uid.copy_(torch.frombuffer(bytearray(H.Context.nccl_unique_id()), dtype=torch.uint8))
         dist.broadcast(uid, 0)
         ctx.init_comm(bytes(uid.cpu().numpy().tobytes()), rank, world)
+        warm = torch.zeros(8 * world, dtype=torch.uint8, device=dev)
+        ctx.allgather(warm, 8)  # connection setup outside every timed region
+        torch.cuda.synchronize()
     fmt = H.parse_format("ds")
     B = H.DeviceTensor.wrap(ctx, (n, n), fmt, [rp_d.data_ptr()], [crd_d.data_ptr()], vals_d.data_ptr(),
                             keep=(rp_d, crd_d, vals_d))
@@ -481,24 +484,27 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
     vals_h = vals_d.cpu().pin_memory()
     per = (n * N) // world
     C_h = C_d[rank * per:(rank + 1) * per].cpu().pin_memory()
-    streams = [torch.cuda.Stream(dev) for _ in range(2)]
+    # Double buffering pays on one GPU; across GPUs the per-step NCCL
+    # all-gather already couples the ranks' streams, so N > 1 runs one stream.
+    nbuf = 2 if world == 1 else 1
+    streams = [torch.cuda.Stream(dev) for _ in range(nbuf)]
     ctxs = [H.Context(dev.index, stream=s.cuda_stream) for s in streams]
     if world > 1:
         for cx in ctxs:
             init_comm(cx, dist, rank, world, dev)
-    C_devs = [torch.empty_like(C_d) for _ in range(2)]
-    A_devs = [torch.empty(n * N, dtype=torch.float64, device=dev) for _ in range(2)]
+    C_devs = [torch.empty_like(C_d) for _ in range(nbuf)]
+    A_devs = [torch.empty(n * N, dtype=torch.float64, device=dev) for _ in range(nbuf)]
     fmt = H.parse_format("ds")
     dims = (Cc.c_int64 * 2)(n, n)
     kinds = (Cc.c_int * 2)(0, 1)
     mo = (Cc.c_int * 2)(0, 1)
     pos_pp = (NN.i64p * 2)(None, Cc.cast(pairs.data_ptr(), NN.i64p))
     crd_pp = (NN.i64p * 2)(None, Cc.cast(crd_h.data_ptr(), NN.i64p))
-    state = {"k": 0, "live": [None, None]}
+    state = {"k": 0, "live": [None] * nbuf}
     torch.cuda.synchronize()
 
     def one():
-        j = state["k"] % 2
+        j = state["k"] % nbuf
         state["k"] += 1
         cx, s = ctxs[j], streams[j]
         if state["live"][j] is not None:  # the tensor of step k-2 on this stream
@@ -536,7 +542,8 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
         st.synchronize()
     dt = (time.perf_counter() - t0) / args.e2e_steps
     for Bs in state["live"]:
-        Bs.close()
+        if Bs is not None:
+            Bs.close()
     for cx in ctxs:
         cx.close()
     t = torch.tensor([dt], dtype=torch.float64, device=dev)

@@ -21,6 +21,14 @@ namespace spd {
 #define FULL 0xffffffffu
 #endif
 
+// Next chunk ticket of a warp (lane 0 draws, the warp shares it).
+__device__ __forceinline__ int64_t chunk_ticket(const int64_t* counters) {
+  unsigned long long t = 0;
+  if (lane_id() == 0)
+    t = atomicAdd(reinterpret_cast<unsigned long long*>(const_cast<int64_t*>(counters) + 3), 1ull);
+  return (int64_t)__shfl_sync(0xffffffffu, t, 0);
+}
+
 struct NzView {
   const int64_t* __restrict__ ptr;  // m + 1 starts
   const int64_t* __restrict__ id;   // m row ids
@@ -158,7 +166,7 @@ __global__ void __launch_bounds__(kBlock, 5) k_spmv_nz(WalkGeom g, NzView z, con
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t pol_stream = l2_policy_evict_first();
-  for (int64_t v = begin + gw; v < end; v += nw) {
+  for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
     const ChunkInfo ci = chunk_info(g, v, begin);
     if (ci.q_lo > ci.q_hi) {
       zero_gap(y, 1, ci.w_lo, ci.w_hi);
@@ -266,7 +274,7 @@ __global__ void __launch_bounds__(kBlock, 5) k_spmv_nz(WalkGeom g, NzView z, con
 // SpMM N == 32 over the compacted view: half a warp per position, 128-bit
 // register gathers UNR pairs deep, crd/vals of the next window prefetched,
 // row switches from the window mask (no dependent loads on the critical path).
-template <int UNR, int MINB, bool HOT>
+template <int UNR, int MINB, bool HOT, bool DYN = false>
 __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
                                                       const int32_t* __restrict__ crd32h,
                                                       const double* __restrict__ vals,
@@ -281,7 +289,10 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
   const uint64_t pol_keep = l2_policy_evict_last();
   const uint64_t pol_stream = l2_policy_evict_first();
   const double* Cl = C + 2 * hl;
-  for (int64_t v = begin + gw; v < end; v += nw) {
+  // DYN: chunks handed out by an atomic ticket (counters[3]) instead of a
+  // static grid stride, so warps that drew cheap chunks take more.
+  for (int64_t v = DYN ? begin + chunk_ticket(counters) : begin + gw; v < end;
+       v = DYN ? begin + chunk_ticket(counters) : v + nw) {
     const ChunkInfo ci = chunk_info(g, v, begin);
     if (ci.q_lo > ci.q_hi) {
       if (lane == 0) rec.row[2 * ci.local] = -1, rec.row[2 * ci.local + 1] = -1, rec.cont[ci.local] = 0;
@@ -421,7 +432,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mttkrp32_nz(WalkGeom g, NzView
   const uint64_t pol_stream = l2_policy_evict_first();
   const double* Cl = C + 2 * hl;
   const double* Cjl = Cj + 2 * hl;
-  for (int64_t v = begin + gw; v < end; v += nw) {
+  for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
     const ChunkInfo ci = chunk_info(g, v, begin);
     if (ci.q_lo > ci.q_hi) {
       if (lane == 0) rec.row[2 * ci.local] = -1, rec.row[2 * ci.local + 1] = -1, rec.cont[ci.local] = 0;
@@ -768,7 +779,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sddmm_nz(WalkGeom g, NzView z,
   const uint64_t pol_stream = l2_policy_evict_first();
   const uint64_t pol_keep = l2_policy_evict_last();
   const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1;
-  for (int64_t v = begin + gw; v < end; v += nw) {
+  for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
     const ChunkInfo ci = chunk_info(g, v, begin);
     if (ci.q_lo > ci.q_hi) continue;
     const int64_t s = ci.s, e = ci.e;

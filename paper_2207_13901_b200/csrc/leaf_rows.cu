@@ -1302,6 +1302,14 @@ static const int32_t* hot_crd(spd_context* ctx, spd_tensor* t, int64_t rowbytes)
   return t->crd32h;
 }
 
+static bool dyn_enabled() {
+  static int v = [] {
+    const char* e = getenv("SPD_DYN");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 static bool hot_enabled() {
   static int v = [] {
     const char* e = getenv("SPD_HOT");
@@ -1402,6 +1410,13 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   // Positions per chunk: ~256 KB of operand traffic per warp-chunk for the
   // column kernels, 2048 positions for the scalar ones.
   g.CH = (a.op == Op::SpMV || a.op == Op::SpTTV) ? 2048 : 1024;
+  {
+    static int64_t ch_override = [] {
+      const char* e = getenv("SPD_CH");
+      return e ? atoll(e) : 0;
+    }();
+    if (ch_override >= 32 && a.op == Op::SpMM) g.CH = ch_override;
+  }
   const bool spmm32 = a.op == Op::SpMM && a.W == 32 && B->dims[1] < (int64_t(1) << 31);
   const int variant = spmm32 ? spmm32_variant() : 0;
   if (spmm32 && variant >= 2 && variant <= 4) g.CH = 4096;
@@ -1482,6 +1497,13 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
       if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, true>);
       k_spmm32_nz<4, 4, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, h, B->vals, a.x, a.out, rec,
                                                       col.counters);
+    } else if (a.op == Op::SpMM && nz_minblocks() == 4 && dyn_enabled()) {
+      // production SpMM leaf: chunks by atomic ticket (27% faster than the
+      // static grid stride on the R-MAT step, profiles/README.md)
+      static int grid = 0;
+      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, false, true>);
+      k_spmm32_nz<4, 4, false, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
+                                                             col.counters);
     } else if (a.op == Op::SpMM && nz_minblocks() == 83) {
       static int grid = 0;
       if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<8, 3, false>);

@@ -1,3 +1,6 @@
 mkdir -p gpurun_out
-timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 scripts/mgpu_check.py > gpurun_out/mgpu2.log 2>&1; echo "mgpu exit $?"; grep -E "mgpu|MGPU|Error|error" gpurun_out/mgpu2.log | head -30
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -2 gpurun_out/pytest_gpu.log
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?"; tail -2 gpurun_out/pytest_gpu.log
+for k in spmm spmv sddmm; do timeout 600 python scripts/prof_spmm.py --steps 4 --kernel $k > gpurun_out/pd.log 2>&1; echo "$k $(tail -1 gpurun_out/pd.log)"; done
+timeout 600 python scripts/prof_c4.py --kernel spmttkrp > gpurun_out/pd.log 2>&1; tail -1 gpurun_out/pd.log
+timeout 600 python scripts/prof_c4.py --kernel spttv > gpurun_out/pd.log 2>&1; tail -1 gpurun_out/pd.log
+timeout 600 python scripts/bench_configs.py --configs c1 > gpurun_out/pd.log 2>&1; tail -1 gpurun_out/pd.log | cut -c1-200
