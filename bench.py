@@ -441,7 +441,7 @@ def main():
                        "input_gen_s": round(t_gen, 1)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "k_spmm32_nz<4,4> (+ k_zero_empty for the empty rows)", "peak_source": peak_src,
+                         "kernel": "k_spmm32_nz<4,4,false,true> (dynamic chunk tickets; + k_zero_empty for the empty rows)", "peak_source": peak_src,
                          "bytes_per_launch": per_launch, "leaf_ms": leaf_avg},
             "clocks": clock_summary,
             "gpu_launches": launches,

@@ -291,8 +291,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
   const double* Cl = C + 2 * hl;
   // DYN: chunks handed out by an atomic ticket (counters[3]) instead of a
   // static grid stride, so warps that drew cheap chunks take more.
-  for (int64_t v = DYN ? begin + chunk_ticket(counters) : begin + gw; v < end;
-       v = DYN ? begin + chunk_ticket(counters) : v + nw) {
+  const int64_t tmax = end - begin;
+  for (int64_t t = DYN ? chunk_ticket(counters) : gw; t < tmax; t = DYN ? chunk_ticket(counters) : t + nw) {
+    const int64_t v = begin + t;
     const ChunkInfo ci = chunk_info(g, v, begin);
     if (ci.q_lo > ci.q_hi) {
       if (lane == 0) rec.row[2 * ci.local] = -1, rec.row[2 * ci.local + 1] = -1, rec.cont[ci.local] = 0;

@@ -327,15 +327,23 @@ __global__ void __launch_bounds__(kSaBlock) k_sa_mid(Csr B, Csr C, Csr D,
                                                      int64_t* __restrict__ cnt,
                                                      const int64_t* __restrict__ rpA,
                                                      int64_t* __restrict__ Acrd,
-                                                     double* __restrict__ Avals) {
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t w = gw; w < nr; w += nw) {
-    const int64_t i = rows[w];
-    const Row3 r = row3(B, C, D, i);
-    const int64_t out0 = MODE == 1 ? __ldg(rpA + i) : 0;
-    const int64_t out = merge_steps<KEY, MODE>(B, C, D, r.b0, r.b1, r.c0, r.c1, r.d0, r.d1, out0, Acrd, Avals);
-    if (MODE == 0 && lane_id() == 0) cnt[i] = out;
+                                                     double* __restrict__ Avals,
+                                                     unsigned long long* __restrict__ ticket) {
+  // batches of kMidBatch rows handed out by an atomic ticket: row lengths
+  // vary by two orders of magnitude, a static stride leaves a long tail
+  constexpr int64_t kMidBatch = 8;
+  for (;;) {
+    unsigned long long t = 0;
+    if (lane_id() == 0) t = atomicAdd(ticket, 1ull);
+    const int64_t w0 = (int64_t)__shfl_sync(0xffffffffu, t, 0) * kMidBatch;
+    if (w0 >= nr) break;
+    for (int64_t w = w0; w < min(nr, w0 + kMidBatch); w++) {
+      const int64_t i = rows[w];
+      const Row3 r = row3(B, C, D, i);
+      const int64_t out0 = MODE == 1 ? __ldg(rpA + i) : 0;
+      const int64_t out = merge_steps<KEY, MODE>(B, C, D, r.b0, r.b1, r.c0, r.c1, r.d0, r.d1, out0, Acrd, Avals);
+      if (MODE == 0 && lane_id() == 0) cnt[i] = out;
+    }
   }
 }
 
@@ -419,8 +427,9 @@ static void run_spadd3(spd_context* ctx, const spd_tensor* B, const spd_tensor* 
   int32_t* midrows = (int32_t*)ctx->scratch[1].reserve(sizeof(int32_t) * 2 * (n + 1));
   int32_t* longrows = midrows + (n + 1);
   int32_t* nlists = (int32_t*)ctx->counters.reserve(64);
+  unsigned long long* tickets = reinterpret_cast<unsigned long long*>(nlists) + 2;  // one per merge pass
   SPD_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int64_t) * (n + 1), s));
-  SPD_CUDA(cudaMemsetAsync(nlists, 0, 2 * sizeof(int32_t), s));
+  SPD_CUDA(cudaMemsetAsync(nlists, 0, 32, s));
   if (lo <= hi) {
     k_sa_count<<<grid_n(ctx, hi - lo + 1), kSaBlock, 0, s>>>(b, c, d, lo, hi, Tl, cnt, midrows, longrows,
                                                              nlists);
@@ -435,10 +444,10 @@ static void run_spadd3(spd_context* ctx, const spd_tensor* B, const spd_tensor* 
   const int lgrid = ctx->num_sms * 8;
   if (nmid > 0) {
     if (key32)
-      k_sa_mid<int, 0><<<lgrid, kSaBlock, 0, s>>>(b, c, d, midrows, nmid, cnt, nullptr, nullptr, nullptr);
+      k_sa_mid<int, 0><<<lgrid, kSaBlock, 0, s>>>(b, c, d, midrows, nmid, cnt, nullptr, nullptr, nullptr, tickets);
     else
       k_sa_mid<long long, 0><<<lgrid, kSaBlock, 0, s>>>(b, c, d, midrows, nmid, cnt, nullptr, nullptr,
-                                                        nullptr);
+                                                        nullptr, tickets);
     SPD_CHECK_LAUNCH();
     launches++;
   }
@@ -499,10 +508,11 @@ static void run_spadd3(spd_context* ctx, const spd_tensor* B, const spd_tensor* 
     launches++;
     if (nmid > 0) {
       if (key32)
-        k_sa_mid<int, 1><<<lgrid, kSaBlock, 0, s>>>(b, c, d, midrows, nmid, nullptr, rpA, Acrd, Avals);
+        k_sa_mid<int, 1><<<lgrid, kSaBlock, 0, s>>>(b, c, d, midrows, nmid, nullptr, rpA, Acrd, Avals,
+                                                    tickets + 1);
       else
         k_sa_mid<long long, 1><<<lgrid, kSaBlock, 0, s>>>(b, c, d, midrows, nmid, nullptr, rpA, Acrd,
-                                                          Avals);
+                                                          Avals, tickets + 1);
       SPD_CHECK_LAUNCH();
       launches++;
     }
