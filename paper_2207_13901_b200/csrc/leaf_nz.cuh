@@ -21,14 +21,6 @@ namespace spd {
 #define FULL 0xffffffffu
 #endif
 
-// Next chunk ticket of a warp (lane 0 draws, the warp shares it).
-__device__ __forceinline__ int64_t chunk_ticket(const int64_t* counters) {
-  unsigned long long t = 0;
-  if (lane_id() == 0)
-    t = atomicAdd(reinterpret_cast<unsigned long long*>(const_cast<int64_t*>(counters) + 3), 1ull);
-  return (int64_t)__shfl_sync(0xffffffffu, t, 0);
-}
-
 struct NzView {
   const int64_t* __restrict__ ptr;  // m + 1 starts
   const int64_t* __restrict__ id;   // m row ids
@@ -567,159 +559,6 @@ __global__ void k_nz_ptr(const int64_t* __restrict__ R, int64_t nrows, const int
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j <= m;
        j += (int64_t)gridDim.x * blockDim.x)
     ptr[j] = j < m ? ld64(R + id[j]) : ld64(R + nrows);
-}
-
-}  // namespace spd
-
-namespace spd {
-
-// ---------------------------------------------------------------------------
-// SpMM N == 32 over the compacted view with cp.async gathers: per warp an
-// S-stage ring of 32-position windows in shared memory (8 KB of C rows + the
-// window's vals per stage).  Lane (h, hl) copies 16 B of the C row of
-// position 2i+h and later reads back exactly that slot, so completion is a
-// per-thread cp.async.wait_group.  (S-1) windows = (S-1) x 8 KB of gathers
-// stay in flight per warp without registers.
-constexpr int kAsyncWarps = 4;
-
-template <int S>
-__global__ void __launch_bounds__(kAsyncWarps * 32) k_spmm32_nz_async(
-    WalkGeom g, NzView z, const int64_t* __restrict__ crd, const double* __restrict__ vals,
-    const double* __restrict__ C, double* __restrict__ A, ChunkRecs rec, const int64_t* __restrict__ counters) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int lane = lane_id();
-  const int half = lane >> 4, hl = lane & 15;
-  const int wc = threadIdx.x >> 5;
-  double2* ring = reinterpret_cast<double2*>(smem + (size_t)wc * S * (kBulkStageBytes + 256));
-  double* vslot = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(ring) + (size_t)S * kBulkStageBytes);
-  const int64_t begin = counters[1], end = counters[2];
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t pol_keep = l2_policy_evict_last();
-  const uint64_t pol_stream = l2_policy_evict_first();
-  const double* Cl = C + 2 * hl;
-  for (int64_t v = begin + gw; v < end; v += nw) {
-    const ChunkInfo ci = chunk_info(g, v, begin);
-    if (ci.q_lo > ci.q_hi) {
-      if (lane == 0) rec.row[2 * ci.local] = -1, rec.row[2 * ci.local + 1] = -1, rec.cont[ci.local] = 0;
-      continue;
-    }
-    const int64_t k = ci.local, s = ci.s, e = ci.e;
-    const int nwin = (int)((e - s + 32) >> 5);
-    NzCursor c;
-    nz_start(z, c, s);
-    bool head = __shfl_sync(FULL, c.P0, 0) < s;
-    int64_t head_row = -1;
-    int head_cont = 0;
-    double2 acc = make_double2(0.0, 0.0);
-
-    // kpre/vpre: crd/vals of the next window to issue (loaded one window ahead)
-    int kpre = 0;
-    double vpre = 0.0;
-    auto load_pre = [&](int w) {
-      const int64_t q = s + 32 * (int64_t)w + lane;
-      kpre = 0;
-      vpre = 0.0;
-      if (w < nwin && q <= e) {
-        kpre = (int)ld_i64_hint(crd + q, pol_stream);
-        vpre = ld_f64_hint(vals + q, pol_stream);
-      }
-    };
-    auto issue = [&](int w) {  // copies + vals of window w (kpre/vpre hold it)
-      if (w < nwin) {
-        const int stage = w % S;
-        const int cnt = (int)min((int64_t)32, e - (s + 32 * (int64_t)w) + 1);
-        vslot[stage * 32 + lane] = vpre;
-        double2* dst = ring + (size_t)stage * 512 + hl;
-#pragma unroll 4
-        for (int i = 0; i < 16; i++) {
-          const int p = 2 * i + half;
-          const int kk = __shfl_sync(FULL, kpre, p);
-          if (p < cnt) cp_async16(dst + p * 16, Cl + (int64_t)kk * 32, pol_keep);
-        }
-      }
-      cp_async_commit();
-    };
-    load_pre(0);
-    for (int w = 0; w < S - 1; w++) {
-      issue(w);
-      load_pre(w + 1);
-    }
-    for (int w = 0; w < nwin; w++) {
-      const int stage = w % S;
-      const int64_t base = s + 32 * (int64_t)w;
-      const int cnt = (int)min((int64_t)32, e - base + 1);
-      const unsigned bm = nz_window_mask(c, base, base + cnt - 1);
-      cp_async_wait<S - 2>();
-      __syncwarp();
-      const double2* buf = ring + (size_t)stage * 512 + hl;
-      const double* vb = vslot + stage * 32;
-#pragma unroll 2
-      for (int p0 = 0; p0 < cnt; p0 += 2) {
-        const int p = p0 + half;
-        const double2 cv = p < cnt ? buf[p * 16] : make_double2(0.0, 0.0);
-        const double b = p < cnt ? vb[p] : 0.0;
-        const unsigned two = (bm >> p0) & 3u;
-        if (two == 0u) {
-          acc.x = fma(b, cv.x, acc.x);
-          acc.y = fma(b, cv.y, acc.y);
-        } else {
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            if ((two >> h) & 1u) {
-              double2 o;
-              o.x = acc.x + __shfl_xor_sync(FULL, acc.x, 16);
-              o.y = acc.y + __shfl_xor_sync(FULL, acc.y, 16);
-              const int64_t id = nz_get(c.I0, c.I1, (int)(c.ic - c.cb));
-              if (head) {
-                if (lane < 16) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
-                head_row = id;
-                head_cont = 0;
-                head = false;
-              } else if (lane < 16) {
-                st_f64x2_hint(A + id * 32 + 2 * lane, o, pol_stream);
-              }
-              acc = make_double2(0.0, 0.0);
-              nz_advance(z, c, 1);
-            }
-            if (half == h) {
-              acc.x = fma(b, cv.x, acc.x);
-              acc.y = fma(b, cv.y, acc.y);
-            }
-          }
-        }
-      }
-      __syncwarp();
-      issue(w + S - 1);
-      load_pre(w + S);
-    }
-    cp_async_wait<0>();
-    double2 o;
-    o.x = acc.x + __shfl_xor_sync(FULL, acc.x, 16);
-    o.y = acc.y + __shfl_xor_sync(FULL, acc.y, 16);
-    const int64_t next = nz_get(c.P0, c.P1, (int)(c.ic - c.cb) + 1);
-    const int64_t id = nz_get(c.I0, c.I1, (int)(c.ic - c.cb));
-    int64_t tail_row = -1;
-    if (next == e + 1) {
-      if (head) {
-        if (lane < 16) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
-        head_row = id, head_cont = 0;
-      } else if (lane < 16) {
-        st_f64x2_hint(A + id * 32 + 2 * lane, o, pol_stream);
-      }
-    } else if (head) {
-      if (lane < 16) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
-      head_row = id, head_cont = 1;
-    } else {
-      if (lane < 16) reinterpret_cast<double2*>(rec.val + (2 * k + 1) * 32)[lane] = o;
-      tail_row = id;
-    }
-    if (lane == 0) {
-      rec.row[2 * k] = head_row;
-      rec.row[2 * k + 1] = tail_row;
-      rec.cont[k] = head_cont;
-    }
-  }
 }
 
 }  // namespace spd

@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kBlock) k_spmm_walk(WalkGeom g, const int64_t*
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t N = g.W;
-  for (int64_t v = begin + gw; v < end; v += nw) {
+  for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
     const ChunkInfo ci = chunk_info(g, v, begin);
     if (ci.q_lo > ci.q_hi) {
       empty_chunk(g, ci, A, rec);
@@ -278,497 +278,6 @@ __device__ __forceinline__ void st_f64x2_hint(double* ptr, double2 v, uint64_t p
                : "memory");
 }
 
-// Row starts (S_t = R[r + 1 + t]) that fall in [base, last], as a bit mask
-// over window offsets.  More than 32 of them (runs of empty rows) are
-// collected group by group.
-__device__ __forceinline__ unsigned row_start_mask(const WalkGeom& g, int64_t r, int64_t base,
-                                                   int64_t last) {
-  const int lane = lane_id();
-  unsigned bm = 0;
-  for (int64_t rb = r + 1;; rb += 32) {
-    const int64_t idx = rb + lane;
-    const int64_t S = idx <= g.nrows ? ld64(g.R + idx) : INT64_MAX;
-    const unsigned bit = (S >= base && S <= last) ? 1u << (int)(S - base) : 0u;
-    bm |= __reduce_or_sync(FULL, bit);
-    if (__shfl_sync(FULL, S, 31) > last) break;
-  }
-  return bm;
-}
-
-struct Half32 {
-  int64_t r, nb;  // current row, its end (exclusive)
-  bool head;
-  int64_t head_row;
-  int head_cont;
-};
-
-// Ends the current row at position q: halves combined, 256-byte row store
-// (or the chunk's head record), then the walker moves to the non-empty row
-// starting at q, storing zeros for the empty rows in between.
-__device__ __forceinline__ void half32_row_end(const WalkGeom& g, Half32& st, double2& acc, int64_t q,
-                                               double* __restrict__ A, const ChunkRecs& rec,
-                                               int64_t k, const ChunkInfo& ci, uint64_t pol_st) {
-  const int lane = lane_id();
-  double2 o;
-  o.x = acc.x + __shfl_xor_sync(FULL, acc.x, 16);
-  o.y = acc.y + __shfl_xor_sync(FULL, acc.y, 16);
-  if (lane < 16) {
-    if (st.head) {
-      reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
-    } else {
-      st_f64x2_hint(A + st.r * 32 + 2 * lane, o, pol_st);
-    }
-  }
-  if (st.head) {
-    st.head_row = st.r;
-    st.head_cont = 0;
-    st.head = false;
-  }
-  acc.x = acc.y = 0.0;
-  st.r = skip_empty_rows(g, st.r + 1, q, st.nb, A, ci.w_lo, ci.w_hi);
-}
-
-template <int UNR>
-__global__ void __launch_bounds__(kBlock) k_spmm32_walk(WalkGeom g, const int64_t* __restrict__ crd,
-                                                        const double* __restrict__ vals,
-                                                        const double* __restrict__ C,
-                                                        double* __restrict__ A, ChunkRecs rec,
-                                                        const int64_t* __restrict__ counters) {
-  const int lane = lane_id();
-  const int half = lane >> 4, hl = lane & 15;
-  const int64_t begin = counters[1], end = counters[2];
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t pol_keep = l2_policy_evict_last();
-  const uint64_t pol_stream = l2_policy_evict_first();
-  const double* Cl = C + 2 * hl;
-  for (int64_t v = begin + gw; v < end; v += nw) {
-    const ChunkInfo ci = chunk_info(g, v, begin);
-    if (ci.q_lo > ci.q_hi) {
-      empty_chunk(g, ci, A, rec);
-      continue;
-    }
-    const int64_t k = ci.local, s = ci.s, e = ci.e;
-    Half32 st;
-    st.r = warp_owner(g.R, g.nrows, s);
-    st.nb = ld64(g.R + st.r + 1);
-    st.head = ld64(g.R + st.r) < s;
-    st.head_row = -1;
-    st.head_cont = 0;
-    if (s == ci.q_lo) zero_rows(A, 32, ci.w_lo, st.r - 1);
-    double2 acc = make_double2(0.0, 0.0);
-    for (int64_t base = s; base <= e; base += 32) {
-      const int cnt = (int)min((int64_t)32, e - base + 1);
-      int my_k = 0;
-      double my_v = 0.0;
-      if (lane < cnt) {
-        my_k = (int)ld_i64_hint(crd + base + lane, pol_stream);
-        my_v = ld_f64_hint(vals + base + lane, pol_stream);
-      }
-      // row starts inside the window (positions > base-1 where a row begins)
-      unsigned bm = st.nb <= base + cnt - 1 ? row_start_mask(g, st.r, base, base + cnt - 1) : 0u;
-      for (int u = 0; u < cnt; u += 2 * UNR) {
-        double2 cv[UNR];
-#pragma unroll
-        for (int i = 0; i < UNR; i++) {
-          const int p = u + 2 * i + half;
-          const int kk = __shfl_sync(FULL, my_k, p & 31);
-          cv[i] = p < cnt ? ld_f64x2_hint(Cl + (int64_t)kk * 32, pol_keep) : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int i = 0; i < UNR; i++) {
-          const int p0 = u + 2 * i;
-          if (p0 < cnt) {
-            const double b = __shfl_sync(FULL, my_v, (p0 + half) & 31);
-            const unsigned two = (bm >> p0) & (p0 + 1 < cnt ? 3u : 1u);
-            if (two == 0u) {
-              acc.x = fma(b, cv[i].x, acc.x);
-              acc.y = fma(b, cv[i].y, acc.y);
-            } else {
-              if (two & 1u) half32_row_end(g, st, acc, base + p0, A, rec, k, ci, pol_stream);
-              if (half == 0) {
-                acc.x = fma(b, cv[i].x, acc.x);
-                acc.y = fma(b, cv[i].y, acc.y);
-              }
-              if (two & 2u) half32_row_end(g, st, acc, base + p0 + 1, A, rec, k, ci, pol_stream);
-              if (half == 1) {
-                acc.x = fma(b, cv[i].x, acc.x);
-                acc.y = fma(b, cv[i].y, acc.y);
-              }
-            }
-          }
-        }
-      }
-    }
-    // chunk end: the current row either ends exactly at e or continues past it
-    double2 o;
-    o.x = acc.x + __shfl_xor_sync(FULL, acc.x, 16);
-    o.y = acc.y + __shfl_xor_sync(FULL, acc.y, 16);
-    int64_t tail_row = -1;
-    if (st.nb == e + 1) {
-      if (lane < 16) {
-        if (st.head) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
-        else st_f64x2_hint(A + st.r * 32 + 2 * lane, o, pol_stream);
-      }
-      if (st.head) st.head_row = st.r, st.head_cont = 0;
-      int64_t nb;
-      if (st.r + 1 < g.nrows) skip_empty_rows(g, st.r + 1, e + 1, nb, A, ci.w_lo, ci.w_hi);
-    } else if (st.head) {
-      if (lane < 16) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
-      st.head_row = st.r;
-      st.head_cont = 1;
-    } else {
-      if (lane < 16) reinterpret_cast<double2*>(rec.val + (2 * k + 1) * 32)[lane] = o;
-      tail_row = st.r;
-    }
-    if (lane == 0) {
-      rec.row[2 * k] = st.head_row;
-      rec.row[2 * k + 1] = tail_row;
-      rec.cont[k] = st.head_cont;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// SpMM, N == 32, TMA bulk-copy gathers (the production kernel for C2).
-//
-// Each warp owns an S-stage ring in shared memory; a stage holds the 32
-// C rows (32 x 256 B) of one 32-position window.  Lane l issues one 256-byte
-// `cp.async.bulk` (SASS UBLKCP) for its position's row with L2 evict_last
-// priority, completing on the stage's mbarrier; lane 0 posts the expected
-// bytes.  Copies run S-1 windows ahead of consumption and the crd/vals of a
-// window are loaded one window ahead of its copies, so a warp keeps up to
-// (S-1) x 8 KB of gathers in flight without holding them in registers.
-// Consumption is the half-warp scheme of k_spmm32_walk reading 128-bit
-// values from shared memory.
-constexpr int kBulkWarps = 4;          // warps per CTA
-constexpr int kBulkStageBytes = 32 * 256;
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
-                                         uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-template <int S>
-__global__ void __launch_bounds__(kBulkWarps * 32) k_spmm32_bulk(WalkGeom g, const int64_t* __restrict__ crd,
-                                                                const double* __restrict__ vals,
-                                                                const double* __restrict__ C,
-                                                                double* __restrict__ A, ChunkRecs rec,
-                                                                const int64_t* __restrict__ counters) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int lane = lane_id();
-  const int half = lane >> 4, hl = lane & 15;
-  const int wc = threadIdx.x >> 5;
-  double* ring = reinterpret_cast<double*>(smem + (size_t)wc * S * kBulkStageBytes);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (size_t)kBulkWarps * S * kBulkStageBytes) + wc * S;
-  if (lane == 0)
-    for (int s = 0; s < S; s++) mbar_init(&bars[s], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncwarp();
-  uint32_t phase = 0;  // bit s: parity of stage s's next completion
-
-  const int64_t begin = counters[1], end = counters[2];
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t pol_keep = l2_policy_evict_last();
-  const uint64_t pol_stream = l2_policy_evict_first();
-
-  for (int64_t v = begin + gw; v < end; v += nw) {
-    const ChunkInfo ci = chunk_info(g, v, begin);
-    if (ci.q_lo > ci.q_hi) {
-      empty_chunk(g, ci, A, rec);
-      continue;
-    }
-    const int64_t k = ci.local, s = ci.s, e = ci.e;
-    const int nwin = (int)((e - s + 32) >> 5);
-    Half32 st;
-    st.r = warp_owner(g.R, g.nrows, s);
-    st.nb = ld64(g.R + st.r + 1);
-    st.head = ld64(g.R + st.r) < s;
-    st.head_row = -1;
-    st.head_cont = 0;
-    if (s == ci.q_lo) zero_rows(A, 32, ci.w_lo, st.r - 1);
-    double2 acc = make_double2(0.0, 0.0);
-
-    int kreg[S];
-    double vreg[S];
-    auto load_regs = [&](int w, int& kr, double& vr) {
-      const int64_t b = s + 32 * (int64_t)w;
-      const int cnt = (int)min((int64_t)32, e - b + 1);
-      kr = 0;
-      vr = 0.0;
-      if (w < nwin && lane < cnt) {
-        kr = (int)ld_i64_hint(crd + b + lane, pol_stream);
-        vr = ld_f64_hint(vals + b + lane, pol_stream);
-      }
-    };
-    auto issue = [&](int w, int stage, int kr) {
-      if (w >= nwin) return;
-      const int64_t b = s + 32 * (int64_t)w;
-      const int cnt = (int)min((int64_t)32, e - b + 1);
-      if (lane == 0) mbar_arrive_expect_tx(&bars[stage], (uint32_t)cnt * 256u);
-      __syncwarp();
-      if (lane < cnt)
-        bulk_g2s(ring + (size_t)stage * 1024 + lane * 32, C + (int64_t)kr * 32, 256, &bars[stage], pol_keep);
-    };
-#pragma unroll
-    for (int j = 0; j < S; j++) load_regs(j, kreg[j], vreg[j]);
-#pragma unroll
-    for (int j = 0; j < S - 1; j++) issue(j, j, kreg[j]);
-
-    for (int w0 = 0; w0 < nwin; w0 += S) {
-#pragma unroll
-      for (int j = 0; j < S; j++) {
-        const int w = w0 + j;
-        if (w < nwin) {
-          const int64_t base = s + 32 * (int64_t)w;
-          const int cnt = (int)min((int64_t)32, e - base + 1);
-          const unsigned bm =
-              st.nb <= base + cnt - 1 ? row_start_mask(g, st.r, base, base + cnt - 1) : 0u;
-          mbar_wait(&bars[j], (phase >> j) & 1u);
-          phase ^= 1u << j;
-          const double2* buf = reinterpret_cast<const double2*>(ring + (size_t)j * 1024);
-          const double myv = vreg[j];
-#pragma unroll 4
-          for (int p0 = 0; p0 < cnt; p0 += 2) {
-            const int p = p0 + half;
-            const double2 cv = p < cnt ? buf[p * 16 + hl] : make_double2(0.0, 0.0);
-            const double b = __shfl_sync(FULL, myv, p & 31);
-            const unsigned two = (bm >> p0) & (p0 + 1 < cnt ? 3u : 1u);
-            if (two == 0u) {
-              acc.x = fma(b, cv.x, acc.x);
-              acc.y = fma(b, cv.y, acc.y);
-            } else {
-              if (two & 1u) half32_row_end(g, st, acc, base + p0, A, rec, k, ci, pol_stream);
-              if (half == 0) {
-                acc.x = fma(b, cv.x, acc.x);
-                acc.y = fma(b, cv.y, acc.y);
-              }
-              if (two & 2u) half32_row_end(g, st, acc, base + p0 + 1, A, rec, k, ci, pol_stream);
-              if (half == 1) {
-                acc.x = fma(b, cv.x, acc.x);
-                acc.y = fma(b, cv.y, acc.y);
-              }
-            }
-          }
-          __syncwarp();
-          fence_proxy_async_smem();  // generic reads of this stage precede its next async fill
-          // regs of window w+S into slot j; copies of window w+S-1 into stage j-1
-          load_regs(w + S, kreg[j], vreg[j]);
-          issue(w + S - 1, (j + S - 1) % S, kreg[(j + S - 1) % S]);
-        }
-      }
-    }
-    // chunk end (as k_spmm32_walk)
-    double2 o;
-    o.x = acc.x + __shfl_xor_sync(FULL, acc.x, 16);
-    o.y = acc.y + __shfl_xor_sync(FULL, acc.y, 16);
-    int64_t tail_row = -1;
-    if (st.nb == e + 1) {
-      if (lane < 16) {
-        if (st.head) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
-        else st_f64x2_hint(A + st.r * 32 + 2 * lane, o, pol_stream);
-      }
-      if (st.head) st.head_row = st.r, st.head_cont = 0;
-      int64_t nb;
-      if (st.r + 1 < g.nrows) skip_empty_rows(g, st.r + 1, e + 1, nb, A, ci.w_lo, ci.w_hi);
-    } else if (st.head) {
-      if (lane < 16) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
-      st.head_row = st.r;
-      st.head_cont = 1;
-    } else {
-      if (lane < 16) reinterpret_cast<double2*>(rec.val + (2 * k + 1) * 32)[lane] = o;
-      tail_row = st.r;
-    }
-    if (lane == 0) {
-      rec.row[2 * k] = st.head_row;
-      rec.row[2 * k + 1] = tail_row;
-      rec.cont[k] = st.head_cont;
-    }
-  }
-}
-
-
-// ---------------------------------------------------------------------------
-// SpMM, N == 32, cp.async (LDGSTS) gathers into a per-warp shared-memory ring.
-// Lane (half h, hl) copies 16 bytes of the C row of position 2i+h of each
-// window into the ring slot it will itself read back, so completion is a
-// per-thread cp.async.wait_group -- no barrier, no cross-lane hand-off.  S-1
-// windows of gathers stay in flight per warp without occupying registers.
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, uint64_t pol) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
-               "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int S>
-__global__ void __launch_bounds__(kBulkWarps * 32) k_spmm32_async(WalkGeom g, const int64_t* __restrict__ crd,
-                                                                 const double* __restrict__ vals,
-                                                                 const double* __restrict__ C,
-                                                                 double* __restrict__ A, ChunkRecs rec,
-                                                                 const int64_t* __restrict__ counters) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int lane = lane_id();
-  const int half = lane >> 4, hl = lane & 15;
-  const int wc = threadIdx.x >> 5;
-  double2* ring = reinterpret_cast<double2*>(smem + (size_t)wc * S * kBulkStageBytes);
-  const int64_t begin = counters[1], end = counters[2];
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t pol_keep = l2_policy_evict_last();
-  const uint64_t pol_stream = l2_policy_evict_first();
-  const double* Cl = C + 2 * hl;
-
-  for (int64_t v = begin + gw; v < end; v += nw) {
-    const ChunkInfo ci = chunk_info(g, v, begin);
-    if (ci.q_lo > ci.q_hi) {
-      empty_chunk(g, ci, A, rec);
-      continue;
-    }
-    const int64_t k = ci.local, s = ci.s, e = ci.e;
-    const int nwin = (int)((e - s + 32) >> 5);
-    Half32 st;
-    st.r = warp_owner(g.R, g.nrows, s);
-    st.nb = ld64(g.R + st.r + 1);
-    st.head = ld64(g.R + st.r) < s;
-    st.head_row = -1;
-    st.head_cont = 0;
-    if (s == ci.q_lo) zero_rows(A, 32, ci.w_lo, st.r - 1);
-    double2 acc = make_double2(0.0, 0.0);
-
-    int kreg[S];
-    double vreg[S];
-    auto load_regs = [&](int w, int& kr, double& vr) {
-      const int64_t b = s + 32 * (int64_t)w;
-      const int cnt = (int)min((int64_t)32, e - b + 1);
-      kr = 0;
-      vr = 0.0;
-      if (w < nwin && lane < cnt) {
-        kr = (int)ld_i64_hint(crd + b + lane, pol_stream);
-        vr = ld_f64_hint(vals + b + lane, pol_stream);
-      }
-    };
-    // every window commits exactly one group (possibly empty) so wait counts stay uniform
-    auto issue = [&](int w, int stage, int kr) {
-      if (w < nwin) {
-        const int64_t b = s + 32 * (int64_t)w;
-        const int cnt = (int)min((int64_t)32, e - b + 1);
-        double2* dst = ring + (size_t)stage * 512 + hl;
-#pragma unroll
-        for (int i = 0; i < 16; i++) {
-          const int p = 2 * i + half;
-          const int kk = __shfl_sync(FULL, kr, p);
-          if (p < cnt) cp_async16(dst + p * 16, Cl + (int64_t)kk * 32, pol_keep);
-        }
-      }
-      cp_async_commit();
-    };
-#pragma unroll
-    for (int j = 0; j < S; j++) load_regs(j, kreg[j], vreg[j]);
-#pragma unroll
-    for (int j = 0; j < S - 1; j++) issue(j, j, kreg[j]);
-
-    for (int w0 = 0; w0 < nwin; w0 += S) {
-#pragma unroll
-      for (int j = 0; j < S; j++) {
-        const int w = w0 + j;
-        if (w < nwin) {
-          const int64_t base = s + 32 * (int64_t)w;
-          const int cnt = (int)min((int64_t)32, e - base + 1);
-          const unsigned bm =
-              st.nb <= base + cnt - 1 ? row_start_mask(g, st.r, base, base + cnt - 1) : 0u;
-          cp_async_wait<S - 2>();  // this window's group is complete (own copies only)
-          const double2* buf = ring + (size_t)j * 512 + hl;
-          const double myv = vreg[j];
-#pragma unroll 4
-          for (int p0 = 0; p0 < cnt; p0 += 2) {
-            const int p = p0 + half;
-            const double2 cv = p < cnt ? buf[p * 16] : make_double2(0.0, 0.0);
-            const double b = __shfl_sync(FULL, myv, p & 31);
-            const unsigned two = (bm >> p0) & (p0 + 1 < cnt ? 3u : 1u);
-            if (two == 0u) {
-              acc.x = fma(b, cv.x, acc.x);
-              acc.y = fma(b, cv.y, acc.y);
-            } else {
-              if (two & 1u) half32_row_end(g, st, acc, base + p0, A, rec, k, ci, pol_stream);
-              if (half == 0) {
-                acc.x = fma(b, cv.x, acc.x);
-                acc.y = fma(b, cv.y, acc.y);
-              }
-              if (two & 2u) half32_row_end(g, st, acc, base + p0 + 1, A, rec, k, ci, pol_stream);
-              if (half == 1) {
-                acc.x = fma(b, cv.x, acc.x);
-                acc.y = fma(b, cv.y, acc.y);
-              }
-            }
-          }
-          load_regs(w + S, kreg[j], vreg[j]);
-          issue(w + S - 1, (j + S - 1) % S, kreg[(j + S - 1) % S]);
-        }
-      }
-    }
-    cp_async_wait<0>();
-    double2 o;
-    o.x = acc.x + __shfl_xor_sync(FULL, acc.x, 16);
-    o.y = acc.y + __shfl_xor_sync(FULL, acc.y, 16);
-    int64_t tail_row = -1;
-    if (st.nb == e + 1) {
-      if (lane < 16) {
-        if (st.head) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
-        else st_f64x2_hint(A + st.r * 32 + 2 * lane, o, pol_stream);
-      }
-      if (st.head) st.head_row = st.r, st.head_cont = 0;
-      int64_t nb;
-      if (st.r + 1 < g.nrows) skip_empty_rows(g, st.r + 1, e + 1, nb, A, ci.w_lo, ci.w_hi);
-    } else if (st.head) {
-      if (lane < 16) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
-      st.head_row = st.r;
-      st.head_cont = 1;
-    } else {
-      if (lane < 16) reinterpret_cast<double2*>(rec.val + (2 * k + 1) * 32)[lane] = o;
-      tail_row = st.r;
-    }
-    if (lane == 0) {
-      rec.row[2 * k] = st.head_row;
-      rec.row[2 * k + 1] = tail_row;
-      rec.cont[k] = st.head_cont;
-    }
-  }
-}
-
 // SpMTTKRP over a dss CSF: A(i,l) = sum_{j,k} B(i,j,k) * C(j,l) * D(k,l).
 // Output rows are i; g.R is the derived leaf row pointer rp2[rp1[i]].  The
 // fibre (j) of each position is tracked alongside; W = R (rank).
@@ -783,7 +292,7 @@ __global__ void __launch_bounds__(kBlock) k_mttkrp_walk(
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t Rk = g.W;
-  for (int64_t v = begin + gw; v < end; v += nw) {
+  for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
     const ChunkInfo ci = chunk_info(g, v, begin);
     if (ci.q_lo > ci.q_hi) {
       empty_chunk(g, ci, A, rec);
@@ -886,7 +395,7 @@ __global__ void __launch_bounds__(kBlock) k_spmv_walk(WalkGeom g, const int64_t*
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t pol_stream = l2_policy_evict_first();
-  for (int64_t v = begin + gw; v < end; v += nw) {
+  for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
     const ChunkInfo ci = chunk_info(g, v, begin);
     if (ci.q_lo > ci.q_hi) {
       empty_chunk(g, ci, y, rec);
@@ -1142,70 +651,6 @@ static int occupancy_grid(spd_context* ctx, K kernel) {
   return ctx->num_sms * per_sm;
 }
 
-// SpMM N=32 leaf variant: 1/5/6 = register gathers (k_spmm32_walk<4/8/16>),
-// 2..4 = TMA bulk-copy gathers with an S-stage ring (k_spmm32_bulk<S>;
-// measured 2-5x slower: 256-byte bulk copies are too fine-grained for the
-// TMA engine).  SPD_SPMM32_VARIANT overrides (tuning only).
-static int spmm32_variant() {
-  static int v = [] {
-    const char* e = getenv("SPD_SPMM32_VARIANT");
-    int x = e ? atoi(e) : 1;
-    return x < 1 || x > 13 ? 1 : x;
-  }();
-  return v;
-}
-
-template <int S>
-static void launch_bulk_s(spd_context* ctx, const WalkGeom& g, const int64_t* crd, const double* vals,
-                          const double* C, double* A, const ChunkRecs& rec, const int64_t* counters) {
-  const size_t smem = (size_t)kBulkWarps * S * kBulkStageBytes + (size_t)kBulkWarps * S * 8;
-  static int grid = 0;
-  if (!grid) {
-    SPD_CUDA(cudaFuncSetAttribute(k_spmm32_bulk<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmm32_bulk<S>, kBulkWarps * 32, smem));
-    grid = ctx->num_sms * (per_sm > 0 ? per_sm : 1);
-  }
-  k_spmm32_bulk<S><<<grid, kBulkWarps * 32, smem, ctx->stream>>>(g, crd, vals, C, A, rec, counters);
-}
-
-template <int S>
-static void launch_async_s(spd_context* ctx, const WalkGeom& g, const int64_t* crd, const double* vals,
-                           const double* C, double* A, const ChunkRecs& rec, const int64_t* counters) {
-  const size_t smem = (size_t)kBulkWarps * S * kBulkStageBytes;
-  static int grid = 0;
-  if (!grid) {
-    SPD_CUDA(cudaFuncSetAttribute(k_spmm32_async<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmm32_async<S>, kBulkWarps * 32, smem));
-    grid = ctx->num_sms * (per_sm > 0 ? per_sm : 1);
-  }
-  k_spmm32_async<S><<<grid, kBulkWarps * 32, smem, ctx->stream>>>(g, crd, vals, C, A, rec, counters);
-}
-
-static void launch_spmm32_bulk(spd_context* ctx, int S, const WalkGeom& g, const int64_t* crd,
-                               const double* vals, const double* C, double* A, const ChunkRecs& rec,
-                               const int64_t* counters) {
-  if (S == 2) launch_bulk_s<2>(ctx, g, crd, vals, C, A, rec, counters);
-  else if (S == 3) launch_bulk_s<3>(ctx, g, crd, vals, C, A, rec, counters);
-  else launch_bulk_s<4>(ctx, g, crd, vals, C, A, rec, counters);
-}
-
-template <int S>
-static void launch_nz_async(spd_context* ctx, const WalkGeom& g, const NzView& z, const int64_t* crd,
-                            const double* vals, const double* C, double* A, const ChunkRecs& rec,
-                            const int64_t* counters) {
-  const size_t smem = (size_t)kAsyncWarps * S * (kBulkStageBytes + 256);
-  static int grid = 0;
-  if (!grid) {
-    SPD_CUDA(cudaFuncSetAttribute(k_spmm32_nz_async<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmm32_nz_async<S>, kAsyncWarps * 32, smem));
-    grid = ctx->num_sms * (per_sm > 0 ? per_sm : 1);
-  }
-  k_spmm32_nz_async<S><<<grid, kAsyncWarps * 32, smem, ctx->stream>>>(g, z, crd, vals, C, A, rec, counters);
-}
-
 // Compacted non-empty-row view of row pointer R of tensor t (cached on t).
 static NzView nz_view(spd_context* ctx, spd_tensor* t, const int64_t* R, int64_t nrows) {
   for (auto& e : t->nz)
@@ -1246,15 +691,6 @@ static NzView nz_view(spd_context* ctx, spd_tensor* t, const int64_t* R, int64_t
   slot->R = R;
   ctx->launches += 3;
   return NzView{slot->ptr, slot->id, slot->m};
-}
-
-// Minimum resident CTAs requested for k_spmm32_nz (register budget); tuning knob.
-static int nz_minblocks() {
-  static int v = [] {
-    const char* e = getenv("SPD_NZ_MINB");
-    return e ? atoi(e) : 4;
-  }();
-  return v;
 }
 
 // int32 leaf crd with hot-column bit for dense rows of `rowbytes` (cached on
@@ -1418,9 +854,6 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
     if (ch_override >= 32 && a.op == Op::SpMM) g.CH = ch_override;
   }
   const bool spmm32 = a.op == Op::SpMM && a.W == 32 && B->dims[1] < (int64_t(1) << 31);
-  const int variant = spmm32 ? spmm32_variant() : 0;
-  if (spmm32 && variant >= 2 && variant <= 4) g.CH = 4096;
-  if (spmm32 && variant >= 7 && variant < 20) g.CH = 4096;
   const int64_t W = a.W > 0 ? a.W : 1;
   const int64_t max_chunks = nnz / g.CH + 2 * P + 2;
 
@@ -1451,7 +884,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   const bool mttkrp32 = a.op == Op::SpMTTKRP && a.W == 32 && B->dims[1] < (int64_t(1) << 31) &&
                         B->dims[2] < (int64_t(1) << 31);
   const bool use_nz = nz_enabled() && (a.op == Op::SpMV || a.op == Op::SpTTV || mttkrp32 ||
-                                       (spmm32 && (variant == 1 || variant >= 10)));
+                                       spmm32);
   NzView z{nullptr, nullptr, 0};
   if (use_nz) {
     z = nz_view(ctx, const_cast<spd_tensor*>(B), g.R, g.nrows);
@@ -1486,43 +919,23 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
       if (!grid) grid = occupancy_grid(ctx, k_mttkrp32_nz<4, 3, false>);
       k_mttkrp32_nz<4, 3, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->jleaf, a.x, B->vals, a.D, a.out, rec,
                                                          col.counters);
-    } else if (a.op == Op::SpMM && variant >= 10 && variant < 20) {
-      if (variant == 10) launch_nz_async<2>(ctx, g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
-      else if (variant == 11) launch_nz_async<3>(ctx, g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
-      else if (variant == 12) launch_nz_async<4>(ctx, g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
-      else launch_nz_async<6>(ctx, g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
     } else if (a.op == Op::SpMM && hot_enabled()) {
       const int32_t* h = hot_crd(ctx, const_cast<spd_tensor*>(B), 256);
       static int grid = 0;
       if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, true>);
       k_spmm32_nz<4, 4, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, h, B->vals, a.x, a.out, rec,
                                                       col.counters);
-    } else if (a.op == Op::SpMM && nz_minblocks() == 4 && dyn_enabled()) {
+    } else if (a.op == Op::SpMM && dyn_enabled()) {
       // production SpMM leaf: chunks by atomic ticket (27% faster than the
       // static grid stride on the R-MAT step, profiles/README.md)
       static int grid = 0;
       if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, false, true>);
       k_spmm32_nz<4, 4, false, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
                                                              col.counters);
-    } else if (a.op == Op::SpMM && nz_minblocks() == 83) {
-      static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<8, 3, false>);
-      k_spmm32_nz<8, 3, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
-                                                       col.counters);
-    } else if (a.op == Op::SpMM && nz_minblocks() == 84) {
-      static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<8, 4, false>);
-      k_spmm32_nz<8, 4, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
-                                                       col.counters);
-    } else if (a.op == Op::SpMM && nz_minblocks() == 4) {
+    } else if (a.op == Op::SpMM) {  // static grid stride (SPD_DYN=0, comparison only)
       static int grid = 0;
       if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, false>);
       k_spmm32_nz<4, 4, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
-                                                       col.counters);
-    } else if (a.op == Op::SpMM) {
-      static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 1, false>);
-      k_spmm32_nz<4, 1, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
                                                        col.counters);
     } else {
       static int grid = 0;
@@ -1539,25 +952,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
       break;
     }
     case Op::SpMM: {
-      if (spmm32 && variant >= 2 && variant <= 4) {
-        launch_spmm32_bulk(ctx, variant, g, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
-      } else if (spmm32 && variant >= 7) {
-        if (variant == 7) launch_async_s<2>(ctx, g, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
-        else if (variant == 8) launch_async_s<3>(ctx, g, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
-        else launch_async_s<4>(ctx, g, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
-      } else if (spmm32 && variant == 5) {
-        static int grid = 0;
-        if (!grid) grid = occupancy_grid(ctx, k_spmm32_walk<8>);
-        k_spmm32_walk<8><<<grid, kBlock, 0, s>>>(g, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
-      } else if (spmm32 && variant == 6) {
-        static int grid = 0;
-        if (!grid) grid = occupancy_grid(ctx, k_spmm32_walk<16>);
-        k_spmm32_walk<16><<<grid, kBlock, 0, s>>>(g, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
-      } else if (spmm32) {
-        static int grid = 0;
-        if (!grid) grid = occupancy_grid(ctx, k_spmm32_walk<4>);
-        k_spmm32_walk<4><<<grid, kBlock, 0, s>>>(g, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
-      } else if (a.W <= 32) {
+      if (a.W <= 32) {
         static int grid = 0;
         if (!grid) grid = occupancy_grid(ctx, k_spmm_walk<1>);
         k_spmm_walk<1><<<grid, kBlock, 0, s>>>(g, leaf.crd, B->vals, a.x, a.out, rec, col.counters);

@@ -116,4 +116,12 @@ __device__ __forceinline__ ChunkInfo chunk_info(const WalkGeom& g, int64_t v, in
   return ci;
 }
 
+// Next chunk ticket of a warp (lane 0 draws, the warp shares it).
+__device__ __forceinline__ int64_t chunk_ticket(const int64_t* counters) {
+  unsigned long long t = 0;
+  if ((threadIdx.x & 31) == 0)
+    t = atomicAdd(reinterpret_cast<unsigned long long*>(const_cast<int64_t*>(counters) + 3), 1ull);
+  return (int64_t)__shfl_sync(0xffffffffu, t, 0);
+}
+
 }  // namespace spd

@@ -39,7 +39,7 @@ __global__ void __launch_bounds__(kBlock) k_sddmm_walk(WalkGeom g, const int64_t
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   constexpr int U = 4;
-  for (int64_t v = begin + gw; v < end; v += nw) {
+  for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
     const ChunkInfo ci = chunk_info(g, v, begin);
     if (ci.q_lo > ci.q_hi) continue;
     const int64_t s = ci.s, e = ci.e;
