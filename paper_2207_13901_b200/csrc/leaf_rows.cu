@@ -922,9 +922,9 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
     } else if (a.op == Op::SpMM && hot_enabled()) {
       const int32_t* h = hot_crd(ctx, const_cast<spd_tensor*>(B), 256);
       static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, true>);
-      k_spmm32_nz<4, 4, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, h, B->vals, a.x, a.out, rec,
-                                                      col.counters);
+      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, true, true>);
+      k_spmm32_nz<4, 4, true, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, h, B->vals, a.x, a.out, rec,
+                                                            col.counters);
     } else if (a.op == Op::SpMM && dyn_enabled()) {
       // production SpMM leaf: chunks by atomic ticket (27% faster than the
       // static grid stride on the R-MAT step, profiles/README.md)
