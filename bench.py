@@ -353,24 +353,28 @@ def main():
         return float(t[0]), float(t[1]), nl, (sampler.summary() if sampler else None)
 
     ms, leaf_avg, launches, clock_summary = measure(step, args.steps, args.warmup, True)
-    if args.trace:  # phase breakdown of the step on every rank (outside the timed region)
-        ctx.timing(2)
-        for _ in range(4):
-            step()
-        d = np.asarray(ctx.read_timing())
-        ctx.timing(False)
-        names = ["memset+setup", "zero", "leaf", "fixup", "allgather", "combine", "partition+gaps"]
-        per = d[: (len(d) // 7) * 7].reshape(-1, 7)[:-1].mean(axis=0) if len(d) >= 14 else d
-        t = torch.tensor(per, dtype=torch.float64, device=dev)
-        allt = [torch.zeros_like(t) for _ in range(world)]
-        if world > 1:
-            dist.all_gather(allt, t)
-        else:
-            allt = [t]
-        if rank == 0:
-            for r, v in enumerate(allt):
-                print(f"[trace rank {r}] " + " ".join(f"{k}={x * 1e3:.1f}us" for k, x in zip(names, v.cpu().numpy())),
-                      file=sys.stderr, flush=True)
+    # Phase breakdown of the step (outside the timed region): partition,
+    # setup, zero-fill, leaf, chunk fixup, NCCL all-gather, colour combine --
+    # CUDA-event markers on every rank, reported as the max over ranks
+    # (`--trace` also prints every rank's row).
+    ctx.timing(2)
+    for _ in range(4):
+        step()
+    d = np.asarray(ctx.read_timing())
+    ctx.timing(False)
+    names = ["setup", "zero_fill", "leaf", "fixup", "allgather", "combine", "partition_and_gaps"]
+    per = d[: (len(d) // 7) * 7].reshape(-1, 7)[:-1].mean(axis=0) if len(d) >= 14 else np.zeros(7)
+    t = torch.tensor(per, dtype=torch.float64, device=dev)
+    allt = [torch.zeros_like(t) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(allt, t)
+    else:
+        allt = [t]
+    phases = {k: float(max(float(v[i]) for v in allt)) for i, k in enumerate(names)}
+    if args.trace and rank == 0:
+        for r, v in enumerate(allt):
+            print(f"[trace rank {r}] " + " ".join(f"{k}={x * 1e3:.1f}us" for k, x in zip(names, v.cpu().numpy())),
+                  file=sys.stderr, flush=True)
 
     # Secondary: SpMV on the same R-MAT (the metric names SpMV and SpMM).
     x_d = torch.from_numpy(dense_vals(n, args.seed + 2)).to(dev) if rank == 0 else torch.empty(n, dtype=torch.float64, device=dev)
@@ -442,7 +446,9 @@ def main():
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": "k_spmm32_nz<4,4,false,true> (dynamic chunk tickets; + k_zero_empty for the empty rows)", "peak_source": peak_src,
-                         "bytes_per_launch": per_launch, "leaf_ms": leaf_avg},
+                         "bytes_per_launch": per_launch, "leaf_ms": leaf_avg,
+                         "frac_vs_8tbs_nominal": (achieved / 8000.0) if achieved else None},
+            "phases_ms_max_over_ranks": phases,
             "clocks": clock_summary,
             "gpu_launches": launches,
             "placement": placement,

@@ -256,6 +256,16 @@ int spd_gather_rows(spd_context* ctx, const spd_tensor* A, int root, spd_tensor*
  * entries. */
 int spd_last_work(spd_context* ctx, int64_t* work, int64_t pieces);
 
+/* CUDA graphs: capture the ops enqueued on `ctx` between begin and end
+ * (e.g. spd_partition_* with colors_out NULL + a leaf op with stats NULL)
+ * and replay them with one launch.  The context must own an explicit
+ * stream.  Ops that need a host read-back fail the capture. */
+typedef struct spd_graph spd_graph;
+int spd_capture_begin(spd_context* ctx);
+int spd_capture_end(spd_context* ctx, spd_graph** out);
+int spd_graph_launch(spd_graph* g, spd_context* ctx);
+int spd_graph_destroy(spd_graph* g);
+
 /* ---- (5) instrumentation ----------------------------------------------- */
 /* Records a CUDA-event pair around every leaf kernel launched on the
  * context's stream while enabled (no host synchronisation). */

@@ -90,6 +90,10 @@ SIGNATURES = {
     "spd_tensor_store": (C.c_int, [vp, C.c_char_p]),
     "spd_tensor_place": (C.c_int, [vp, C.c_int, vp, C.c_int, C.POINTER(vp), i64p]),
     "spd_tensor_piece_span": (C.c_int, [vp, i64p, i64p]),
+    "spd_capture_begin": (C.c_int, [vp]),
+    "spd_capture_end": (C.c_int, [vp, C.POINTER(vp)]),
+    "spd_graph_launch": (C.c_int, [vp, vp]),
+    "spd_graph_destroy": (C.c_int, [vp]),
     "spd_tensor_pack": (C.c_int, [vp, C.c_int, i64p, C.POINTER(C.c_int), C.POINTER(C.c_int), i64,
                                   C.POINTER(i64p), dblp, C.c_int, C.POINTER(vp)]),
     "spd_last_work": (C.c_int, [vp, i64p, i64]),

@@ -685,3 +685,71 @@ int spd_last_work(spd_context* ctx, int64_t* work, int64_t pieces) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// CUDA graphs: a sequence of ops on a context (partition + leaf + combine of
+// a step) captured once and replayed, so launch-bound small problems pay one
+// graph launch instead of a dozen host API calls per step.  Ops stay
+// capturable as long as they need no host read-back: colours kept on the
+// device (colors_out NULL), stats NULL, derived indices already built.
+struct spd_graph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+extern "C" {
+
+int spd_capture_begin(spd_context* ctx) {
+  return guarded([&] {
+    checked(ctx);
+    if (ctx->stream == nullptr || ctx->stream == cudaStreamLegacy || ctx->stream == cudaStreamPerThread)
+      throw ValidationError("capture needs a context on an explicit stream (not the legacy default stream)");
+    activate(ctx);
+    SPD_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+  });
+}
+
+int spd_capture_end(spd_context* ctx, spd_graph** out) {
+  return guarded([&] {
+    checked(ctx);
+    if (!out) throw ValidationError("null output handle");
+    activate(ctx);
+    auto* g = new spd_graph();
+    cudaError_t e = cudaStreamEndCapture(ctx->stream, &g->graph);
+    if (e != cudaSuccess) {
+      if (g->graph) cudaGraphDestroy(g->graph);
+      delete g;
+      (void)cudaGetLastError();  // an invalidated capture is not a sticky error: clear it
+      throw RuntimeError(std::string("stream capture failed (an op needed a host read-back?): ") +
+                         cudaGetErrorString(e));
+    }
+    e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+    if (e != cudaSuccess) {
+      cudaGraphDestroy(g->graph);
+      delete g;
+      SPD_CUDA(e);
+    }
+    *out = g;
+  });
+}
+
+int spd_graph_launch(spd_graph* g, spd_context* ctx) {
+  return guarded([&] {
+    checked(ctx);
+    if (!g) throw ValidationError("null spd_graph");
+    activate(ctx);
+    SPD_CUDA(cudaGraphLaunch(g->exec, ctx->stream));
+    ctx->launches += 1;
+  });
+}
+
+int spd_graph_destroy(spd_graph* g) {
+  return guarded([&] {
+    if (!g) return;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    if (g->graph) cudaGraphDestroy(g->graph);
+    delete g;
+  });
+}
+
+}  // extern "C"

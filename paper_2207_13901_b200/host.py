@@ -239,6 +239,27 @@ class Context:
         buf = C.create_string_buffer(unique_id, 128)
         check(N.lib().spd_context_init_comm(self.h, buf, rank, world))
 
+    def capture(self):
+        """Context manager: the ops enqueued inside become a Graph
+        (spd_capture_begin/end) replayed with Graph.launch()."""
+        ctx = self
+
+        class _Capture:
+            def __enter__(self_):
+                check(N.lib().spd_capture_begin(ctx.h))
+                self_.graph = None
+                return self_
+
+            def __exit__(self_, exc_type, *rest):
+                h = C.c_void_p()
+                rc = N.lib().spd_capture_end(ctx.h, C.byref(h))
+                if exc_type is None:
+                    check(rc)
+                    self_.graph = Graph(ctx, h)
+                return False
+
+        return _Capture()
+
     def allgather(self, dev_buf, bytes_per_rank: int):
         """In-place NCCL all-gather of a device buffer (spd_allgather)."""
         check(N.lib().spd_allgather(self.h, _ptr(dev_buf), int(bytes_per_rank)))
@@ -283,6 +304,27 @@ def _format_arrays(dims, fmt: FormatSpec):
     kinds = (C.c_int * order)(*[N.SPD_DENSE if k == DENSE else N.SPD_COMPRESSED for k in fmt.kinds])
     mo = (C.c_int * order)(*fmt.mode_order)
     return d, kinds, mo
+
+
+class Graph:
+    """A captured op sequence (spd_graph)."""
+
+    def __init__(self, ctx, handle):
+        self.ctx, self.h = ctx, handle
+
+    def launch(self):
+        check(N.lib().spd_graph_launch(self.h, self.ctx.h))
+
+    def close(self):
+        if self.h:
+            check(N.lib().spd_graph_destroy(self.h))
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 class DeviceTensor:
