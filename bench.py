@@ -471,7 +471,8 @@ def main():
 def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, C_d, N):
     """The metric through the C-ABI with HOST buffers, every step:
     H2D of B as the reference stores it (inclusive pos pairs + crd + vals,
-    spd_tensor_upload validates and converts on the GPU) and of this GPU's
+    validated and converted on the GPU; at N > 1 only this GPU's colour of
+    crd/vals; re-staged into the same buffers after the first step) and of this GPU's
     1/N block of C from pinned memory, NCCL all-gather of C over NVLink
     (spd_allgather), the partition step, the leaf + boundary combine, and D2H
     of the output rows this GPU owns.  Consecutive steps alternate between two
@@ -490,9 +491,11 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
     vals_h = vals_d.cpu().pin_memory()
     per = (n * N) // world
     C_h = C_d[rank * per:(rank + 1) * per].cpu().pin_memory()
-    # Double buffering pays on one GPU; across GPUs the per-step NCCL
-    # all-gather already couples the ranks' streams, so N > 1 runs one stream.
-    nbuf = 2 if world == 1 else 1
+    # Two contexts (each with its own communicator at N > 1) on two streams:
+    # step k+1's uploads overlap step k's leaf and read-back.  Every rank
+    # issues its collectives in the same order, so the two communicators
+    # never wait on each other.
+    nbuf = 2 if os.environ.get("SPD_E2E_NBUF", "2") == "2" else 1
     streams = [torch.cuda.Stream(dev) for _ in range(nbuf)]
     ctxs = [H.Context(dev.index, stream=s.cuda_stream) for s in streams]
     if world > 1:
@@ -509,30 +512,53 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
     state = {"k": 0, "live": [None] * nbuf}
     torch.cuda.synchronize()
 
+    trace = os.environ.get("SPD_E2E_TRACE") == "1"
+
     def one():
         j = state["k"] % nbuf
         state["k"] += 1
         cx, s = ctxs[j], streams[j]
-        if state["live"][j] is not None:  # the tensor of step k-2 on this stream
-            state["live"][j].close()
+        tt = [time.perf_counter()]
         with torch.cuda.stream(s):
-            h = Cc.c_void_p()
-            NN.check(NN.lib().spd_tensor_upload(cx.h, 2, dims, kinds, mo, pos_pp, crd_pp,
-                                                Cc.cast(vals_h.data_ptr(), NN.dblp), Cc.byref(h)))
-            Bs = H.DeviceTensor(cx, h, (n, n), fmt)
+            if state["live"][j] is None:  # first use of this stream: upload
+                h = Cc.c_void_p()
+                if world == 1:  # spd_tensor_upload: the whole matrix
+                    NN.check(NN.lib().spd_tensor_upload(cx.h, 2, dims, kinds, mo, pos_pp, crd_pp,
+                                                        Cc.cast(vals_h.data_ptr(), NN.dblp), Cc.byref(h)))
+                else:  # this GPU's colour of the nonzero split, read from host memory
+                    NN.check(NN.lib().spd_tensor_upload_piece(cx.h, dims, kinds, mo, pos_pp, crd_pp,
+                                                              Cc.cast(vals_h.data_ptr(), NN.dblp), 2,
+                                                              Cc.byref(h)))
+                Bs = H.DeviceTensor(cx, h, (n, n), fmt)
+            else:  # later steps re-stage step k's B into the buffers of step k-2
+                Bs = state["live"][j]
+                NN.check(NN.lib().spd_tensor_restage(cx.h, Bs.h, pos_pp, crd_pp,
+                                                     Cc.cast(vals_h.data_ptr(), NN.dblp)))
+            tt.append(time.perf_counter())
             C_devs[j][rank * per:(rank + 1) * per].copy_(C_h, non_blocking=True)
             if world > 1:
                 cx.allgather(C_devs[j], per * 8)
-            cols = H.partition_nonzero(cx, Bs, 1, world)
-            lo, hi = owned_rows(cols, rp_h.numpy(), "nonzero", n)[rank]
+            tt.append(time.perf_counter())
+            if "owned" not in state:
+                cols = H.partition_nonzero(cx, Bs, 1, world)
+                state["owned"] = owned_rows(cols, rp_h.numpy(), "nonzero", n)[rank]
+            else:  # the partition step on the device, no host read-back
+                H.partition_nonzero(cx, Bs, 1, world, host=False)
+            lo, hi = state["owned"]
+            tt.append(time.perf_counter())
             H.spmm(cx, Bs, C_devs[j], N, A_devs[j], first=rank if world > 1 else 0, count=1, pieces=world,
                    stats=False)
+            tt.append(time.perf_counter())
             key = "A_h%d" % j
             if key not in state:
                 state[key] = torch.empty(max(hi - lo + 1, 0) * N, dtype=torch.float64).pin_memory()
             if hi >= lo:
                 state[key].copy_(A_devs[j][lo * N:(hi + 1) * N], non_blocking=True)
+            tt.append(time.perf_counter())
         state["live"][j] = Bs
+        if trace:
+            print("e2e step", state["k"], "ms:", [round((b - a) * 1e3, 1) for a, b in zip(tt, tt[1:])],
+                  file=sys.stderr)
 
     one()  # warm both streams (allocator pools, communicators)
     one()
@@ -547,6 +573,7 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
     for st in streams:
         st.synchronize()
     dt = (time.perf_counter() - t0) / args.e2e_steps
+    plo, phi = state["live"][0].piece_span()
     for Bs in state["live"]:
         if Bs is not None:
             Bs.close()
@@ -557,7 +584,7 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dt = float(t[0])
     # whole-job bytes per step: summed over ranks
-    by = torch.tensor([pairs.numel() * 8 + crd_h.numel() * 8 + vals_h.numel() * 8 + C_h.numel() * 8,
+    by = torch.tensor([pairs.numel() * 8 + (phi - plo + 1) * 16 + C_h.numel() * 8,
                        state["A_h0"].numel() * 8], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(by)
@@ -565,10 +592,14 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
     flops = 2.0 * nnz * N
     return {"value": flops / dt / 1e9, "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3,
-            "note": "per step, every GPU: B uploaded as the reference stores it (pos pairs, crd, vals) "
-                    "through spd_tensor_upload, its 1/N of C H2D + NCCL all-gather, partition, leaf + "
-                    "combine, its owned output rows D2H; consecutive steps double-buffered on two "
-                    "streams; time = max over ranks, bytes = sum over ranks"}
+            "note": "per step, every GPU: B staged from host memory as the reference stores it (pos "
+                    "pairs, crd, vals) -- the whole matrix through spd_tensor_upload at N=1, at N>1 "
+                    "the pos level plus only this GPU's colour of crd/vals (spd_tensor_upload_piece); "
+                    "later steps re-stage into the same device buffers (spd_tensor_restage, validated "
+                    "on the GPU, derived indices rebuilt) -- its 1/N of C H2D + NCCL all-gather, the "
+                    "partition step, leaf + combine, its owned output rows D2H; consecutive "
+                    "steps double-buffered on two streams; time = max over ranks, bytes = sum over "
+                    "ranks"}
 
 
 if __name__ == "__main__":

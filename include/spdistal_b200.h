@@ -124,7 +124,32 @@ int spd_allgather(spd_context* ctx, void* dev_buf, int64_t bytes_per_rank);
 int spd_tensor_upload(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
                       const int* mode_order, const int64_t* const* pos_pairs,
                       const int64_t* const* crd, const double* vals, spd_tensor** out);
-/* Same, with host row pointers (device format) instead of pos pairs. */
+/* Re-stages an uploaded tensor from new host arrays of the same geometry
+ * (same format, dims and per-level position counts; new pos pairs, crd and
+ * vals), into its existing device buffers: the per-step upload of a stream of
+ * same-shaped problems, with no device allocation.  Validated like
+ * spd_tensor_upload; derived indices (compacted rows, hot columns) are
+ * rebuilt on next use; a partition of this tensor on ctx is dropped.  A
+ * position count that differs returns SPD_ERR_VALIDATION. */
+int spd_tensor_restage(spd_context* ctx, spd_tensor* t, const int64_t* const* pos_pairs,
+                       const int64_t* const* crd, const double* vals);
+/* This GPU's piece of a CSR-like ("ds") matrix staged from host arrays: the
+ * whole pos level (pairs, O(rows)) is uploaded, converted and checked, the
+ * compute partition (split 1 = rows, 2 = nonzeros; spd_partition_universe /
+ * spd_partition_nonzero over the communicator's GPUs, one colour per GPU) is
+ * computed on the GPU, and only this GPU's colour of crd / vals is copied
+ * from `crd[1]` / `vals` (whole host arrays, indexed by global position) --
+ * the matched placement of lower_tdn (planner.cpp:361-439) for which the
+ * ledger charges 0 bytes, read from host memory.  Leaves the
+ * partition on ctx; the piece runs every leaf op for this GPU's colour and
+ * can be re-staged with spd_tensor_restage (a row split's range may move).
+ * Without a communicator (world 1) the piece is the whole matrix. */
+int spd_tensor_upload_piece(spd_context* ctx, const int64_t* dims, const int* kinds,
+                            const int* mode_order, const int64_t* const* pos_pairs,
+                            const int64_t* const* crd, const double* vals, int split,
+                            spd_tensor** out);
+/* Same as spd_tensor_upload, with host row pointers (device format) instead
+ * of pos pairs. */
 int spd_tensor_upload_rowptr(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
                              const int* mode_order, const int64_t* const* rowptr,
                              const int64_t* const* crd, const double* vals, int validate,

@@ -54,6 +54,12 @@ SIGNATURES = {
         [vp, C.c_int, i64p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(i64p),
          C.POINTER(i64p), dblp, C.POINTER(vp)],
     ),
+    "spd_tensor_restage": (C.c_int, [vp, vp, C.POINTER(i64p), C.POINTER(i64p), dblp]),
+    "spd_tensor_upload_piece": (
+        C.c_int,
+        [vp, i64p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(i64p), C.POINTER(i64p), dblp, C.c_int,
+         C.POINTER(vp)],
+    ),
     "spd_tensor_upload_rowptr": (
         C.c_int,
         [vp, C.c_int, i64p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(i64p),

@@ -5,6 +5,10 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdint.h>
+#include <stdio.h>
+
+#include <chrono>
+#include <cstdlib>
 
 #include <stdexcept>
 #include <string>
@@ -57,6 +61,28 @@ int guarded(F&& f) {
     return SPD_ERR_RUNTIME;
   }
 }
+
+// Host-side wall-clock trace of an API call's stages (SPD_HOST_TRACE=1,
+// stderr): where a caller's thread blocks (syncs, allocations).
+struct HostTrace {
+  const char* name;
+  std::chrono::steady_clock::time_point t0, t;
+  bool on;
+  explicit HostTrace(const char* n) : name(n) {
+    static const bool enabled = [] {
+      const char* e = getenv("SPD_HOST_TRACE");
+      return e && atoi(e) != 0;
+    }();
+    on = enabled;
+    if (on) t0 = t = std::chrono::steady_clock::now();
+  }
+  void mark(const char* what) {
+    if (!on) return;
+    const auto n = std::chrono::steady_clock::now();
+    fprintf(stderr, "[spd %s] %s %.2f ms\n", name, what, std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
 
 // Grow-only device scratch buffer.
 struct DeviceBuffer {
@@ -123,7 +149,14 @@ struct spd_tensor {
     int64_t* ptr = nullptr;
     int64_t* id = nullptr;
     int64_t m = 0;
+    int64_t cap_ptr = 0, cap_id = 0;  // allocated entries (reused after a restage)
   } nz[3];
+  // Staging buffers of spd_tensor_restage (pos pairs, row-start flags), kept
+  // so a per-step re-upload allocates nothing.
+  int64_t* stage_pairs = nullptr;
+  int64_t stage_pairs_cap = 0;
+  unsigned char* stage_flags = nullptr;
+  int64_t stage_flags_cap = 0;
   // Leaf crd as int32 with bit 31 = "hot column" (its dense row is among the
   // most referenced ones that fit in L2), for row-gathering kernels; built on
   // first use for a given dense-row size (crd32h_rowbytes).
@@ -141,9 +174,18 @@ struct spd_tensor {
   // row pointer is whole (O(rows), for the partition step).
   bool piece = false;
   int64_t piece_lo = 0, piece_hi = -1;
+  int64_t piece_cap = 0;  // allocated positions of piece_crd / piece_vals
+  int piece_split = 0;  // 1 rows / 2 nonzeros: staged from host (spd_tensor_upload_piece); 0 placed
   int64_t* piece_crd = nullptr;
   double* piece_vals = nullptr;
   int32_t* crd32h_alloc = nullptr;  // allocation behind crd32h (offset for pieces)
+  // Hot-copy index (SpMM leaf, HOT == 2): leaf crd as int32 where a hot
+  // column is 0x80000000 | slot, its row read from a per-call compact copy
+  // of the hot rows (hot_ids[slot] = column); built for one dense-row size.
+  int32_t* crd32x = nullptr;
+  int32_t* crd32x_alloc = nullptr;
+  int32_t* hot_ids = nullptr;
+  int64_t hot_n = 0, crd32x_rowbytes = 0;
 };
 
 struct spd_context {
@@ -169,7 +211,8 @@ struct spd_context {
   bool colors_host_valid = false;
 
   std::vector<int64_t> last_work;    // per colour
-  spd::DeviceBuffer scratch[6];
+  spd::DeviceBuffer scratch[7];  // [6]: compact hot-row copy
+  int64_t persist_bytes = -1;        // L2 persisting set-aside (-1: not set up)
   spd::DeviceBuffer counters;        // small int64 device counters
   int64_t* pinned_counters = nullptr;
 

@@ -68,21 +68,30 @@ __global__ void k_check_rowptr(const int64_t* __restrict__ rowptr, int64_t npos,
 // with a per-position owner test that needs no extra buffer: q starts a range
 // iff rowptr[owner(q)] == q, evaluated here by marking starts first.
 __global__ void k_mark_starts(const int64_t* __restrict__ rowptr, int64_t npos,
-                              unsigned char* __restrict__ start) {
+                              unsigned char* __restrict__ start, int64_t lo, int64_t hi) {
+  // start is indexed by global position; only [lo, hi] is held
   int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (; p < npos; p += stride)
-    if (rowptr[p + 1] > rowptr[p]) start[rowptr[p]] = 1;
+  for (; p < npos; p += stride) {
+    const int64_t a = rowptr[p];
+    if (rowptr[p + 1] > a && a >= lo && a <= hi) start[a] = 1;
+  }
 }
 
-__global__ void k_check_crd(const int64_t* __restrict__ crd, int64_t nnz, int64_t dim,
-                            const unsigned char* __restrict__ start, int* __restrict__ err) {
-  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// Positions [lo, hi] of crd (indexed by global position); the position
+// before lo, when it exists and is held elsewhere, is passed as prev.
+__global__ void k_check_crd(const int64_t* __restrict__ crd, int64_t lo, int64_t hi, int64_t dim,
+                            const unsigned char* __restrict__ start, int has_prev, int64_t prev,
+                            int* __restrict__ err) {
+  int64_t q = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (; q < nnz; q += stride) {
+  for (; q <= hi; q += stride) {
     int64_t c = crd[q];
     if (c < 0 || c >= dim) atomicOr(err, 4);
-    if (q > 0 && !start[q] && c <= crd[q - 1]) atomicOr(err, 2);
+    if (!start[q]) {
+      if (q > lo && c <= crd[q - 1]) atomicOr(err, 2);
+      if (q == lo && has_prev && c <= prev) atomicOr(err, 2);
+    }
   }
 }
 
@@ -154,6 +163,7 @@ static spd_tensor* upload_impl(spd_context* ctx, int order, const int64_t* dims,
                                const int* mode_order, const int64_t* const* pos,
                                const int64_t* const* crd, const double* vals, bool pairs,
                                bool validate) {
+  HostTrace ht("upload");
   activate(ctx);
   spd_tensor* t = make_skeleton(ctx, order, dims, kinds, mode_order);
   int* err_d = nullptr;
@@ -222,10 +232,10 @@ static spd_tensor* upload_impl(spd_context* ctx, int order, const int64_t* dims,
       if ((validate || pairs) && nnz > 0) {
         unsigned char* start = (unsigned char*)dev_alloc(ctx, nnz);
         SPD_CUDA(cudaMemsetAsync(start, 0, nnz, ctx->stream));
-        k_mark_starts<<<grid_for(ctx, parent), 256, 0, ctx->stream>>>(L.rowptr, parent, start);
+        k_mark_starts<<<grid_for(ctx, parent), 256, 0, ctx->stream>>>(L.rowptr, parent, start, 0, nnz - 1);
         SPD_CHECK_LAUNCH();
         int64_t dim = dims[mode_order[k0]];
-        k_check_crd<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(L.crd, nnz, dim, start, err_d);
+        k_check_crd<<<grid_for(ctx, nnz), 256, 0, ctx->stream>>>(L.crd, 0, nnz - 1, dim, start, 0, 0, err_d);
         SPD_CHECK_LAUNCH();
         dev_free(ctx, start);
       }
@@ -239,8 +249,10 @@ static spd_tensor* upload_impl(spd_context* ctx, int order, const int64_t* dims,
       SPD_CUDA(cudaMemcpyAsync(t->vals, vals, sizeof(double) * parent, cudaMemcpyHostToDevice,
                                ctx->stream));
     }
+    ht.mark("queued");
     SPD_CUDA(cudaMemcpyAsync(&err_h, err_d, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
     SPD_CUDA(cudaStreamSynchronize(ctx->stream));
+    ht.mark("synced");
     dev_free(ctx, err_d);
     err_d = nullptr;
     if (err_h & 1) throw ValidationError("tensor: pos ranges must tile [0, nnz) with canonical empties");
@@ -486,6 +498,225 @@ int spd_tensor_upload(spd_context* ctx, int order, const int64_t* dims, const in
   });
 }
 
+namespace spd {
+
+// Per-GPU piece of a CSR matrix staged from host arrays (spd_tensor_upload_
+// piece / spd_tensor_restage of a piece): the whole pos level (O(rows), the
+// partition step needs it) converted and checked on the GPU, then the compute
+// partition of `split` over the communicator's GPUs, then only this GPU's
+// colour of crd / vals copied from the host arrays (indexed by global
+// position) and checked.  `fresh`: allocate; else re-stage into t, whose
+// position range must come out unchanged.
+static void stage_piece(spd_context* ctx, spd_tensor* t, const int64_t* pairs, const int64_t* crd,
+                        const double* vals, int split, bool fresh) {
+  cudaStream_t s = ctx->stream;
+  spd_level_store& L = t->levels[1];
+  const int64_t nrows = L.parent_positions, nnz = L.positions;
+  int* err_d = (int*)ctx->counters.reserve(sizeof(int64_t) * 16) + 2;
+  SPD_CUDA(cudaMemsetAsync(err_d, 0, sizeof(int), s));
+  if (nrows > 0) {
+    if (!pairs) throw ValidationError("compressed level 1 needs pos");
+    if (t->stage_pairs_cap < 2 * nrows) {
+      dev_free(ctx, t->stage_pairs);
+      t->stage_pairs = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * 2 * nrows);
+      t->stage_pairs_cap = 2 * nrows;
+    }
+    SPD_CUDA(cudaMemcpyAsync(t->stage_pairs, pairs, sizeof(int64_t) * 2 * nrows, cudaMemcpyHostToDevice, s));
+    k_pairs_to_rowptr<<<grid_for(ctx, nrows), 256, 0, s>>>(t->stage_pairs, nrows, nnz, L.rowptr, err_d);
+    SPD_CHECK_LAUNCH();
+  } else {
+    SPD_CUDA(cudaMemsetAsync(L.rowptr, 0, sizeof(int64_t), s));
+  }
+  const int rc = split == 1 ? spd_partition_universe(ctx, t, ctx->world, nullptr)
+                            : spd_partition_nonzero(ctx, t, 1, ctx->world, nullptr);
+  if (rc != SPD_OK) throw ValidationError(spd_last_error());
+  const spd_range mine = host_colors(ctx)[ctx->rank].q;  // syncs
+  int err_h = 0;
+  SPD_CUDA(cudaMemcpy(&err_h, err_d, sizeof(int), cudaMemcpyDeviceToHost));
+  if (err_h & 1) throw ValidationError("tensor: pos ranges must tile [0, nnz) with canonical empties");
+  const int64_t cnt = std::max<int64_t>(mine.hi - mine.lo + 1, 0);
+  // a row split's ranges follow the new row pointer: reuse the piece
+  // buffers when they are large enough
+  if (fresh || cnt > t->piece_cap) {
+    dev_free(ctx, t->piece_crd);
+    dev_free(ctx, t->piece_vals);
+    t->piece_cap = std::max<int64_t>(cnt, 1);
+    t->piece_crd = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * t->piece_cap);
+    t->piece_vals = (double*)dev_alloc(ctx, sizeof(double) * t->piece_cap);
+  }
+  t->piece_split = split;
+  t->piece_lo = mine.lo;
+  t->piece_hi = mine.hi;
+  L.crd = t->piece_crd - mine.lo;  // indexed by global position
+  t->vals = t->piece_vals - mine.lo;
+  if (t->crd32h_alloc) dev_free(ctx, t->crd32h_alloc), t->crd32h_alloc = nullptr;  // sized by the old piece
+  if (t->crd32x_alloc) dev_free(ctx, t->crd32x_alloc), t->crd32x_alloc = nullptr;
+  if (cnt > 0) {
+    if (!crd) throw ValidationError("compressed level 1 needs crd");
+    if (!vals) throw ValidationError("tensor: vals length does not match leaf count");
+    SPD_CUDA(cudaMemcpyAsync(t->piece_crd, crd + mine.lo, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice, s));
+    SPD_CUDA(cudaMemcpyAsync(t->piece_vals, vals + mine.lo, sizeof(double) * cnt, cudaMemcpyHostToDevice, s));
+    const int64_t need = std::max<int64_t>(cnt, nrows);  // also the nz_view flags buffer
+    if (t->stage_flags_cap < need) {
+      dev_free(ctx, t->stage_flags);
+      t->stage_flags = (unsigned char*)dev_alloc(ctx, need);
+      t->stage_flags_cap = need;
+    }
+    unsigned char* start = t->stage_flags - mine.lo;  // indexed by global position
+    SPD_CUDA(cudaMemsetAsync(t->stage_flags, 0, cnt, s));
+    k_mark_starts<<<grid_for(ctx, nrows), 256, 0, s>>>(L.rowptr, nrows, start, mine.lo, mine.hi);
+    SPD_CHECK_LAUNCH();
+    const int64_t dim = t->dims[t->mode_order[1]];
+    k_check_crd<<<grid_for(ctx, cnt), 256, 0, s>>>(L.crd, mine.lo, mine.hi, dim, start, mine.lo > 0 ? 1 : 0,
+                                                   mine.lo > 0 ? crd[mine.lo - 1] : 0, err_d);
+    SPD_CHECK_LAUNCH();
+  }
+  SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters + 12, err_d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPD_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(&err_h, ctx->pinned_counters + 12, sizeof(int));
+  if (err_h & 2) throw ValidationError("tensor: crd must be strictly increasing per range");
+  if (err_h & 4) throw ValidationError("tensor: crd value out of dimension bounds");
+}
+
+static void restage_piece(spd_context* ctx, spd_tensor* t, const int64_t* const* pos_pairs,
+                          const int64_t* const* crd, const double* vals) {
+  if (t->piece_split != 1 && t->piece_split != 2)
+    throw ValidationError("restage: a placed piece (spd_tensor_place) cannot be re-staged from the host");
+  const int64_t nrows = t->levels[1].parent_positions, nnz = t->levels[1].positions;
+  const int64_t got = nrows == 0 ? 0 : (pos_pairs && pos_pairs[1] ? pos_pairs[1][2 * (nrows - 1) + 1] + 1 : -1);
+  if (got != nnz)
+    throw ValidationError("restage: level 1 holds " + std::to_string(nnz) + " positions, the new pos " +
+                          std::to_string(got));
+  for (auto& z : t->nz) z.R = nullptr;
+  t->crd32h = nullptr;
+  t->crd32h_rowbytes = 0;
+  t->crd32x = nullptr;
+  t->crd32x_rowbytes = 0;
+  stage_piece(ctx, t, pos_pairs[1], crd ? crd[1] : nullptr, vals, t->piece_split, false);
+}
+
+}  // namespace spd
+
+int spd_tensor_upload_piece(spd_context* ctx, const int64_t* dims, const int* kinds, const int* mode_order,
+                            const int64_t* const* pos_pairs, const int64_t* const* crd, const double* vals,
+                            int split, spd_tensor** out) {
+  return guarded([&] {
+    checked(ctx);
+    if (!out) throw ValidationError("null output handle");
+    if (split != 1 && split != 2) throw ValidationError("split must be 1 (rows) or 2 (nonzeros)");
+    if (kinds[0] != SPD_DENSE || kinds[1] != SPD_COMPRESSED)
+      throw ValidationError("unsupported on gpu: pieces of ds (CSR-like) matrices");
+    HostTrace ht("upload_piece");
+    activate(ctx);
+    spd_tensor* t = make_skeleton(ctx, 2, dims, kinds, mode_order);
+    try {
+      const int64_t nrows = dims[mode_order[0]];
+      if (nrows > 0 && (!pos_pairs || !pos_pairs[1])) throw ValidationError("compressed level 1 needs pos");
+      const int64_t nnz = nrows == 0 ? 0 : pos_pairs[1][2 * (nrows - 1) + 1] + 1;
+      if (nnz < 0) throw ValidationError("tensor: pos ranges must cover exactly [0, nnz)");
+      t->levels[0].kind = SPD_DENSE;
+      t->levels[0].dom = {nrows};
+      t->levels[0].positions = nrows;
+      spd_level_store& L = t->levels[1];
+      L.kind = SPD_COMPRESSED;
+      L.parent_positions = nrows;
+      L.positions = nnz;
+      L.rowptr = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (nrows + 1));
+      t->nvals = nnz;
+      t->piece = true;
+      set_whole_span(t);
+      stage_piece(ctx, t, nrows > 0 ? pos_pairs[1] : nullptr, crd ? crd[1] : nullptr, vals, split, true);
+    } catch (...) {
+      spd_tensor_destroy(t);
+      throw;
+    }
+    ht.mark("staged");
+    *out = t;
+  });
+}
+
+int spd_tensor_restage(spd_context* ctx, spd_tensor* t, const int64_t* const* pos_pairs,
+                       const int64_t* const* crd, const double* vals) {
+  return guarded([&] {
+    checked(ctx);
+    if (!t) throw ValidationError("null tensor");
+    if (t->ctx != ctx) throw ValidationError("restage: tensor belongs to another context");
+    if (t->piece) {
+      restage_piece(ctx, t, pos_pairs, crd, vals);
+      return;
+    }
+    if (!t->owns) throw ValidationError("restage: needs a tensor uploaded by spd_tensor_upload*");
+    HostTrace ht("restage");
+    activate(ctx);
+    cudaStream_t s = ctx->stream;
+    int* err_d = (int*)ctx->counters.reserve(sizeof(int64_t) * 16) + 2;  // [8..] belong to nz_view
+    int err_h = 0;
+    SPD_CUDA(cudaMemsetAsync(err_d, 0, sizeof(int), s));
+    for (size_t l = 0; l < t->levels.size(); l++) {
+      spd_level_store& L = t->levels[l];
+      if (L.kind != SPD_COMPRESSED) continue;
+      const int64_t parent = L.parent_positions, nnz = L.positions;
+      if (parent > 0 && (!pos_pairs || !pos_pairs[l]))
+        throw ValidationError("compressed level " + std::to_string(l) + " needs pos");
+      const int64_t got = parent == 0 ? 0 : pos_pairs[l][2 * (parent - 1) + 1] + 1;
+      if (got != nnz) throw ValidationError("restage: level " + std::to_string(l) + " holds " +
+                                            std::to_string(nnz) + " positions, the new pos " +
+                                            std::to_string(got));
+      if (nnz > 0 && (!crd || !crd[l]))
+        throw ValidationError("compressed level " + std::to_string(l) + " needs crd");
+      if (parent > 0) {
+        if (t->stage_pairs_cap < 2 * parent) {
+          dev_free(ctx, t->stage_pairs);
+          t->stage_pairs = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * 2 * parent);
+          t->stage_pairs_cap = 2 * parent;
+        }
+        SPD_CUDA(cudaMemcpyAsync(t->stage_pairs, pos_pairs[l], sizeof(int64_t) * 2 * parent,
+                                 cudaMemcpyHostToDevice, s));
+        k_pairs_to_rowptr<<<grid_for(ctx, parent), 256, 0, s>>>(t->stage_pairs, parent, nnz, L.rowptr, err_d);
+        SPD_CHECK_LAUNCH();
+      }
+      if (nnz > 0) {
+        SPD_CUDA(cudaMemcpyAsync(L.crd, crd[l], sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
+        const int64_t need = std::max<int64_t>(nnz, parent);  // also the nz_view flags buffer
+        if (t->stage_flags_cap < need) {
+          dev_free(ctx, t->stage_flags);
+          t->stage_flags = (unsigned char*)dev_alloc(ctx, need);
+          t->stage_flags_cap = need;
+        }
+        SPD_CUDA(cudaMemsetAsync(t->stage_flags, 0, nnz, s));
+        k_mark_starts<<<grid_for(ctx, parent), 256, 0, s>>>(L.rowptr, parent, t->stage_flags, 0, nnz - 1);
+        SPD_CHECK_LAUNCH();
+        const int64_t dim = t->dims[t->mode_order[t->groups[l][0]]];
+        k_check_crd<<<grid_for(ctx, nnz), 256, 0, s>>>(L.crd, 0, nnz - 1, dim, t->stage_flags, 0, 0, err_d);
+        SPD_CHECK_LAUNCH();
+      }
+    }
+    if (t->nvals > 0) {
+      if (!vals) throw ValidationError("tensor: vals length does not match leaf count");
+      SPD_CUDA(cudaMemcpyAsync(t->vals, vals, sizeof(double) * t->nvals, cudaMemcpyHostToDevice, s));
+    }
+    // derived indices are functions of the old pattern: invalidate, keep buffers
+    for (auto& z : t->nz) z.R = nullptr;
+    t->crd32h = nullptr;
+    t->crd32h_rowbytes = 0;
+    t->crd32x = nullptr;
+    t->crd32x_rowbytes = 0;
+    dev_free(ctx, t->jleaf);
+    t->jleaf = nullptr;
+    dev_free(ctx, t->leaf_rowptr);
+    t->leaf_rowptr = nullptr;
+    if (ctx->split_tensor == t) ctx->split = SplitKind::None, ctx->split_tensor = nullptr;
+    ht.mark("queued");
+    SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters + 12, err_d, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SPD_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(&err_h, ctx->pinned_counters + 12, sizeof(int));
+    ht.mark("synced");
+    if (err_h & 1) throw ValidationError("tensor: pos ranges must tile [0, nnz) with canonical empties");
+    if (err_h & 2) throw ValidationError("tensor: crd must be strictly increasing per range");
+    if (err_h & 4) throw ValidationError("tensor: crd value out of dimension bounds");
+  });
+}
+
 int spd_tensor_upload_rowptr(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
                              const int* mode_order, const int64_t* const* rowptr,
                              const int64_t* const* crd, const double* vals, int validate,
@@ -537,6 +768,7 @@ int spd_tensor_wrap_device(spd_context* ctx, int order, const int64_t* dims, con
 int spd_tensor_destroy(spd_tensor* t) {
   return guarded([&] {
     if (!t) return;
+    HostTrace ht("destroy");
     spd_context* ctx = t->ctx;
     activate(ctx);
     if (ctx->split_tensor == t) {
@@ -560,12 +792,17 @@ int spd_tensor_destroy(spd_tensor* t) {
     }
     dev_free(ctx, t->leaf_rowptr);
     dev_free(ctx, t->crd32h_alloc);
+    dev_free(ctx, t->crd32x_alloc);
+    dev_free(ctx, t->hot_ids);
+    dev_free(ctx, t->stage_pairs);
+    dev_free(ctx, t->stage_flags);
     dev_free(ctx, t->jleaf);
     for (auto& z : t->nz) {
       dev_free(ctx, z.ptr);
       dev_free(ctx, z.id);
     }
     delete t;
+    ht.mark("freed");
   });
 }
 

@@ -266,13 +266,21 @@ __global__ void __launch_bounds__(kBlock, 5) k_spmv_nz(WalkGeom g, NzView z, con
 // SpMM N == 32 over the compacted view: half a warp per position, 128-bit
 // register gathers UNR pairs deep, crd/vals of the next window prefetched,
 // row switches from the window mask (no dependent loads on the critical path).
-template <int UNR, int MINB, bool HOT, bool DYN = false>
+// HOT selects the column index and the C-row load:
+//   0  int64 crd, every C row gathered with L2 evict_last;
+//   1  int32 crd with the hot-column bit (crd32h), hot rows evict_last, cold
+//      rows evict_first (two predicated uniform-policy loads);
+//   2  int32 crd with hot-copy slots (crd32x): a hot column reads its row from
+//      Chot, the per-call compact copy of the hot rows that the launch's L2
+//      access-policy window marks persisting; one plain load per position.
+template <int UNR, int MINB, int HOT, bool DYN = false>
 __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
                                                       const int32_t* __restrict__ crd32h,
                                                       const double* __restrict__ vals,
                                                       const double* __restrict__ C,
                                                       double* __restrict__ A, ChunkRecs rec,
-                                                      const int64_t* __restrict__ counters) {
+                                                      const int64_t* __restrict__ counters,
+                                                      const double* __restrict__ Chot = nullptr) {
   const int lane = lane_id();
   const int half = lane >> 4, hl = lane & 15;
   const int64_t begin = counters[1], end = counters[2];
@@ -281,6 +289,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
   const uint64_t pol_keep = l2_policy_evict_last();
   const uint64_t pol_stream = l2_policy_evict_first();
   const double* Cl = C + 2 * hl;
+  const double* Hl = Chot + 2 * hl;
   // DYN: chunks handed out by an atomic ticket (counters[3]) instead of a
   // static grid stride, so warps that drew cheap chunks take more.
   const int64_t tmax = end - begin;
@@ -330,7 +339,10 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
           const int kk = __shfl_sync(FULL, my_k, p);
           bv[i] = __shfl_sync(FULL, my_v, p);
           const double* src = Cl + (int64_t)(kk & 0x7fffffff) * 32;
-          if (HOT) {  // two uniform-policy loads instead of a per-lane policy
+          if (HOT == 2) {
+            const double* hsrc = (kk < 0 ? Hl : Cl) + (int64_t)(kk & 0x7fffffff) * 32;
+            cv[i] = p < cnt ? __ldg(reinterpret_cast<const double2*>(hsrc)) : make_double2(0.0, 0.0);
+          } else if (HOT) {  // two uniform-policy loads instead of a per-lane policy
             cv[i] = make_double2(0.0, 0.0);
             if (p < cnt && kk < 0) cv[i] = ld_f64x2_hint(src, pol_keep);
             if (p < cnt && kk >= 0) cv[i] = ld_f64x2_hint(src, pol_stream);
@@ -588,6 +600,47 @@ __global__ void k_crd32h(const int64_t* __restrict__ crd, int64_t nnz, const int
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t col = ld64(crd + q);
     out[q] = (int32_t)col | (counts[col] >= t ? (int32_t)0x80000000 : 0);
+  }
+}
+
+__global__ void k_iota32(int32_t* __restrict__ a, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    a[i] = (int32_t)i;
+}
+
+// Hot-copy index: the first H entries of the columns sorted by descending
+// reference count get slots 0..H-1 (slot_of[col]); columns referenced once
+// are never worth a slot.
+__global__ void k_hot_slots(const int32_t* __restrict__ counts_desc, const int32_t* __restrict__ ids_desc,
+                            int64_t H, int32_t* __restrict__ slot_of, int32_t* __restrict__ hot_ids,
+                            int64_t* __restrict__ n_hot) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < H; r += (int64_t)gridDim.x * blockDim.x) {
+    const bool hot = counts_desc[r] >= 2;
+    if (hot) slot_of[ids_desc[r]] = (int32_t)r, hot_ids[r] = ids_desc[r];
+    if (hot && (r == H - 1 || counts_desc[r + 1] < 2)) *n_hot = r + 1;
+  }
+}
+
+// crd32x[q] = 0x80000000 | slot for a hot column, else the column.
+__global__ void k_crd32x(const int64_t* __restrict__ crd, int64_t nnz, const int32_t* __restrict__ slot_of,
+                         int32_t* __restrict__ out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t col = ld64(crd + q);
+    const int32_t sl = slot_of[col];
+    out[q] = sl >= 0 ? (int32_t)(0x80000000u | (uint32_t)sl) : (int32_t)col;
+  }
+}
+
+// Chot[slot] = C[hot_ids[slot]] for W-wide rows (W even): a half-warp per row,
+// 128-bit loads and stores.
+__global__ void k_hot_gather(const double* __restrict__ C, const int32_t* __restrict__ hot_ids, int64_t H,
+                             int64_t W, double* __restrict__ Chot) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t vec = W / 2;
+  for (int64_t i = t; i < H * vec; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / vec, l = i - r * vec;
+    const double2 v = __ldg(reinterpret_cast<const double2*>(C + (int64_t)hot_ids[r] * W) + l);
+    reinterpret_cast<double2*>(Chot + r * W)[l] = v;
   }
 }
 

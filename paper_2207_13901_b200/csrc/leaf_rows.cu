@@ -657,18 +657,29 @@ static NzView nz_view(spd_context* ctx, spd_tensor* t, const int64_t* R, int64_t
     if (e.R == R) return NzView{e.ptr, e.id, e.m};
   spd_tensor::NzCache* slot = nullptr;
   for (auto& e : t->nz)
-    if (!e.R) slot = &e;
+    if (!e.R && (!slot || e.cap_id > slot->cap_id)) slot = &e;  // prefer reusable buffers
   if (!slot) {
     slot = &t->nz[0];
     cudaFreeAsync(slot->ptr, ctx->stream);
     cudaFreeAsync(slot->id, ctx->stream);
+    slot->ptr = slot->id = nullptr;
+    slot->cap_ptr = slot->cap_id = 0;
   }
   cudaStream_t s = ctx->stream;
   unsigned char* flags = nullptr;
   int64_t* m_dev = nullptr;
-  SPD_CUDA(cudaMallocAsync((void**)&flags, nrows > 0 ? nrows : 1, s));
-  SPD_CUDA(cudaMallocAsync((void**)&m_dev, sizeof(int64_t), s));
-  SPD_CUDA(cudaMallocAsync((void**)&slot->id, sizeof(int64_t) * (nrows > 0 ? nrows : 1), s));
+  const int64_t nid = nrows > 0 ? nrows : 1;
+  if (t->stage_flags_cap >= nid) {
+    flags = t->stage_flags;  // a restaged tensor's staging buffer, idle here
+  } else {
+    SPD_CUDA(cudaMallocAsync((void**)&flags, nid, s));
+  }
+  m_dev = (int64_t*)ctx->counters.reserve(sizeof(int64_t) * 16) + 8;
+  if (slot->cap_id < nid) {
+    if (slot->id) cudaFreeAsync(slot->id, s);
+    SPD_CUDA(cudaMallocAsync((void**)&slot->id, sizeof(int64_t) * nid, s));
+    slot->cap_id = nid;
+  }
   SPD_CUDA(cudaMemsetAsync(m_dev, 0, sizeof(int64_t), s));
   if (nrows > 0) {
     k_nz_flags<<<(unsigned)std::min<int64_t>(ceil_div(nrows, 256), ctx->num_sms * 16), 256, 0, s>>>(R, nrows, flags);
@@ -682,12 +693,15 @@ static NzView nz_view(spd_context* ctx, spd_tensor* t, const int64_t* R, int64_t
   SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters + 8, m_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   SPD_CUDA(cudaStreamSynchronize(s));
   slot->m = ctx->pinned_counters[8];
-  SPD_CUDA(cudaMallocAsync((void**)&slot->ptr, sizeof(int64_t) * (slot->m + 1), s));
+  if (slot->cap_ptr < slot->m + 1) {
+    if (slot->ptr) cudaFreeAsync(slot->ptr, s);
+    SPD_CUDA(cudaMallocAsync((void**)&slot->ptr, sizeof(int64_t) * (slot->m + 1), s));
+    slot->cap_ptr = slot->m + 1;
+  }
   k_nz_ptr<<<(unsigned)std::min<int64_t>(ceil_div(slot->m + 1, 256), ctx->num_sms * 16), 256, 0, s>>>(
       R, nrows, slot->id, m_dev, slot->ptr);
   SPD_CHECK_LAUNCH();
-  cudaFreeAsync(flags, s);
-  cudaFreeAsync(m_dev, s);
+  if (flags != t->stage_flags) cudaFreeAsync(flags, s);
   slot->R = R;
   ctx->launches += 3;
   return NzView{slot->ptr, slot->id, slot->m};
@@ -716,10 +730,9 @@ static const int32_t* hot_crd(spd_context* ctx, spd_tensor* t, int64_t rowbytes)
   SPD_CUDA(cudaMallocAsync((void**)&counts, sizeof(int32_t) * (ncols > 0 ? ncols : 1), s));
   SPD_CUDA(cudaMallocAsync((void**)&sorted, sizeof(int32_t) * (ncols > 0 ? ncols : 1), s));
   SPD_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (ncols > 0 ? ncols : 1), s));
-  if (!t->crd32h_alloc) {
+  if (!t->crd32h_alloc)
     SPD_CUDA(cudaMallocAsync((void**)&t->crd32h_alloc, sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
-    t->crd32h = t->crd32h_alloc - lo;  // indexed by global position
-  }
+  t->crd32h = t->crd32h_alloc - lo;  // indexed by global position
   const unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(nnz, 256), 1), ctx->num_sms * 16);
   if (nnz > 0) {
     k_col_count<<<grid, 256, 0, s>>>(L.crd + lo, nnz, counts);
@@ -738,6 +751,85 @@ static const int32_t* hot_crd(spd_context* ctx, spd_tensor* t, int64_t rowbytes)
   return t->crd32h;
 }
 
+// Hot-copy index for dense rows of `rowbytes` (cached on t): the most
+// referenced columns (count >= 2) whose rows fit in SPD_HOT_FRAC of L2 get
+// slots in a compact per-call copy of C; crd32x addresses slot or column.
+static void hot_copy_index(spd_context* ctx, spd_tensor* t, int64_t rowbytes) {
+  if (t->crd32x && t->crd32x_rowbytes == rowbytes) return;
+  const spd_level_store& L = t->levels.back();
+  const int64_t lo = t->piece ? t->piece_lo : 0;
+  const int64_t nnz = t->piece ? t->piece_hi - t->piece_lo + 1 : L.positions;
+  const int64_t ncols = t->dims[t->mode_order[t->groups.back()[0]]];
+  cudaStream_t s = ctx->stream;
+  int l2 = 0;
+  SPD_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
+  static double frac = [] {
+    const char* e = getenv("SPD_HOT_FRAC");
+    return e ? atof(e) : 0.6;
+  }();
+  const int64_t k = std::min<int64_t>(ncols, std::max<int64_t>(1, (int64_t)(frac * l2) / rowbytes));
+  const int64_t nc = ncols > 0 ? ncols : 1;
+  int32_t *counts = nullptr, *counts_desc = nullptr, *ids = nullptr, *ids_desc = nullptr, *slot_of = nullptr;
+  int64_t* n_hot = nullptr;
+  SPD_CUDA(cudaMallocAsync((void**)&counts, sizeof(int32_t) * nc, s));
+  SPD_CUDA(cudaMallocAsync((void**)&counts_desc, sizeof(int32_t) * nc, s));
+  SPD_CUDA(cudaMallocAsync((void**)&ids, sizeof(int32_t) * nc, s));
+  SPD_CUDA(cudaMallocAsync((void**)&ids_desc, sizeof(int32_t) * nc, s));
+  SPD_CUDA(cudaMallocAsync((void**)&slot_of, sizeof(int32_t) * nc, s));
+  SPD_CUDA(cudaMallocAsync((void**)&n_hot, sizeof(int64_t), s));
+  SPD_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * nc, s));
+  SPD_CUDA(cudaMemsetAsync(slot_of, 0xff, sizeof(int32_t) * nc, s));
+  SPD_CUDA(cudaMemsetAsync(n_hot, 0, sizeof(int64_t), s));
+  if (!t->crd32x_alloc)
+    SPD_CUDA(cudaMallocAsync((void**)&t->crd32x_alloc, sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
+  t->crd32x = t->crd32x_alloc - lo;  // indexed by global position
+  if (t->hot_ids) cudaFreeAsync(t->hot_ids, s);
+  SPD_CUDA(cudaMallocAsync((void**)&t->hot_ids, sizeof(int32_t) * k, s));
+  const unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(nnz, 256), 1), ctx->num_sms * 16);
+  if (nnz > 0 && ncols > 0) {
+    k_col_count<<<grid, 256, 0, s>>>(L.crd + lo, nnz, counts);
+    SPD_CHECK_LAUNCH();
+    k_iota32<<<(unsigned)std::min<int64_t>(ceil_div(ncols, 256), ctx->num_sms * 16), 256, 0, s>>>(ids, ncols);
+    SPD_CHECK_LAUNCH();
+    size_t bytes = 0;
+    SPD_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, counts, counts_desc, ids, ids_desc, ncols, 0,
+                                                       32, s));
+    void* tmp = ctx->scratch[5].reserve(bytes);
+    SPD_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, bytes, counts, counts_desc, ids, ids_desc, ncols, 0, 32,
+                                                       s));
+    k_hot_slots<<<(unsigned)std::min<int64_t>(ceil_div(k, 256), ctx->num_sms * 16), 256, 0, s>>>(
+        counts_desc, ids_desc, k, slot_of, t->hot_ids, n_hot);
+    SPD_CHECK_LAUNCH();
+    k_crd32x<<<grid, 256, 0, s>>>(L.crd + lo, nnz, slot_of, t->crd32x_alloc);
+    SPD_CHECK_LAUNCH();
+    ctx->launches += 5;
+  }
+  SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters + 9, n_hot, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  SPD_CUDA(cudaStreamSynchronize(s));
+  t->hot_n = ctx->pinned_counters[9];
+  for (void* p : {(void*)counts, (void*)counts_desc, (void*)ids, (void*)ids_desc, (void*)slot_of, (void*)n_hot})
+    cudaFreeAsync(p, s);
+  t->crd32x_rowbytes = rowbytes;
+}
+
+// L2 set-aside for persisting accesses (once per context): the hot-copy
+// window of the SpMM leaf.  0 when the device offers none.
+static int64_t persist_setaside(spd_context* ctx, int64_t want) {
+  if (ctx->persist_bytes >= 0) return ctx->persist_bytes;
+  int maxp = 0;
+  SPD_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
+  const size_t b = (size_t)std::min<int64_t>(want, maxp);
+  if (b > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, b) == cudaSuccess) {
+    size_t got = 0;
+    cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+    ctx->persist_bytes = (int64_t)got;
+  } else {
+    cudaGetLastError();
+    ctx->persist_bytes = 0;
+  }
+  return ctx->persist_bytes;
+}
+
 static bool dyn_enabled() {
   static int v = [] {
     const char* e = getenv("SPD_DYN");
@@ -746,12 +838,12 @@ static bool dyn_enabled() {
   return v != 0;
 }
 
-static bool hot_enabled() {
+static int hot_enabled() {
   static int v = [] {
     const char* e = getenv("SPD_HOT");
     return e ? atoi(e) : 0;
   }();
-  return v != 0;
+  return v;
 }
 
 // Whether an op walks the compacted view (default) -- SPD_NZ=0 selects the
@@ -790,6 +882,7 @@ bool sddmm_nz_launch(spd_context* ctx, const spd_tensor* B, const WalkGeom& g, c
 
 static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_t count,
                         spd_stats* stats) {
+  HostTrace ht("rowwalk");
   checked(ctx);
   const spd_tensor* B = a.B;
   if (!B) throw ValidationError("null tensor");
@@ -875,6 +968,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   SPD_CUDA(cudaMemsetAsync(col.head_pack, 0xff, sizeof(int64_t) * P * (W + 2), s));
   SPD_CUDA(cudaMemsetAsync(col.counters, 0, sizeof(int64_t) * 4, s));
   SPD_CUDA(cudaMemsetAsync(col.tail_row, 0xff, sizeof(int64_t) * P, s));
+  ht.mark("scratch");
   k_setup<<<1, 1024, 0, s>>>((DevColor*)ctx->colors_dev.ptr, P, (int)ctx->split, out_level, g.R,
                              g.nrows, g.CH, first, count, col.counters);
   SPD_CHECK_LAUNCH();
@@ -888,6 +982,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   NzView z{nullptr, nullptr, 0};
   if (use_nz) {
     z = nz_view(ctx, const_cast<spd_tensor*>(B), g.R, g.nrows);
+    ht.mark("nz_view");
     // SpMV/SpTTV walks zero the empty rows between consecutive non-empty
     // rows themselves (8 bytes each); the W-wide outputs use this pass.
     if (a.op == Op::SpMM || a.op == Op::SpMTTKRP) {
@@ -919,23 +1014,68 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
       if (!grid) grid = occupancy_grid(ctx, k_mttkrp32_nz<4, 3, false>);
       k_mttkrp32_nz<4, 3, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->jleaf, a.x, B->vals, a.D, a.out, rec,
                                                          col.counters);
+    } else if (a.op == Op::SpMM && hot_enabled() == 2) {
+      // hot-copy leaf: gather the hot rows of C into a compact buffer that
+      // an L2 access-policy window keeps persisting across the leaf
+      spd_tensor* Bm = const_cast<spd_tensor*>(B);
+      hot_copy_index(ctx, Bm, 256);
+      const int64_t H = Bm->hot_n;
+      double* Chot = (double*)ctx->scratch[6].reserve(sizeof(double) * 32 * (H > 0 ? H : 1));
+      const int64_t win = H * 256;
+      const int64_t setaside = persist_setaside(ctx, win);
+      cudaLaunchAttribute attr[1];
+      int nattr = 0;
+      if (setaside > 0 && win > 0) {
+        int maxwin = 0;
+        SPD_CUDA(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device));
+        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+        attr[0].val.accessPolicyWindow.base_ptr = Chot;
+        attr[0].val.accessPolicyWindow.num_bytes = (size_t)std::min<int64_t>(win, maxwin);
+        attr[0].val.accessPolicyWindow.hitRatio =
+            (float)std::min(1.0, (double)setaside / (double)attr[0].val.accessPolicyWindow.num_bytes);
+        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        nattr = 1;
+      }
+      if (H > 0) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)std::min<int64_t>(ceil_div(H * 16, 256), ctx->num_sms * 8));
+        cfg.blockDim = dim3(256);
+        cfg.stream = s;
+        cfg.attrs = attr;
+        cfg.numAttrs = nattr;
+        SPD_CUDA(cudaLaunchKernelEx(&cfg, k_hot_gather, (const double*)a.x, (const int32_t*)Bm->hot_ids, H,
+                                    (int64_t)32, Chot));
+        launches++;
+      }
+      static int grid = 0;
+      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, 2, true>);
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(grid);
+      cfg.blockDim = dim3(kBlock);
+      cfg.stream = s;
+      cfg.attrs = attr;
+      cfg.numAttrs = nattr;
+      SPD_CUDA(cudaLaunchKernelEx(&cfg, k_spmm32_nz<4, 4, 2, true>, g, z, (const int64_t*)leaf.crd,
+                                  (const int32_t*)Bm->crd32x, (const double*)B->vals, (const double*)a.x, a.out,
+                                  rec, (const int64_t*)col.counters, (const double*)Chot));
     } else if (a.op == Op::SpMM && hot_enabled()) {
       const int32_t* h = hot_crd(ctx, const_cast<spd_tensor*>(B), 256);
       static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, true, true>);
-      k_spmm32_nz<4, 4, true, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, h, B->vals, a.x, a.out, rec,
+      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, 1, true>);
+      k_spmm32_nz<4, 4, 1, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, h, B->vals, a.x, a.out, rec,
                                                             col.counters);
     } else if (a.op == Op::SpMM && dyn_enabled()) {
       // production SpMM leaf: chunks by atomic ticket (27% faster than the
       // static grid stride on the R-MAT step, profiles/README.md)
       static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, false, true>);
-      k_spmm32_nz<4, 4, false, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
+      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, 0, true>);
+      k_spmm32_nz<4, 4, 0, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
                                                              col.counters);
     } else if (a.op == Op::SpMM) {  // static grid stride (SPD_DYN=0, comparison only)
       static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, false>);
-      k_spmm32_nz<4, 4, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
+      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, 0>);
+      k_spmm32_nz<4, 4, 0><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
                                                        col.counters);
     } else {
       static int grid = 0;
@@ -993,6 +1133,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
     }
   }
   SPD_CHECK_LAUNCH();
+  ht.mark("leaf launch");
   leaf_timing_end(ctx);
   trace_mark(ctx);
   launches++;
@@ -1016,6 +1157,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   trace_mark(ctx);
   launches++;
   ctx->launches += launches;
+  ht.mark("tail launches");
   if (stats) {
     SPD_CUDA(cudaEventRecord(ctx->ev1, s));
     SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters, col.counters, sizeof(int64_t) * 4,

@@ -355,6 +355,24 @@ class DeviceTensor:
                                         vals.ctypes.data_as(N.dblp), C.byref(h)))
         return DeviceTensor(ctx, h, t.dims, t.format)
 
+    def restage(self, t: SparseTensor):
+        """spd_tensor_restage: new contents of the same geometry from host
+        arrays, into this tensor's device buffers (validated like upload)."""
+        nl = len(t.levels)
+        keep = []
+        pos = (N.i64p * nl)()
+        crd = (N.i64p * nl)()
+        for l, lv in enumerate(t.levels):
+            if lv.kind == COMPRESSED:
+                p = _i64arr(lv.pos).reshape(-1)
+                c = _i64arr(lv.crd)
+                keep += [p, c]
+                pos[l] = p.ctypes.data_as(N.i64p)
+                crd[l] = c.ctypes.data_as(N.i64p)
+        vals = np.ascontiguousarray(t.vals, dtype=np.float64)
+        check(N.lib().spd_tensor_restage(self.ctx.h, self.h, pos, crd, vals.ctypes.data_as(N.dblp)))
+        return self
+
     @staticmethod
     def pack(ctx: Context, dims, fmt: FormatSpec, coords, values) -> "DeviceTensor":
         """spd_tensor_pack: SparseTensor::pack (tensor.cpp:94-182) on the GPU.
@@ -409,6 +427,21 @@ class DeviceTensor:
         check(N.lib().spd_tensor_place(ctx.h, root, whole.h if whole is not None else None,
                                        1 if split == "row" else 2, C.byref(h), C.byref(b)))
         return DeviceTensor(ctx, h, dims, fmt), b.value
+
+    @staticmethod
+    def upload_piece(ctx: Context, t: SparseTensor, split: str = "nonzero"):
+        """spd_tensor_upload_piece: this GPU's colour of a CSR-like matrix,
+        staged from the host arrays of `t` (whole pos, this colour's crd/vals)."""
+        d, kinds, mo = _format_arrays(t.dims, t.format)
+        p = _i64arr(t.levels[1].pos).reshape(-1)
+        c = _i64arr(t.levels[1].crd)
+        vals = np.ascontiguousarray(t.vals, dtype=np.float64)
+        pos = (N.i64p * 2)(None, p.ctypes.data_as(N.i64p))
+        crd = (N.i64p * 2)(None, c.ctypes.data_as(N.i64p))
+        h = C.c_void_p()
+        check(N.lib().spd_tensor_upload_piece(ctx.h, d, kinds, mo, pos, crd, vals.ctypes.data_as(N.dblp),
+                                              1 if split == "row" else 2, C.byref(h)))
+        return DeviceTensor(ctx, h, t.dims, t.format)
 
     def piece_span(self):
         lo, hi = C.c_int64(), C.c_int64()

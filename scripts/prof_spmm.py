@@ -55,5 +55,7 @@ for _ in range(a.steps):
     else:
         H.spmv(ctx, B, C_d, A_d, pieces=1, stats=False)
 torch.cuda.synchronize()
+if a.kernel != "sddmm":
+    print("digest", int(A_d.view(torch.int64).sum().item()), "nan", bool(torch.isnan(A_d).any().item()))
 print("leaf ms:", [round(x, 3) for x in ctx.read_timing()], "nnz", len(crd))
 ctx.close()

@@ -197,3 +197,90 @@ def test_spadd3_hub_and_short_rows(ctx, pieces):
     got_v, want_v = np.asarray(out[2]), np.asarray(want["out"][2])
     assert np.array_equal(np.signbit(got_v), np.signbit(want_v))
     assert st.work == want["work"]
+
+
+def _same_nnz_matrix(rng, n, m, nnz, integers=True):
+    from paper_2207_13901_b200.host import SparseTensor, parse_format
+
+    lin = rng.choice(n * m, size=nnz, replace=False)
+    coords = np.stack([lin // m, lin % m], 1)
+    vals = rng.integers(1, 9, nnz).astype(float) if integers else rng.uniform(0.5, 1.5, nnz)
+    return SparseTensor.pack((n, m), parse_format("ds"), coords, vals)
+
+
+@pytest.mark.parametrize("kernel", ["spmv", "spmm"])
+def test_restage_reuses_buffers_and_matches(ctx, kernel):
+    """spd_tensor_restage: a new pattern of the same geometry into the old
+    buffers; the derived indices (compacted rows, partition) are rebuilt."""
+    import torch
+
+    from paper_2207_13901_b200 import host as H
+    from paper_2207_13901_b200._native import SpdValidationError
+
+    rng = np.random.default_rng(21)
+    n, m, nnz, N = 300, 250, 4000, 32
+    B1, B2 = _same_nnz_matrix(rng, n, m, nnz), _same_nnz_matrix(rng, n, m, nnz)
+    dev = H.DeviceTensor.upload(ctx, B1)
+    if kernel == "spmv":
+        c = K.dense(rng, (m,), "d")
+        x = torch.from_numpy(c.vals.copy()).cuda()
+        out = torch.empty(n, dtype=torch.float64, device="cuda")
+    else:
+        c = K.dense(rng, (m, N), "dd")
+        x = torch.from_numpy(c.vals.copy()).cuda()
+        out = torch.empty(n * N, dtype=torch.float64, device="cuda")
+    try:
+        for Bt, P in ((B1, 3), (B2, 3), (B1, 5)):
+            if Bt is not B1 or P == 5:
+                dev.restage(Bt)
+            H.partition_nonzero(ctx, dev, 1, P)
+            if kernel == "spmv":
+                st = H.spmv(ctx, dev, x, out, pieces=P)
+            else:
+                st = H.spmm(ctx, dev, x, N, out, pieces=P)
+            want = oracle_execute(kernel, {"B": Bt, ("c" if kernel == "spmv" else "C"): c}, "nonzero", P)
+            assert np.array_equal(out.cpu().numpy().reshape(-1), np.asarray(want["out"]).reshape(-1))
+            assert st.work == want["work"] and st.combines == want["combines"]
+        # a different position count, or a broken pattern, is rejected
+        with pytest.raises(SpdValidationError):
+            dev.restage(_same_nnz_matrix(rng, n, m, nnz + 1))
+        bad = _same_nnz_matrix(rng, n, m, nnz)
+        bad.levels[1].crd = bad.levels[1].crd[::-1].copy()
+        with pytest.raises(SpdValidationError):
+            dev.restage(bad)
+    finally:
+        dev.close()
+
+
+@pytest.mark.parametrize("split", ["nonzero", "row"])
+def test_upload_piece_single_gpu_is_whole(ctx, split):
+    """spd_tensor_upload_piece without a communicator: the piece is the whole
+    matrix; SpMM on it and after a restage matches the oracle."""
+    import torch
+
+    from paper_2207_13901_b200 import host as H
+    from paper_2207_13901_b200._native import SpdValidationError
+
+    rng = np.random.default_rng(5)
+    n, m, nnz, N = 200, 300, 3000, 32
+    c = K.dense(rng, (m, N), "dd")
+    x = torch.from_numpy(c.vals.copy()).cuda()
+    out = torch.empty(n * N, dtype=torch.float64, device="cuda")
+    B1, B2 = _same_nnz_matrix(rng, n, m, nnz), _same_nnz_matrix(rng, n, m, nnz)
+    piece = H.DeviceTensor.upload_piece(ctx, B1, split)
+    try:
+        assert piece.piece_span() == (0, nnz - 1)
+        for i, Bt in enumerate((B1, B2)):
+            if i:
+                piece.restage(Bt)
+            (H.partition_universe(ctx, piece, 1) if split == "row" else H.partition_nonzero(ctx, piece, 1, 1))
+            H.spmm(ctx, piece, x, N, out, pieces=1)
+            want = oracle_execute("spmm", {"B": Bt, "C": c}, split, 1)
+            assert np.array_equal(out.cpu().numpy().reshape(-1), np.asarray(want["out"]).reshape(-1))
+        bad = _same_nnz_matrix(rng, n, m, nnz)
+        bad.levels[1].crd = bad.levels[1].crd.copy()
+        bad.levels[1].crd[10] = m + 5  # out of bounds
+        with pytest.raises(SpdValidationError):
+            piece.restage(bad)
+    finally:
+        piece.close()
