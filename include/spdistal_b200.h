@@ -211,6 +211,32 @@ int spd_partition_universe(spd_context* ctx, const spd_tensor* t, int64_t pieces
  * (planner.cpp:50-69).  The owner searches run warp-parallel on the GPU. */
 int spd_partition_nonzero(spd_context* ctx, const spd_tensor* t, int level, int64_t pieces,
                           spd_color* colors_out);
+/* ---- General dependent partitioning over materialised partitions (device
+ * arrays): replaces image / preimage / partition_by_bounds
+ * (deppart.cpp:15-31, 33-53, 55-91) for arbitrary -- non-contiguous,
+ * overlapping -- colour subsets.  A partition is (pieces, off[pieces+1],
+ * idx[off[pieces]]): colour c's subset is idx[off[c] .. off[c+1]), sorted and
+ * unique as Partition holds it (partition.cpp:10-24); unsorted / out-of-range
+ * input returns SPD_ERR_VALIDATION (the reference throws invalid_argument).
+ * `ranges` is a range region: n inclusive (lo,hi) pairs into [0, dest_extent)
+ * (Region::ranges, region.cpp:33-46; lo > hi is empty).  Outputs: out_off
+ * (pieces+1, device) always; out_idx only when it fits `cap` (call with cap 0
+ * to size it); *total = out_off[pieces]; *disjoint = Partition::disjoint()
+ * (-1 when out_idx was not written). */
+int spd_deppart_image(spd_context* ctx, const int64_t* ranges, int64_t n, int64_t dest_extent,
+                      int64_t pieces, const int64_t* off, const int64_t* idx, int64_t* out_off,
+                      int64_t* out_idx, int64_t cap, int64_t* total, int* disjoint);
+int spd_deppart_preimage(spd_context* ctx, const int64_t* ranges, int64_t n, int64_t dest_extent,
+                         int64_t pieces, const int64_t* dest_off, const int64_t* dest_idx,
+                         int64_t* out_off, int64_t* out_idx, int64_t cap, int64_t* total,
+                         int* disjoint);
+/* partition_by_bounds: colour c (0 <= c < pieces) is the box
+ * bounds[(c*rank + d)*2 + {0,1}] = (lo,hi) per dimension d of a row-major
+ * space `extents` (host arrays), enumerated row-major; a box with an empty
+ * dimension colours nothing; a bound outside the space is a validation error. */
+int spd_deppart_by_bounds(spd_context* ctx, int rank, const int64_t* extents, int64_t pieces,
+                          const int64_t* bounds, int64_t* out_off, int64_t* out_idx, int64_t cap,
+                          int64_t* total, int* disjoint);
 /* Test support (K2m): materialise colour `color`'s subset of a bundle region
  * exactly as the reference's Partition holds it (sorted unique indices).
  *   which: 0 dom, 1 pos, 2 crd of `level`; 3 vals.

@@ -15,6 +15,7 @@
 #include <string>
 #include <vector>
 
+#include "dspar/deppart.hpp"
 #include "dspar/errors.hpp"
 #include "dspar/format_lang.hpp"
 #include "dspar/machine.hpp"
@@ -127,6 +128,36 @@ const TensorPartitionBundle* find_bundle(const RefRun* r, int loop, const char* 
   auto it = bo.find(tensor);
   if (it == bo.end()) return nullptr;
   return &r->compute.bundles[it->second];
+}
+
+}  // namespace
+
+namespace {
+struct RefPart {
+  int status = 0;
+  std::string error;
+  Partition part;
+};
+
+static std::vector<std::vector<int64_t>> subsets_of(int64_t P, const int64_t* off, const int64_t* idx) {
+  std::vector<std::vector<int64_t>> s(static_cast<size_t>(P));
+  for (int64_t c = 0; c < P; c++) s[c].assign(idx + off[c], idx + off[c + 1]);
+  return s;
+}
+
+template <class F>
+static void* part_guarded(F&& f) {
+  auto* r = new RefPart();
+  try {
+    r->part = f();
+  } catch (const std::invalid_argument& e) {
+    r->status = 2;
+    r->error = e.what();
+  } catch (const std::exception& e) {
+    r->status = 1;
+    r->error = e.what();
+  }
+  return r;
 }
 
 }  // namespace
@@ -387,6 +418,65 @@ int ref_out_copy_vals(void* h, double* out) {
 }
 
 // Stats (sim.hpp:25-36) without JSON parsing.
+// ---- dependent partitioning (deppart.cpp:15-101) over flat arrays; pins the
+// device deppart (spd_deppart_*).  Partitions are (P, off[P+1], idx); range
+// regions are n (lo,hi) pairs pointing into dest_extent.  The result is read
+// back with ref_part_*.
+void* ref_image(const int64_t* ranges, int64_t n, int64_t dest_extent, int64_t P, const int64_t* off,
+                const int64_t* idx) {
+  return part_guarded([&] {
+    std::vector<CoordRange> rs(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; i++) rs[i] = CoordRange{ranges[2 * i], ranges[2 * i + 1]};
+    Region src = Region::ranges(IndexSpace({n}), std::move(rs), dest_extent);
+    Partition p(IndexSpace({n}), subsets_of(P, off, idx));
+    return image(src, p, IndexSpace({dest_extent}));
+  });
+}
+
+void* ref_preimage(const int64_t* ranges, int64_t n, int64_t dest_extent, int64_t P, const int64_t* off,
+                   const int64_t* idx) {
+  return part_guarded([&] {
+    std::vector<CoordRange> rs(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; i++) rs[i] = CoordRange{ranges[2 * i], ranges[2 * i + 1]};
+    Region src = Region::ranges(IndexSpace({n}), std::move(rs), dest_extent);
+    Partition p(IndexSpace({dest_extent}), subsets_of(P, off, idx));
+    return preimage(src, p, IndexSpace({dest_extent}));
+  });
+}
+
+// colors[k] with box bounds[k*rank*2 ...] (lo,hi per dimension).
+void* ref_partition_by_bounds(int rank, const int64_t* extents, int64_t nentries, const int64_t* colors,
+                              const int64_t* bounds) {
+  return part_guarded([&] {
+    std::map<int64_t, std::vector<CoordRange>> coloring;
+    for (int64_t k = 0; k < nentries; k++) {
+      std::vector<CoordRange> b(static_cast<size_t>(rank));
+      for (int d = 0; d < rank; d++) b[d] = CoordRange{bounds[(k * rank + d) * 2], bounds[(k * rank + d) * 2 + 1]};
+      coloring[colors[k]] = b;
+    }
+    return partition_by_bounds(IndexSpace(std::vector<int64_t>(extents, extents + rank)), coloring);
+  });
+}
+
+int ref_part_status(void* h) { return static_cast<RefPart*>(h)->status; }
+const char* ref_part_error(void* h) { return static_cast<RefPart*>(h)->error.c_str(); }
+int64_t ref_part_colors(void* h) { return static_cast<RefPart*>(h)->part.num_colors(); }
+int ref_part_disjoint(void* h) { return static_cast<RefPart*>(h)->part.disjoint() ? 1 : 0; }
+// off: P+1 entries; idx: off[P] entries (either may be NULL)
+void ref_part_copy(void* h, int64_t* off, int64_t* idx) {
+  const Partition& p = static_cast<RefPart*>(h)->part;
+  int64_t o = 0;
+  for (int64_t c = 0; c < p.num_colors(); c++) {
+    if (off) off[c] = o;
+    for (int64_t v : p.subset(c)) {
+      if (idx) idx[o] = v;
+      o++;
+    }
+  }
+  if (off) off[p.num_colors()] = o;
+}
+void ref_part_free(void* h) { delete static_cast<RefPart*>(h); }
+
 int64_t ref_stats_workers(void* h) { return static_cast<RefRun*>(h)->result.stats.workers; }
 int64_t ref_stats_combines(void* h) { return static_cast<RefRun*>(h)->result.stats.combines; }
 double ref_stats_imbalance(void* h) { return static_cast<RefRun*>(h)->result.stats.imbalance; }

@@ -589,6 +589,96 @@ def partition_nonzero(ctx: Context, t: DeviceTensor, level: int, pieces: int, ho
     return _colours(arr) if host else None
 
 
+# ------------------------------------------------- general deppart (8f.4) ---
+class DevicePartition:
+    """A materialised partition in HBM: (off[P+1], idx) int64 device tensors,
+    colour c = idx[off[c]:off[c+1]] sorted and unique (Partition,
+    partition.hpp:16-46)."""
+
+    def __init__(self, off, idx, disjoint=None):
+        self.off, self.idx, self.disjoint = off, idx, disjoint
+
+    @property
+    def num_colors(self):
+        return self.off.numel() - 1
+
+    @staticmethod
+    def from_subsets(subsets, device="cuda"):
+        import torch
+
+        off = np.zeros(len(subsets) + 1, np.int64)
+        for c, sub in enumerate(subsets):
+            off[c + 1] = off[c] + len(sub)
+        idx = (np.concatenate([np.asarray(x, np.int64) for x in subsets]) if len(subsets)
+               else np.zeros(0, np.int64))
+        return DevicePartition(torch.from_numpy(off).to(device), torch.from_numpy(idx).to(device))
+
+    def subsets(self):
+        off = self.off.cpu().numpy()
+        idx = self.idx.cpu().numpy()
+        return [idx[off[c]:off[c + 1]].copy() for c in range(len(off) - 1)]
+
+
+def _deppart_call(fn, ctx, pieces, args):
+    """Two-phase call: size, then fill."""
+    import torch
+
+    dev = torch.device("cuda", ctx.device)
+    out_off = torch.empty(pieces + 1, dtype=torch.int64, device=dev)
+    total = C.c_int64()
+    disj = C.c_int()
+    check(fn(ctx.h, *args, C.c_void_p(out_off.data_ptr()), None, 0, C.byref(total), C.byref(disj)))
+    out_idx = torch.empty(max(total.value, 1), dtype=torch.int64, device=dev)
+    check(fn(ctx.h, *args, C.c_void_p(out_off.data_ptr()), C.c_void_p(out_idx.data_ptr()), total.value,
+             C.byref(total), C.byref(disj)))
+    return DevicePartition(out_off, out_idx[:total.value], bool(disj.value))
+
+
+def _ranges_dev(ranges, device):
+    import torch
+
+    if isinstance(ranges, torch.Tensor):
+        r = ranges.to(device=device, dtype=torch.int64).contiguous().reshape(-1, 2)
+    else:
+        r = torch.from_numpy(np.ascontiguousarray(np.asarray(ranges, np.int64).reshape(-1, 2))).to(device)
+    return r
+
+
+def image(ctx: Context, ranges, part: DevicePartition, dest_extent: int) -> DevicePartition:
+    """spd_deppart_image: image(source, src_part, dest) (deppart.cpp:15-31)."""
+    r = _ranges_dev(ranges, part.off.device)
+    return _deppart_call(N.lib().spd_deppart_image, ctx, part.num_colors,
+                         (C.c_void_p(r.data_ptr()), r.shape[0], dest_extent, part.num_colors,
+                          C.c_void_p(part.off.data_ptr()), C.c_void_p(part.idx.data_ptr())))
+
+
+def preimage(ctx: Context, ranges, part: DevicePartition, dest_extent: int) -> DevicePartition:
+    """spd_deppart_preimage: preimage(source, dest_part, dest) (deppart.cpp:33-53)."""
+    r = _ranges_dev(ranges, part.off.device)
+    return _deppart_call(N.lib().spd_deppart_preimage, ctx, part.num_colors,
+                         (C.c_void_p(r.data_ptr()), r.shape[0], dest_extent, part.num_colors,
+                          C.c_void_p(part.off.data_ptr()), C.c_void_p(part.idx.data_ptr())))
+
+
+def partition_by_bounds(ctx: Context, extents, coloring: dict) -> DevicePartition:
+    """spd_deppart_by_bounds: partition_by_bounds(space, coloring)
+    (deppart.cpp:55-91); coloring = {colour: [(lo, hi) per dimension]};
+    colours absent from the map are empty."""
+    ext = np.asarray(extents, np.int64)
+    R = len(ext)
+    P = (max(coloring) + 1) if coloring else 0
+    if any(c < 0 for c in coloring):
+        raise N.SpdValidationError("partition_by_bounds: negative color")
+    b = np.tile(np.array([1, 0], np.int64), P * R).reshape(P, R, 2)  # empty boxes
+    for c, box in coloring.items():
+        if len(box) != R:
+            raise N.SpdValidationError("partition_by_bounds: bounds rank mismatch")
+        b[c] = np.asarray(box, np.int64)
+    b = np.ascontiguousarray(b.reshape(-1))
+    return _deppart_call(N.lib().spd_deppart_by_bounds, ctx, P,
+                         (R, ext.ctypes.data_as(N.i64p), P, b.ctypes.data_as(N.i64p)))
+
+
 REGION = {"dom": 0, "pos": 1, "crd": 2, "vals": 3}
 
 

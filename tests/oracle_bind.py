@@ -252,6 +252,12 @@ def ref(path=REF_LIB):
             ("ref_load", vp, [C.c_char_p, C.c_char_p, C.c_int, i64p]),
             ("ref_out_dims", C.c_int, [vp, i64p]),
             ("ref_store", C.c_int, [vp, C.c_char_p]),
+            ("ref_image", vp, [i64p, i64, i64, i64, i64p, i64p]),
+            ("ref_preimage", vp, [i64p, i64, i64, i64, i64p, i64p]),
+            ("ref_partition_by_bounds", vp, [C.c_int, i64p, i64, i64p, i64p]),
+            ("ref_part_status", C.c_int, [vp]), ("ref_part_error", C.c_char_p, [vp]),
+            ("ref_part_colors", i64, [vp]), ("ref_part_disjoint", C.c_int, [vp]),
+            ("ref_part_copy", None, [vp, i64p, i64p]), ("ref_part_free", None, [vp]),
         ]:
             f = getattr(L, name)
             f.restype = res
@@ -434,3 +440,58 @@ def dense_eval(expr, tensors, out_dims):
     if st:
         raise RuntimeError(err.value.decode())
     return out.reshape(out_dims)
+
+
+# ---- dependent partitioning through the reference (deppart.cpp:15-101) ----
+class RefPartitionError(Exception):
+    def __init__(self, status, msg):
+        super().__init__(msg)
+        self.status = status
+
+
+def _flat_partition(subsets):
+    off = np.zeros(len(subsets) + 1, np.int64)
+    for c, s in enumerate(subsets):
+        off[c + 1] = off[c] + len(s)
+    idx = np.concatenate([np.asarray(s, np.int64) for s in subsets]) if subsets else np.zeros(0, np.int64)
+    return off, np.ascontiguousarray(idx, dtype=np.int64)
+
+
+def _read_part(L, h):
+    try:
+        if L.ref_part_status(h):
+            raise RefPartitionError(L.ref_part_status(h), L.ref_part_error(h).decode())
+        P = L.ref_part_colors(h)
+        off = np.zeros(P + 1, np.int64)
+        L.ref_part_copy(h, _p(off), None)
+        idx = np.zeros(max(int(off[-1]), 1), np.int64)
+        L.ref_part_copy(h, _p(off), _p(idx))
+        return [idx[off[c]:off[c + 1]].copy() for c in range(P)], bool(L.ref_part_disjoint(h))
+    finally:
+        L.ref_part_free(h)
+
+
+def ref_image(ranges, subsets, dest_extent):
+    """The reference's image (deppart.cpp:15-31): (subsets, disjoint)."""
+    L = ref()
+    r = np.ascontiguousarray(np.asarray(ranges, np.int64).reshape(-1, 2))
+    off, idx = _flat_partition(subsets)
+    return _read_part(L, L.ref_image(_p(r), len(r), dest_extent, len(subsets), _p(off), _p(idx)))
+
+
+def ref_preimage(ranges, subsets, dest_extent):
+    """The reference's preimage (deppart.cpp:33-53): (subsets, disjoint)."""
+    L = ref()
+    r = np.ascontiguousarray(np.asarray(ranges, np.int64).reshape(-1, 2))
+    off, idx = _flat_partition(subsets)
+    return _read_part(L, L.ref_preimage(_p(r), len(r), dest_extent, len(subsets), _p(off), _p(idx)))
+
+
+def ref_partition_by_bounds(extents, coloring):
+    """The reference's partition_by_bounds (deppart.cpp:55-91); coloring:
+    {colour: [(lo, hi) per dimension]}."""
+    L = ref()
+    ext = np.asarray(extents, np.int64)
+    cols = np.asarray(sorted(coloring), np.int64)
+    b = np.asarray([coloring[c] for c in sorted(coloring)], np.int64).reshape(-1)
+    return _read_part(L, L.ref_partition_by_bounds(len(ext), _p(ext), len(cols), _p(cols), _p(b)))
