@@ -274,7 +274,8 @@ __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + 
 spd_context* checked(spd_context* ctx);
 void activate(spd_context* ctx);
 const std::vector<spd_color>& host_colors(spd_context* ctx);  // syncs if needed
-void require_partition(spd_context* ctx, const spd_tensor* t, int64_t first, int64_t count);
+void require_partition(spd_context* ctx, const spd_tensor* t, int64_t first, int64_t count,
+                       bool allow_grid = false);
 void fill_stats(spd_context* ctx, spd_stats* st, int64_t combines, const std::vector<int64_t>& work,
                 int64_t launches, bool timed);
 // Brackets the leaf kernel of an op with a timing event pair when enabled.

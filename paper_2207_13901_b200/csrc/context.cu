@@ -286,17 +286,23 @@ const std::vector<spd_color>& host_colors(spd_context* ctx) {
   return ctx->colors_host;
 }
 
-void require_partition(spd_context* ctx, const spd_tensor* t, int64_t first, int64_t count) {
+void require_partition(spd_context* ctx, const spd_tensor* t, int64_t first, int64_t count, bool allow_grid) {
   if (ctx->split == SplitKind::None || ctx->split_tensor != t)
     throw ValidationError("no partition of this tensor on the context: call spd_partition_* first");
   if (first < 0 || count < 1 || first + count > ctx->pieces)
     throw ValidationError("colour range outside the partition");
   bool all = first == 0 && count == ctx->pieces;
   bool one_per_rank = ctx->comm && count == 1 && ctx->pieces == ctx->world && first == ctx->rank;
-  if (!all && !one_per_rank)
+  // 2-D machine grid (x major, y minor; MachineGrid::worker_id, machine.cpp:88-92)
+  // with the row loop on x: rank r runs row colour r / (world / pieces) of a
+  // universe split -- rows never straddle colours, so no cross-GPU combine.
+  bool grid_row = allow_grid && ctx->comm && count == 1 && ctx->split == SplitKind::Universe &&
+                  ctx->pieces > 0 && ctx->world % ctx->pieces == 0 &&
+                  first == ctx->rank / (ctx->world / ctx->pieces);
+  if (!all && !one_per_rank && !grid_row)
     throw ValidationError(
         "a GPU runs either every colour of the partition, or (with a communicator) exactly the "
-        "colour equal to its rank with pieces == world");
+        "colour equal to its rank with pieces == world (row loops of a 2-D grid: colour rank / (world / pieces))");
 }
 
 void fill_stats(spd_context* ctx, spd_stats* st, int64_t combines, const std::vector<int64_t>& work,

@@ -886,7 +886,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   checked(ctx);
   const spd_tensor* B = a.B;
   if (!B) throw ValidationError("null tensor");
-  require_partition(ctx, B, first, count);
+  require_partition(ctx, B, first, count, true);
   activate(ctx);
   const int nl = (int)B->levels.size();
   const bool csf = a.op == Op::SpTTV || a.op == Op::SpMTTKRP;
@@ -1145,7 +1145,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
     launches++;
   }
   trace_mark(ctx);
-  if (ctx->comm && count == 1 && P > 1) {
+  if (ctx->comm && count == 1 && P > 1 && ctx->split != SplitKind::Universe) {  // rows cut between GPUs
     const size_t bytes = sizeof(int64_t) * (W + 2);
     SPD_NCCL(ncclAllGather(col.head_pack + first * (W + 2), col.head_pack, bytes, ncclUint8,
                            ctx->comm, s));

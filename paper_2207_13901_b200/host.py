@@ -736,6 +736,65 @@ def spmm(ctx, B: DeviceTensor, Cd, n_cols, A, first=0, count=None, pieces=None, 
     return _stats(ctx, st, pieces) if stats else None
 
 
+def divide_bounds(n: int, pieces: int):
+    """divide_bounds (planner.cpp:10-20): block = n / pieces (truncating);
+    colour c < pieces-1 -> [c*block, c*block+block-1], the last -> [.., n-1]."""
+    block = n // pieces
+    return [(c * block, c * block + block - 1) if c < pieces - 1 else ((pieces - 1) * block, n - 1)
+            for c in range(pieces)]
+
+
+def spmm_batched(ctx, B: DeviceTensor, Cd, n_cols, A, grid, rank=None, stats=True):
+    """SpDISTAL-Batched SpMM (2-D machine grid x=Px, y=Py,
+    test_planner.cpp:193-225): rows of B/A divided over x (a universe split
+    of B, spd_partition_universe with Px pieces), the columns j of C/A
+    divided over y (divide_bounds on N).  Worker (x, y) computes the block
+    A[rows_x, slab_y] = B[rows_x, :] * C[:, slab_y] from its column slab of C
+    only, so C is partitioned instead of replicated; no combine.
+
+    Single GPU (rank None): every tuple, in worker order x*Py + y
+    (MachineGrid::worker_id, machine.cpp:88-92).  With a communicator of
+    Px*Py GPUs: this rank's tuple; Cd is then this rank's slab (K x w,
+    contiguous) and A its n x w block buffer (rows outside rows_x untouched).
+    Stats: work[x*Py+y] = nnz(rows_x) * w_y, combines 0."""
+    import torch
+
+    Px, Py = grid
+    n = B.dims[0]
+    slabs = divide_bounds(n_cols, Py)
+    cols = partition_universe(ctx, B, Px)
+    if rank is not None:
+        x, y = divmod(rank, Py)
+        lo, hi = slabs[y]
+        w = max(hi - lo + 1, 0)
+        if w > 0:
+            spmm(ctx, B, Cd, w, A, first=x, count=1, pieces=Px, stats=False)
+        tuples = [(x, y)]
+    else:
+        K = Cd.numel() // n_cols if n_cols else 0
+        Cv = Cd.view(K, n_cols)
+        Av = A.view(n, n_cols)
+        for y, (lo, hi) in enumerate(slabs):
+            w = hi - lo + 1
+            if w <= 0:
+                continue
+            Cy = Cv[:, lo:hi + 1].contiguous()
+            Ay = torch.empty(n * w, dtype=torch.float64, device=A.device)
+            spmm(ctx, B, Cy, w, Ay, pieces=Px, stats=False)
+            Av[:, lo:hi + 1] = Ay.view(n, w)
+        tuples = [(x, y) for x in range(Px) for y in range(Py)]
+    if not stats:
+        return None
+    nnz_x = [c.q[1] - c.q[0] + 1 if c.q[0] <= c.q[1] else 0 for c in cols]  # crd image of rows_x
+    work = [0] * (Px * Py)
+    for x in range(Px):
+        for y, (lo, hi) in enumerate(slabs):
+            work[x * Py + y] = nnz_x[x] * max(hi - lo + 1, 0)
+    total, mx = sum(work), max(work) if work else 0
+    imb = 1.0 if total == 0 else mx * len(work) / total
+    return Stats(Px * Py, work, imb, 0)
+
+
 def sddmm(ctx, B: DeviceTensor, Cd, Dd, K, dk, dj, Avals, first=0, count=None, pieces=None, stats=True):
     st = N.spd_stats()
     count = pieces - first if count is None else count

@@ -23,6 +23,7 @@ def main():
     import torch
     import torch.distributed as dist
 
+    import oracle_bind as ob
     import oracle_exec
     import spd_kernels as K
     from paper_2207_13901_b200 import host as H
@@ -171,6 +172,41 @@ def main():
                       f"{'OK' if ok else 'MISMATCH'} piece=[{lo},{hi}]", flush=True)
                 failures += 0 if ok else 1
         piece.close()
+
+    # SpDISTAL-Batched SpMM on a 2-D grid of the GPUs (x = rows, y = column
+    # slabs of C / A): every GPU holds only its slab of C, no combine.
+    BATCHED = ("divide(i, io, ii, M.x); divide(j, jo, ji, M.y); reorder(io, jo, ii, ji, k); "
+               "distribute(io, M.x); distribute(jo, M.y); communicate({B}, io); communicate({A, C}, jo)")
+    for Px in [d for d in range(1, world + 1) if world % d == 0]:
+        Py = world // Px
+        rng = np.random.default_rng(500 + Px)
+        n, m, N = 700, 500, 24
+        B = K.random_sparse(rng, (n, m), "ds", 0.05, True)
+        Cm = K.dense(rng, (m, N), "dd", True)
+        Bd = H.DeviceTensor.upload(ctx, B)
+        x, y = divmod(rank, Py)
+        lo, hi = H.divide_bounds(N, Py)[y]
+        w = hi - lo + 1
+        Cs = torch.from_numpy(np.ascontiguousarray(Cm.vals.reshape(m, N)[:, lo:hi + 1])).to(dev)
+        Ab = torch.full((n * max(w, 1),), float("nan"), dtype=torch.float64, device=dev)
+        H.spmm_batched(ctx, Bd, Cs, N, Ab, (Px, Py), rank=rank, stats=False)
+        cols_ = H.partition_universe(ctx, Bd, Px)
+        r0, r1 = cols_[x].top
+        block = Ab.view(n, max(w, 1))[r0:r1 + 1, :w].cpu().numpy() if r0 <= r1 else np.zeros((0, w))
+        blocks = [None] * world
+        dist.all_gather_object(blocks, (r0, r1, lo, hi, block))
+        if rank == 0:
+            got = np.full((n, N), np.nan)
+            for (a, b, c0, c1, blk) in blocks:
+                if a <= b and c0 <= c1:
+                    got[a:b + 1, c0:c1 + 1] = blk
+            run = ob.RefRun("A(i, j) = B(i, k) * C(k, j)", BATCHED, f"x={Px},y={Py}", "dd",
+                            K.ref_inputs("spmm", {"B": B, "C": Cm})).ok()
+            want = run.output()[1].reshape(n, N)
+            ok = np.array_equal(got, want)
+            print(f"[mgpu world={world}] batched spmm grid x={Px},y={Py}: {'OK' if ok else 'MISMATCH'}", flush=True)
+            failures += 0 if ok else 1
+        Bd.close()
 
     # SpAdd3: every GPU assembles its row block, global pos offsets from the
     # all-gathered per-GPU nnz, pieces gathered on rank 0 with NCCL send/recv.

@@ -284,3 +284,43 @@ def test_upload_piece_single_gpu_is_whole(ctx, split):
             piece.restage(bad)
     finally:
         piece.close()
+
+
+BATCHED = ("divide(i, io, ii, M.x); divide(j, jo, ji, M.y); reorder(io, jo, ii, ji, k); "
+           "distribute(io, M.x); distribute(jo, M.y); communicate({B}, io); communicate({A, C}, jo)")
+
+
+@pytest.mark.parametrize("grid", [(2, 2), (3, 2), (1, 4), (4, 3)])
+def test_spmm_batched_two_dimensional_grid(ctx, grid):
+    """SpDISTAL-Batched SpMM on a 2-D machine grid (test_planner.cpp:193-225):
+    output, per-worker work, imbalance and combines against the reference's
+    own plan() + execute() with the same grid."""
+    import torch
+
+    import oracle_bind as ob
+    from paper_2207_13901_b200 import host as H
+
+    rng = np.random.default_rng(sum(grid))
+    for integers in (True, False):
+        n, m, N = 60, 45, 10
+        B = K.random_sparse(rng, (n, m), "ds", 0.15, integers)
+        Cm = K.dense(rng, (m, N), "dd", integers)
+        tensors = {"B": B, "C": Cm}
+        run = ob.RefRun("A(i, j) = B(i, k) * C(k, j)", BATCHED, f"x={grid[0]},y={grid[1]}", "dd",
+                        K.ref_inputs("spmm", tensors)).ok()
+        _, want = run.output()
+        st_ref = run.stats()
+        dev = H.DeviceTensor.upload(ctx, B)
+        try:
+            Cd = torch.from_numpy(Cm.vals.copy()).cuda()
+            A = torch.full((n * N,), float("nan"), dtype=torch.float64, device="cuda")
+            st = H.spmm_batched(ctx, dev, Cd, N, A, grid)
+            got = A.cpu().numpy()
+            if integers:
+                assert np.array_equal(got, want)
+            else:
+                assert np.all(np.abs(got - want) <= 1e-10 * np.maximum(np.abs(want), 1e-300))
+            assert st.workers == st_ref["workers"] and st.work == st_ref["work"]
+            assert st.combines == st_ref["combines"] and st.imbalance == pytest.approx(st_ref["imbalance"], rel=0, abs=0)
+        finally:
+            dev.close()
