@@ -631,6 +631,23 @@ __global__ void k_leaf_rowptr(const int64_t* __restrict__ rp1, const int64_t* __
     out[i] = rp2[rp1[i]];
 }
 
+// Compressed top level (an sss CSF): output row i's leaves start at the
+// first top position whose coordinate is >= i (rows absent from crd0 are
+// empty), so out is a dense row pointer over [0, I] like the dss one.
+__global__ void k_leaf_rowptr_sparse_top(const int64_t* __restrict__ crd0, int64_t n0,
+                                         const int64_t* __restrict__ rp1, const int64_t* __restrict__ rp2,
+                                         int64_t I, int64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i <= I;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n0;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (crd0[mid] < i) lo = mid + 1; else hi = mid;
+    }
+    out[i] = rp2[rp1[lo]];
+  }
+}
+
 // ---------------------------------------------------------------------------
 enum class Op { SpMV, SpMM, SpTTV, SpMTTKRP };
 
@@ -891,9 +908,12 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   const int nl = (int)B->levels.size();
   const bool csf = a.op == Op::SpTTV || a.op == Op::SpMTTKRP;
   if (csf) {
-    if (nl != 3 || B->levels[0].kind != SPD_DENSE || B->levels[1].kind != SPD_COMPRESSED ||
-        B->levels[2].kind != SPD_COMPRESSED || B->levels[0].dom.size() != 1)
-      throw ValidationError("unsupported on gpu: this kernel needs a dss (Dense, Compressed, Compressed) 3-tensor");
+    // dss (the paper's Dense-outer CSF) or sss (every level compressed)
+    const bool top_ok = (B->levels[0].kind == SPD_DENSE && B->levels[0].dom.size() == 1) ||
+                        (B->levels[0].kind == SPD_COMPRESSED && B->levels[0].parent_positions == 1);
+    if (nl != 3 || !top_ok || B->levels[1].kind != SPD_COMPRESSED || B->levels[2].kind != SPD_COMPRESSED ||
+        B->groups[0].size() != 1 || B->groups[1].size() != 1 || B->groups[2].size() != 1)
+      throw ValidationError("unsupported on gpu: this kernel needs a dss or sss 3-tensor (CSF)");
   } else if (nl != 2 || B->levels[0].kind != SPD_DENSE || B->levels[1].kind != SPD_COMPRESSED ||
              B->levels[0].dom.size() != 1) {
     throw ValidationError("unsupported on gpu: this kernel needs a ds (CSR-like) matrix");
@@ -918,13 +938,19 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
       out_level = 1;
       break;
     case Op::SpMTTKRP: {
-      const int64_t I = B->levels[1].parent_positions;
+      const bool sparse_top = B->levels[0].kind == SPD_COMPRESSED;
+      const int64_t I = sparse_top ? B->dims[B->mode_order[0]] : B->levels[1].parent_positions;
       spd_tensor* Bm = const_cast<spd_tensor*>(B);
       if (!Bm->leaf_rowptr) {
         SPD_CUDA(cudaMallocAsync((void**)&Bm->leaf_rowptr, sizeof(int64_t) * (I + 1), ctx->stream));
-        k_leaf_rowptr<<<(unsigned)std::min<int64_t>(ceil_div(I + 1, 256), 4096), 256, 0,
-                        ctx->stream>>>(B->levels[1].rowptr, B->levels[2].rowptr, I,
-                                       Bm->leaf_rowptr);
+        const unsigned gr = (unsigned)std::min<int64_t>(ceil_div(I + 1, 256), 4096);
+        if (sparse_top)
+          k_leaf_rowptr_sparse_top<<<gr, 256, 0, ctx->stream>>>(B->levels[0].crd, B->levels[0].positions,
+                                                                B->levels[1].rowptr, B->levels[2].rowptr, I,
+                                                                Bm->leaf_rowptr);
+        else
+          k_leaf_rowptr<<<gr, 256, 0, ctx->stream>>>(B->levels[1].rowptr, B->levels[2].rowptr, I,
+                                                     Bm->leaf_rowptr);
         SPD_CHECK_LAUNCH();
       }
       g.R = B->leaf_rowptr;
