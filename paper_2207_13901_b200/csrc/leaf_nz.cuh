@@ -263,6 +263,130 @@ __global__ void __launch_bounds__(kBlock, 5) k_spmv_nz(WalkGeom g, NzView z, con
 }
 
 // ---------------------------------------------------------------------------
+// SpMV / SpTTV for short rows (uniform matrices, CSF fibres): lane = one
+// compacted row of the chunk, summed serially in stored-position order (the
+// reference's own order, sim.cpp:326-354) with 4 independent gathers in
+// flight; rows longer than kRowsLong are summed by the whole warp instead
+// (coalesced loads, lane-strided partials + butterfly).  Per 32 positions
+// this issues ~20 warp instructions where the window scan of k_spmv_nz
+// issues ~300 when rows are ~10 long.  Chunk / colour records as k_spmv_nz.
+constexpr int kRowsLong = 48;
+
+__device__ __forceinline__ double row_dot_serial(const int64_t* __restrict__ crd, const double* __restrict__ vals,
+                                                 const double* __restrict__ x, int64_t a, int64_t b) {
+  // L1-allocating loads: a lane walks consecutive positions of its row, so
+  // the 32-byte sectors it touches are reused from L1 by its next loads
+  double sum = 0.0;
+  int64_t q = a;
+  for (; q + 3 <= b; q += 4) {
+    const int64_t k0 = __ldg(crd + q), k1 = __ldg(crd + q + 1), k2 = __ldg(crd + q + 2), k3 = __ldg(crd + q + 3);
+    const double v0 = __ldg(vals + q), v1 = __ldg(vals + q + 1), v2 = __ldg(vals + q + 2), v3 = __ldg(vals + q + 3);
+    const double x0 = __ldg(x + k0), x1 = __ldg(x + k1), x2 = __ldg(x + k2), x3 = __ldg(x + k3);
+    sum += v0 * x0;
+    sum += v1 * x1;
+    sum += v2 * x2;
+    sum += v3 * x3;
+  }
+  if (q <= b) {  // up to 3 more, loads issued together
+    const int64_t k0 = __ldg(crd + q), k1 = q + 1 <= b ? __ldg(crd + q + 1) : 0, k2 = q + 2 <= b ? __ldg(crd + q + 2) : 0;
+    const double v0 = __ldg(vals + q), v1 = q + 1 <= b ? __ldg(vals + q + 1) : 0.0;
+    const double v2 = q + 2 <= b ? __ldg(vals + q + 2) : 0.0;
+    const double x0 = __ldg(x + k0), x1 = q + 1 <= b ? __ldg(x + k1) : 0.0, x2 = q + 2 <= b ? __ldg(x + k2) : 0.0;
+    sum += v0 * x0;
+    if (q + 1 <= b) sum += v1 * x1;
+    if (q + 2 <= b) sum += v2 * x2;
+  }
+  return sum;
+}
+
+__global__ void __launch_bounds__(kBlock, 4) k_spmv_rows(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
+                                                      const double* __restrict__ vals,
+                                                      const double* __restrict__ x, double* __restrict__ y,
+                                                      ChunkRecs rec, const int64_t* __restrict__ counters) {
+  const int lane = lane_id();
+  const int64_t begin = counters[1], end = counters[2];
+  const uint64_t pol = l2_policy_evict_first();
+  for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
+    const ChunkInfo ci = chunk_info(g, v, begin);
+    if (ci.q_lo > ci.q_hi) {
+      zero_gap(y, 1, ci.w_lo, ci.w_hi);
+      if (lane == 0) rec.row[2 * ci.local] = -1, rec.row[2 * ci.local + 1] = -1, rec.cont[ci.local] = 0;
+      continue;
+    }
+    const int64_t k = ci.local, s = ci.s, e = ci.e;
+    const int64_t ic0 = warp_owner(z.ptr, z.m, s);  // the last row is found by the walk itself
+    const bool head = ld64(z.ptr + ic0) < s;
+    int64_t ic1 = z.m - 1;
+    if (s == ci.q_lo && !head) zero_gap(y, 1, ci.w_lo, ld64(z.id + ic0) - 1);
+    int64_t head_row = -1, tail_row = -1;
+    int head_cont = 0;
+    double head_val = 0.0, tail_val = 0.0;
+    for (int64_t g0 = ic0; g0 <= ic1; g0 += 32) {
+      const int64_t r = g0 + lane;
+      const int64_t pa = r < z.m ? ld64(z.ptr + r) : INT64_MAX;
+      // rows of this group that start inside the chunk (or the head row)
+      const unsigned in = __ballot_sync(FULL, r == ic0 || pa <= e);
+      if (in != FULL) ic1 = g0 + 31 - __clz(in);  // the chunk's last row is in this group
+      const bool act = r <= ic1;
+      int64_t a = 0, b = -1, id = -1, nid = -1, rend = -1;
+      if (act) {
+        rend = ld64(z.ptr + r + 1) - 1;
+        a = max(pa, s);
+        b = min(rend, e);
+        id = ld64(z.id + r);
+        nid = r + 1 < z.m ? ld64(z.id + r + 1) : -1;
+      }
+      const bool lng = act && b - a + 1 > kRowsLong;
+      double sum = 0.0;
+      if (act && !lng) sum = row_dot_serial(crd, vals, x, a, b);
+      unsigned long_mask = __ballot_sync(FULL, lng);
+      while (long_mask) {
+        const int t = __ffs(long_mask) - 1;
+        long_mask &= long_mask - 1;
+        const int64_t aa = __shfl_sync(FULL, a, t), bb = __shfl_sync(FULL, b, t);
+        double part = 0.0;
+        for (int64_t q = aa + lane; q <= bb; q += 32)
+          part += ld_f64_hint(vals + q, pol) * __ldg(x + ld_i64_hint(crd + q, pol));
+        part = warp_sum(part);
+        if (lane == t) sum = part;
+      }
+      if (act) {
+        const bool is_head = r == ic0 && head;
+        const bool ends_here = rend <= e;
+        if (is_head) {
+          head_row = id;
+          head_val = sum;
+          head_cont = ends_here ? 0 : 1;
+        } else if (!ends_here) {
+          tail_row = id;
+          tail_val = sum;
+        } else {
+          y[id] = sum;
+        }
+        if (ends_here) {  // empty rows up to the next non-empty one (bounded by W_c at a chunk end)
+          const int64_t stop = rend == e ? (nid < 0 ? ci.w_hi : min(nid - 1, ci.w_hi)) : nid - 1;
+          for (int64_t rr = id + 1; rr <= stop; rr++) y[rr] = 0.0;
+        }
+      }
+    }
+    // records of the chunk's first (head) and last (tail) rows
+    head_row = __shfl_sync(FULL, head_row, 0);  // the head row is lane 0 of the first group
+    head_val = __shfl_sync(FULL, head_val, 0);
+    head_cont = __shfl_sync(FULL, head_cont, 0);
+    const int tl = (int)((ic1 - ic0) & 31);  // the tail row is lane (ic1 - ic0) % 32 of the last group
+    tail_row = __shfl_sync(FULL, tail_row, tl);
+    tail_val = __shfl_sync(FULL, tail_val, tl);
+    if (lane == 0) {
+      rec.row[2 * k] = head_row;
+      rec.row[2 * k + 1] = tail_row;
+      rec.cont[k] = head_cont;
+      rec.val[2 * k] = head_val;
+      rec.val[2 * k + 1] = tail_val;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // SpMM N == 32 over the compacted view: half a warp per position, 128-bit
 // register gathers UNR pairs deep, crd/vals of the next window prefetched,
 // row switches from the window mask (no dependent loads on the critical path).

@@ -863,6 +863,21 @@ static int hot_enabled() {
   return v;
 }
 
+// SpMV / SpTTV leaf choice: the lane-per-row kernel when the non-empty rows
+// are not long on average (SPD_SPMV_ROWS: 1 always, 0 never, unset: average
+// <= kRowsAvg positions per non-empty row), else the window-scan walk.
+// Measured (profiles/README.md): C1 uniform 0.184 -> 0.117 ms, C4 SpTTV
+// 0.255 -> 0.19 ms, R-MAT SpMV leaf 1.32 -> 1.12 ms.
+constexpr int64_t kRowsAvg = 64;
+static bool spmv_rows_mode(int64_t nnz, int64_t m) {
+  static int v = [] {
+    const char* e = getenv("SPD_SPMV_ROWS");
+    return e ? atoi(e) : -1;
+  }();
+  if (v >= 0) return v != 0;
+  return m > 0 && nnz <= kRowsAvg * m;
+}
+
 // Whether an op walks the compacted view (default) -- SPD_NZ=0 selects the
 // direct row-pointer walks (kept for comparison).
 static bool nz_enabled() {
@@ -964,13 +979,19 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   g.W = a.W;
   // Positions per chunk: ~256 KB of operand traffic per warp-chunk for the
   // column kernels, 2048 positions for the scalar ones.
-  g.CH = (a.op == Op::SpMV || a.op == Op::SpTTV) ? 2048 : 1024;
+  // (the lane-per-row SpMV kernel balances small problems better with 1024)
+  g.CH = (a.op == Op::SpMV || a.op == Op::SpTTV) ? (nnz < (int64_t(1) << 26) ? 1024 : 2048) : 1024;
   {
     static int64_t ch_override = [] {
       const char* e = getenv("SPD_CH");
       return e ? atoll(e) : 0;
     }();
     if (ch_override >= 32 && a.op == Op::SpMM) g.CH = ch_override;
+    static int64_t ch_spmv = [] {
+      const char* e = getenv("SPD_CH_SPMV");
+      return e ? atoll(e) : 0;
+    }();
+    if (ch_spmv >= 32 && (a.op == Op::SpMV || a.op == Op::SpTTV)) g.CH = ch_spmv;
   }
   const bool spmm32 = a.op == Op::SpMM && a.W == 32 && B->dims[1] < (int64_t(1) << 31);
   const int64_t W = a.W > 0 ? a.W : 1;
@@ -1103,6 +1124,10 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
       if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, 0>);
       k_spmm32_nz<4, 4, 0><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
                                                        col.counters);
+    } else if (spmv_rows_mode(nnz, z.m)) {  // short rows: a lane per row
+      static int grid = 0;
+      if (!grid) grid = occupancy_grid(ctx, k_spmv_rows);
+      k_spmv_rows<<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
     } else {
       static int grid = 0;
       if (!grid) grid = occupancy_grid(ctx, k_spmv_nz);
