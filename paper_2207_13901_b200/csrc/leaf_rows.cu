@@ -1027,6 +1027,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   const bool use_nz = nz_enabled() && (a.op == Op::SpMV || a.op == Op::SpTTV || mttkrp32 ||
                                        spmm32);
   NzView z{nullptr, nullptr, 0};
+  bool zero_joined = false;
   if (use_nz) {
     z = nz_view(ctx, const_cast<spd_tensor*>(B), g.R, g.nrows);
     ht.mark("nz_view");
@@ -1035,9 +1036,26 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
     if (a.op == Op::SpMM || a.op == Op::SpMTTKRP) {
       static int zgrid = 0;
       if (!zgrid) zgrid = occupancy_grid(ctx, k_zero_empty);
+      // zero-fill CTAs on the aux stream, concurrent with the leaf (its
+      // late-starting CTAs just draw the remaining chunk tickets): 4 per SM
+      // measured best (step 6.05 -> 5.95 ms, profiles/README.md);
+      // SPD_ZCONC=0 runs the pass before the leaf instead.
+      static int zconc = [ctx] {
+        const char* e = getenv("SPD_ZCONC");
+        return e ? atoi(e) : 4 * ctx->num_sms;
+      }();
       trace_mark(ctx);
-      k_zero_empty<<<zgrid, kBlock, 0, s>>>(g.R, g.nrows, (const DevColor*)ctx->colors_dev.ptr, first, count,
-                                           a.W, a.out);
+      if (zconc > 0 && ctx->aux) {
+        SPD_CUDA(cudaEventRecord(ctx->fork, s));
+        SPD_CUDA(cudaStreamWaitEvent(ctx->aux, ctx->fork, 0));
+        k_zero_empty<<<zconc, kBlock, 0, ctx->aux>>>(g.R, g.nrows, (const DevColor*)ctx->colors_dev.ptr, first,
+                                                    count, a.W, a.out);
+        SPD_CUDA(cudaEventRecord(ctx->join, ctx->aux));
+        zero_joined = true;
+      } else {
+        k_zero_empty<<<zgrid, kBlock, 0, s>>>(g.R, g.nrows, (const DevColor*)ctx->colors_dev.ptr, first, count,
+                                             a.W, a.out);
+      }
       SPD_CHECK_LAUNCH();
       launches++;
     }
@@ -1186,6 +1204,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   SPD_CHECK_LAUNCH();
   ht.mark("leaf launch");
   leaf_timing_end(ctx);
+  if (zero_joined) SPD_CUDA(cudaStreamWaitEvent(s, ctx->join, 0));
   trace_mark(ctx);
   launches++;
   {
