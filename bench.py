@@ -445,7 +445,7 @@ def main():
                        "input_gen_s": round(t_gen, 1)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "k_spmm32_nz<4,4,false,true> (dynamic chunk tickets; + k_zero_empty for the empty rows)", "peak_source": peak_src,
+                         "kernel": "k_spmm32_nz<4,4,0,1> (dynamic chunk tickets; k_zero_empty for the empty rows runs concurrently on the aux stream, inside the timed leaf window)", "peak_source": peak_src,
                          "bytes_per_launch": per_launch, "leaf_ms": leaf_avg,
                          "frac_vs_8tbs_nominal": (achieved / 8000.0) if achieved else None},
             "phases_ms_max_over_ranks": phases,
@@ -458,7 +458,7 @@ def main():
                      "roofline": {"bound": "hbm", "achieved": (spmv_bytes / world) / (leaf_v * 1e-3) / 1e9 if leaf_v else None,
                                   "peak": peak, "unit": "GB/s",
                                   "frac": (spmv_bytes / world) / (leaf_v * 1e-3) / 1e9 / peak if leaf_v else None,
-                                  "kernel": "k_spmv_nz", "leaf_ms": leaf_v}},
+                                  "kernel": "k_spmv_rows", "leaf_ms": leaf_v}},
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
