@@ -541,6 +541,176 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
 }
 
 // ---------------------------------------------------------------------------
+// SpMM for N in {8, 16, 64, 128}: k_spmm32_nz generalised.  LP = min(N/2, 32)
+// lanes gather one position's C row with 128-bit loads (VPL = N/64 of them
+// per lane when N = 128), so a warp instruction covers PPI = 32/LP positions
+// (8 at N = 8, 4 at N = 16, 1 at N >= 64).  Positions go in fixed-trip
+// groups of PPI*UNR; a group without a row start adds every product; a group
+// with one walks its PPI sub-positions in order (runtime loop, to keep the
+// code small), flushing the finished row -- the sub-lane partials summed by
+// an xor butterfly over the sub index -- at each start.  Chunk tickets,
+// records and ownership as k_spmm32_nz.
+template <int N, int UNR, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_spmm_nzv(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
+                                                     const double* __restrict__ vals,
+                                                     const double* __restrict__ C, double* __restrict__ A,
+                                                     ChunkRecs rec, const int64_t* __restrict__ counters) {
+  constexpr int LP = N / 2 < 32 ? N / 2 : 32;  // lanes per position
+  constexpr int VPL = N / 64 > 1 ? N / 64 : 1;  // double2 per lane
+  constexpr int PPI = 32 / LP;                 // positions per warp instruction
+  constexpr int GP = PPI * UNR;                // positions per group
+  static_assert(GP <= 32, "a group must fit one 32-position window");
+  const int lane = lane_id();
+  const int sub = lane / LP, sl = lane % LP;
+  const int64_t begin = counters[1], end = counters[2];
+  const uint64_t pol_keep = l2_policy_evict_last();
+  const uint64_t pol_stream = l2_policy_evict_first();
+  const double* Cl = C + 2 * sl;
+  const int64_t tmax = end - begin;
+  for (int64_t t = chunk_ticket(counters); t < tmax; t = chunk_ticket(counters)) {
+    const int64_t v = begin + t;
+    const ChunkInfo ci = chunk_info(g, v, begin);
+    if (ci.q_lo > ci.q_hi) {
+      if (lane == 0) rec.row[2 * ci.local] = -1, rec.row[2 * ci.local + 1] = -1, rec.cont[ci.local] = 0;
+      continue;
+    }
+    const int64_t k = ci.local, s = ci.s, e = ci.e;
+    NzCursor c;
+    nz_start(z, c, s);
+    bool head = __shfl_sync(FULL, c.P0, 0) < s;
+    int64_t head_row = -1;
+    int head_cont = 0;
+    double2 acc[VPL];
+#pragma unroll
+    for (int w = 0; w < VPL; w++) acc[w] = make_double2(0.0, 0.0);
+    // finished row: sum the sub-lane partials, store (or record) it, reset
+    auto flush = [&](double* dst_row_base, bool to_record, double* rec_base) {
+      double2 o[VPL];
+#pragma unroll
+      for (int w = 0; w < VPL; w++) {
+        o[w] = acc[w];
+#pragma unroll
+        for (int m = LP; m < 32; m <<= 1) {
+          o[w].x += __shfl_xor_sync(FULL, o[w].x, m);
+          o[w].y += __shfl_xor_sync(FULL, o[w].y, m);
+        }
+      }
+      if (sub == 0) {
+#pragma unroll
+        for (int w = 0; w < VPL; w++) {
+          if (to_record)
+            reinterpret_cast<double2*>(rec_base)[sl + w * 32] = o[w];
+          else
+            st_f64x2_hint(dst_row_base + 2 * sl + w * 64, o[w], pol_stream);
+        }
+      }
+#pragma unroll
+      for (int w = 0; w < VPL; w++) acc[w] = make_double2(0.0, 0.0);
+    };
+    int kn = 0;
+    double vn = 0.0;
+    if (lane <= e - s) {
+      kn = (int)ld_i64_hint(crd + s + lane, pol_stream);
+      vn = ld_f64_hint(vals + s + lane, pol_stream);
+    }
+    for (int64_t base = s; base <= e; base += 32) {
+      const int last_off = (int)min((int64_t)31, e - base);
+      const int cnt = last_off + 1;
+      const int my_k = kn;
+      const double my_v = vn;
+      if (base + 32 + lane <= e) {
+        kn = (int)ld_i64_hint(crd + base + 32 + lane, pol_stream);
+        vn = ld_f64_hint(vals + base + 32 + lane, pol_stream);
+      }
+      const unsigned bm = nz_window_mask(c, base, base + last_off);
+#pragma unroll 1
+      for (int u = 0; u < 32; u += GP) {
+        if (u >= cnt) break;
+        double2 cv[UNR][VPL];
+        double bv[UNR];
+#pragma unroll
+        for (int i = 0; i < UNR; i++) {
+          const int p = u + PPI * i + sub;
+          const int kk = __shfl_sync(FULL, my_k, p & 31);
+          bv[i] = __shfl_sync(FULL, my_v, p & 31);
+          const double* src = Cl + (int64_t)kk * N;
+#pragma unroll
+          for (int w = 0; w < VPL; w++)
+            cv[i][w] = p < cnt ? ld_f64x2_hint(src + w * 64, pol_keep) : make_double2(0.0, 0.0);
+        }
+        const unsigned gm = GP == 32 ? (bm >> u) : ((bm >> u) & ((1u << GP) - 1u));
+        if (gm == 0u) {
+#pragma unroll
+          for (int i = 0; i < UNR; i++)
+#pragma unroll
+            for (int w = 0; w < VPL; w++) {
+              acc[w].x = fma(bv[i], cv[i][w].x, acc[w].x);
+              acc[w].y = fma(bv[i], cv[i][w].y, acc[w].y);
+            }
+        } else {
+#pragma unroll
+          for (int i = 0; i < UNR; i++) {
+            const unsigned bits = (gm >> (PPI * i)) & ((1u << PPI) - 1u);
+            if (bits == 0u) {
+#pragma unroll
+              for (int w = 0; w < VPL; w++) {
+                acc[w].x = fma(bv[i], cv[i][w].x, acc[w].x);
+                acc[w].y = fma(bv[i], cv[i][w].y, acc[w].y);
+              }
+              continue;
+            }
+#pragma unroll 1
+            for (int h = 0; h < PPI; h++) {
+              if ((bits >> h) & 1u) {  // a new row starts at position u + PPI*i + h
+                const int64_t id = nz_get(c.I0, c.I1, (int)(c.ic - c.cb));
+                if (head) {
+                  flush(nullptr, true, rec.val + 2 * k * N);
+                  head_row = id;
+                  head_cont = 0;
+                  head = false;
+                } else {
+                  flush(A + id * N, false, nullptr);
+                }
+                nz_advance(z, c, 1);
+              }
+              if (sub == h) {
+#pragma unroll
+                for (int w = 0; w < VPL; w++) {
+                  acc[w].x = fma(bv[i], cv[i][w].x, acc[w].x);
+                  acc[w].y = fma(bv[i], cv[i][w].y, acc[w].y);
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+    const int64_t next = nz_get(c.P0, c.P1, (int)(c.ic - c.cb) + 1);
+    const int64_t id = nz_get(c.I0, c.I1, (int)(c.ic - c.cb));
+    int64_t tail_row = -1;
+    if (next == e + 1) {
+      if (head) {
+        flush(nullptr, true, rec.val + 2 * k * N);
+        head_row = id, head_cont = 0;
+      } else {
+        flush(A + id * N, false, nullptr);
+      }
+    } else if (head) {
+      flush(nullptr, true, rec.val + 2 * k * N);
+      head_row = id, head_cont = 1;
+    } else {
+      flush(nullptr, true, rec.val + (2 * k + 1) * N);
+      tail_row = id;
+    }
+    if (lane == 0) {
+      rec.row[2 * k] = head_row;
+      rec.row[2 * k + 1] = tail_row;
+      rec.cont[k] = head_cont;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // SpMTTKRP, R == 32, over the compacted rows i (leaf row pointer): the
 // k_spmm32_nz walk with two gathers per position -- D(k,:) by the leaf crd and
 // C(j,:) by the position's fibre coordinate (jleaf, a per-leaf copy of crd1

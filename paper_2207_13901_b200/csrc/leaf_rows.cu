@@ -855,6 +855,16 @@ static bool dyn_enabled() {
   return v != 0;
 }
 
+// The compacted-row SpMM for N in {8, 16, 64, 128} (k_spmm_nzv);
+// SPD_SPMMV=0 selects the lane-per-column walks instead.
+static bool spmmv_enabled() {
+  static int v = [] {
+    const char* e = getenv("SPD_SPMMV");
+    return e ? atoi(e) : 1;
+  }();
+  return v != 0;
+}
+
 static int hot_enabled() {
   static int v = [] {
     const char* e = getenv("SPD_HOT");
@@ -994,6 +1004,8 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
     if (ch_spmv >= 32 && (a.op == Op::SpMV || a.op == Op::SpTTV)) g.CH = ch_spmv;
   }
   const bool spmm32 = a.op == Op::SpMM && a.W == 32 && B->dims[1] < (int64_t(1) << 31);
+  const bool spmmv = a.op == Op::SpMM && (a.W == 8 || a.W == 16 || a.W == 64 || a.W == 128) &&
+                     B->dims[1] < (int64_t(1) << 31) && spmmv_enabled();
   const int64_t W = a.W > 0 ? a.W : 1;
   const int64_t max_chunks = nnz / g.CH + 2 * P + 2;
 
@@ -1025,7 +1037,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   const bool mttkrp32 = a.op == Op::SpMTTKRP && a.W == 32 && B->dims[1] < (int64_t(1) << 31) &&
                         B->dims[2] < (int64_t(1) << 31);
   const bool use_nz = nz_enabled() && (a.op == Op::SpMV || a.op == Op::SpTTV || mttkrp32 ||
-                                       spmm32);
+                                       spmm32 || spmmv);
   NzView z{nullptr, nullptr, 0};
   bool zero_joined = false;
   if (use_nz) {
@@ -1079,6 +1091,21 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
       if (!grid) grid = occupancy_grid(ctx, k_mttkrp32_nz<4, 3, false>);
       k_mttkrp32_nz<4, 3, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->jleaf, a.x, B->vals, a.D, a.out, rec,
                                                          col.counters);
+    } else if (spmmv) {  // N in {8, 16, 64, 128}
+      switch (a.W) {
+#define SPD_SPMMV(NN, UU, MB)                                                                        \
+  case NN: {                                                                                         \
+    static int grid = 0;                                                                             \
+    if (!grid) grid = occupancy_grid(ctx, k_spmm_nzv<NN, UU, MB>);                                  \
+    k_spmm_nzv<NN, UU, MB><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters); \
+    break;                                                                                           \
+  }
+        SPD_SPMMV(8, 4, 4)
+        SPD_SPMMV(16, 4, 4)
+        SPD_SPMMV(64, 4, 4)
+        SPD_SPMMV(128, 2, 4)
+#undef SPD_SPMMV
+      }
     } else if (a.op == Op::SpMM && hot_enabled() == 2) {
       // hot-copy leaf: gather the hot rows of C into a compact buffer that
       // an L2 access-policy window keeps persisting across the leaf

@@ -142,7 +142,8 @@ def test_empty_and_degenerate(ctx, pieces):
     assert st.combines == want["combines"] and st.work == want["work"]
 
 
-@pytest.mark.parametrize("kernel,N", [("spmv", 1), ("spmm", 8), ("spmm", 32)])
+@pytest.mark.parametrize("kernel,N", [("spmv", 1), ("spmm", 8), ("spmm", 16), ("spmm", 32), ("spmm", 64),
+                                      ("spmm", 128)])
 def test_long_hub_rows_cross_many_chunks(ctx, kernel, N):
     """Rows far longer than a warp chunk exercise the carry chains."""
     from paper_2207_13901_b200.execute import execute
@@ -355,3 +356,25 @@ def test_sss_csf_matches_reference(ctx, kernel, schedule, pieces):
         else:
             assert np.all(np.abs(got - want) <= 1e-10 * np.maximum(np.abs(want), 1e-300))
         assert st.work == st_ref["work"] and st.combines == st_ref["combines"]
+
+
+@pytest.mark.parametrize("N", [8, 16, 64, 128])
+@pytest.mark.parametrize("schedule,pieces", [("nonzero", 1), ("nonzero", 3), ("nonzero", 8), ("row", 4)])
+def test_spmm_widths_match_restatement(ctx, N, schedule, pieces):
+    """The compacted-row SpMM for N in {8, 16, 64, 128} (k_spmm_nzv): power-law
+    rows (empty rows, short rows, a hub) against the oracle."""
+    from paper_2207_13901_b200.execute import execute
+    from paper_2207_13901_b200.host import SparseTensor, parse_format
+
+    rng = np.random.default_rng(N * 10 + pieces)
+    n, m = 900, 700
+    rows = np.concatenate([np.full(3000, 5), (rng.pareto(1.2, 20000) * 20).astype(np.int64) % n])
+    cols = rng.integers(0, m, rows.shape[0])
+    for integers in (True, False):
+        vals = rng.integers(1, 5, rows.shape[0]).astype(float) if integers else rng.uniform(0.5, 1.5, rows.shape[0])
+        B = SparseTensor.pack((n, m), parse_format("ds"), np.stack([rows, cols], 1), vals)
+        t = {"B": B, "C": K.dense(rng, (m, N), "dd", integers)}
+        want = oracle_execute("spmm", t, schedule, pieces)
+        out, st, _ = execute("spmm", t, schedule, pieces, ctx)
+        assert_close("spmm", out, want["out"], integers)
+        assert st.work == want["work"] and st.combines == want["combines"]
