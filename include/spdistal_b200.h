@@ -133,6 +133,17 @@ int spd_tensor_upload(spd_context* ctx, int order, const int64_t* dims, const in
  * position count that differs returns SPD_ERR_VALIDATION. */
 int spd_tensor_restage(spd_context* ctx, spd_tensor* t, const int64_t* const* pos_pairs,
                        const int64_t* const* crd, const double* vals);
+/* The reference's communication ledger for a CSR-like tensor (transfer_bytes,
+ * sim.cpp:134-147, over residency_from_placements :547-566; 16 B per pos
+ * range, 8 B per crd, 8 B per val, sim.hpp:21-23): bytes_out[w] for worker w
+ * of `pieces` = the bytes of colour w of the compute partition (need_split:
+ * 1 row split, 2 nonzero split)
+ * that colour w of the placement (held_split: 1 rows "B(x,y) onto M(x)",
+ * 2 nonzeros "... fuse(x,y->f) onto M(~f)", 3 replicated) does not hold.
+ * A matched placement (need == held) charges 0.  Leaves the
+ * compute partition on ctx. */
+int spd_ledger_bytes(spd_context* ctx, const spd_tensor* t, int need_split, int held_split,
+                     int64_t pieces, int64_t* bytes_out);
 /* This GPU's piece of a CSR-like ("ds") matrix staged from host arrays: the
  * whole pos level (pairs, O(rows)) is uploaded, converted and checked, the
  * compute partition (split 1 = rows, 2 = nonzeros; spd_partition_universe /

@@ -724,6 +724,48 @@ static NzView nz_view(spd_context* ctx, spd_tensor* t, const int64_t* R, int64_t
   return NzView{slot->ptr, slot->id, slot->m};
 }
 
+// Non-empty rows of row pointer R (of t) inside each span [lo, hi]: two
+// binary searches over the compacted view's sorted row ids.
+__global__ void k_nonempty_in_spans(const int64_t* __restrict__ ids, int64_t m, const int64_t* __restrict__ spans,
+                                    int64_t nspans, int64_t* __restrict__ out) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nspans; j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lo = spans[2 * j], hi = spans[2 * j + 1];
+    if (lo > hi) {
+      out[j] = 0;
+      continue;
+    }
+    int64_t a = 0, b = m;  // first id >= lo
+    while (a < b) {
+      const int64_t mid = (a + b) >> 1;
+      if (ids[mid] < lo) a = mid + 1; else b = mid;
+    }
+    int64_t c = a, d = m;  // first id > hi
+    while (c < d) {
+      const int64_t mid = (c + d) >> 1;
+      if (ids[mid] <= hi) c = mid + 1; else d = mid;
+    }
+    out[j] = c - a;
+  }
+}
+
+std::vector<int64_t> nonempty_in_spans(spd_context* ctx, spd_tensor* t, const int64_t* R, int64_t nrows,
+                                       const std::vector<int64_t>& spans) {
+  const NzView z = nz_view(ctx, t, R, nrows);
+  const int64_t ns = (int64_t)spans.size() / 2;
+  std::vector<int64_t> out(ns, 0);
+  if (ns == 0) return out;
+  cudaStream_t s = ctx->stream;
+  int64_t* d = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * 3 * ns);
+  SPD_CUDA(cudaMemcpyAsync(d, spans.data(), sizeof(int64_t) * 2 * ns, cudaMemcpyHostToDevice, s));
+  k_nonempty_in_spans<<<(unsigned)std::min<int64_t>(ceil_div(ns, 256), 1024), 256, 0, s>>>(z.id, z.m, d, ns,
+                                                                                             d + 2 * ns);
+  SPD_CHECK_LAUNCH();
+  SPD_CUDA(cudaMemcpyAsync(out.data(), d + 2 * ns, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost, s));
+  SPD_CUDA(cudaStreamSynchronize(s));
+  dev_free(ctx, d);
+  return out;
+}
+
 // int32 leaf crd with hot-column bit for dense rows of `rowbytes` (cached on
 // t): the most referenced columns whose rows fit in ~70% of L2 are hot and
 // gathered with L2 evict_last, the rest with evict_first -- an LFU-like L2

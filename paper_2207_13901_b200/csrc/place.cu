@@ -12,7 +12,14 @@
 // tensor whose leaf arrays are indexed by global position, so the leaf ops
 // run on it unchanged for that colour.  The bytes each GPU received are
 // returned (the placement's cost, reported apart from compute).
+#include <algorithm>
+
 #include "common.cuh"
+
+namespace spd {
+std::vector<int64_t> nonempty_in_spans(spd_context* ctx, spd_tensor* t, const int64_t* R, int64_t nrows,
+                                       const std::vector<int64_t>& spans);
+}
 
 namespace spd {
 
@@ -113,11 +120,92 @@ void run_place(spd_context* ctx, int root, const spd_tensor* whole, int split, s
   *out = t;
 }
 
+// The reference's communication ledger for one CSR-like tensor
+// (transfer_bytes sim.cpp:134-147 over worker_needed_sets :505-516 and
+// residency_from_placements :547-566; units sim.hpp:21-23): worker w needs
+// colour w of the compute partition (need_split 1 rows / 2 nonzeros -- the
+// communicate site of a distributed loop, which the planner places there by
+// default) and holds colour w of its placement
+// (held_split 1 rows / 2 nonzeros; 3 = replicated).  Per level-1 region the
+// sets are contiguous spans: crd / vals = q; pos = every row of `par` for a
+// row split (partition_from_parent copies the row block) or only its
+// non-empty rows for a nonzero split (preimage, deppart.cpp:46).
+struct PosSet {
+  int64_t lo = 0, hi = -1;
+  bool nonempty_only = false;
+};
+
+void run_ledger(spd_context* ctx, const spd_tensor* t, int need_split, int held_split, int64_t pieces,
+                int64_t* bytes_out) {
+  checked(ctx);
+  if (!t || !bytes_out) throw ValidationError("null argument");
+  if (t->levels.size() != 2 || t->levels[0].kind != SPD_DENSE || t->levels[1].kind != SPD_COMPRESSED)
+    throw ValidationError("unsupported on gpu: the ledger covers ds (CSR-like) tensors");
+  if (need_split < 1 || need_split > 2) throw ValidationError("need_split must be 1 or 2");
+  if (held_split < 1 || held_split > 3) throw ValidationError("held_split must be 1, 2 or 3");
+  if (pieces < 1) throw ValidationError("pieces must be positive");
+  activate(ctx);
+  spd_tensor* tm = const_cast<spd_tensor*>(t);
+  const int64_t n = t->levels[1].parent_positions, nnz = t->levels[1].positions;
+  auto colours = [&](int split) {
+    const int rc = split == 1 ? spd_partition_universe(ctx, tm, pieces, nullptr)
+                              : spd_partition_nonzero(ctx, tm, 1, pieces, nullptr);
+    if (rc != SPD_OK) throw ValidationError(spd_last_error());
+    return host_colors(ctx);
+  };
+  std::vector<spd_color> held, need;
+  if (held_split != 3) held = colours(held_split);
+  need = colours(need_split);  // leaves the compute partition on ctx
+  auto pos_of = [&](const std::vector<spd_color>& cs, int split, int64_t w) {
+    PosSet p;
+    if (cs.empty()) {  // full / replicated: every pos entry
+      p.lo = 0, p.hi = n - 1;
+      return p;
+    }
+    const spd_color& c = cs[w];
+    if (split == 1) {
+      p.lo = c.par.lo, p.hi = c.par.hi;
+    } else if (c.q.lo <= c.q.hi) {
+      p.lo = c.par.lo, p.hi = c.par.hi, p.nonempty_only = true;
+    }
+    return p;
+  };
+  auto crd_of = [&](const std::vector<spd_color>& cs, int64_t w) {
+    return cs.empty() ? spd_range{0, nnz - 1} : cs[w].q;
+  };
+  // spans whose non-empty rows are counted on the device: per worker
+  // |needed pos| and |needed pos & held pos|
+  std::vector<int64_t> spans;
+  std::vector<int64_t> need_all(pieces), both_all(pieces);
+  for (int64_t w = 0; w < pieces; w++) {
+    const PosSet N = pos_of(need, need_split, w), H = pos_of(held, held_split, w);
+    const int64_t lo = std::max(N.lo, H.lo), hi = std::min(N.hi, H.hi);
+    need_all[w] = N.nonempty_only ? -1 : std::max<int64_t>(N.hi - N.lo + 1, 0);
+    both_all[w] = (N.nonempty_only || H.nonempty_only) ? -1 : std::max<int64_t>(hi - lo + 1, 0);
+    spans.insert(spans.end(), {N.lo, N.hi, lo, hi});
+  }
+  const std::vector<int64_t> ne = nonempty_in_spans(ctx, tm, t->levels[1].rowptr, n, spans);
+  for (int64_t w = 0; w < pieces; w++) {
+    const int64_t npos = need_all[w] >= 0 ? need_all[w] : ne[2 * w];
+    const int64_t both = both_all[w] >= 0 ? both_all[w] : ne[2 * w + 1];
+    const spd_range nc = crd_of(need, w), hc = crd_of(held, w);
+    const int64_t ncount = std::max<int64_t>(nc.hi - nc.lo + 1, 0);
+    const int64_t ov = std::max<int64_t>(std::min(nc.hi, hc.hi) - std::max(nc.lo, hc.lo) + 1, 0);
+    const int64_t missing_pos = npos - both, missing_crd = ncount - ov;
+    bytes_out[w] = 16 * missing_pos + 8 * missing_crd + 8 * missing_crd;  // pos ranges, crd, vals
+  }
+}
+
 }  // namespace
 
 }  // namespace spd
 
 using namespace spd;
+
+extern "C" int spd_ledger_bytes(spd_context* ctx, const spd_tensor* t, int need_split, int held_split,
+                                int64_t pieces, int64_t* bytes_out) {
+  return guarded([&] { run_ledger(ctx, t, need_split, held_split, pieces, bytes_out); });
+}
 
 extern "C" int spd_tensor_place(spd_context* ctx, int root, const spd_tensor* whole, int split,
                                 spd_tensor** piece, int64_t* bytes_in) {

@@ -736,6 +736,18 @@ def spmm(ctx, B: DeviceTensor, Cd, n_cols, A, first=0, count=None, pieces=None, 
     return _stats(ctx, st, pieces) if stats else None
 
 
+SPLITS = {"row": 1, "nonzero": 2, "replicated": 3}
+
+
+def ledger_bytes(ctx, B: DeviceTensor, need: str, held: str, pieces: int):
+    """spd_ledger_bytes: per-worker bytes_by_tensor of B (transfer_bytes,
+    sim.cpp:134-147) for compute split `need` ("row" | "nonzero") against
+    placement `held` ("row" | "nonzero" | "replicated")."""
+    out = (C.c_int64 * pieces)()
+    check(N.lib().spd_ledger_bytes(ctx.h, B.h, SPLITS[need], SPLITS[held], pieces, out))
+    return list(out)
+
+
 def divide_bounds(n: int, pieces: int):
     """divide_bounds (planner.cpp:10-20): block = n / pieces (truncating);
     colour c < pieces-1 -> [c*block, c*block+block-1], the last -> [.., n-1]."""

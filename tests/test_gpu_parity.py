@@ -378,3 +378,51 @@ def test_spmm_widths_match_restatement(ctx, N, schedule, pieces):
         out, st, _ = execute("spmm", t, schedule, pieces, ctx)
         assert_close("spmm", out, want["out"], integers)
         assert st.work == want["work"] and st.combines == want["combines"]
+
+
+LEDGER_SCHED = {
+    "row": "divide(i, io, ii, M.x); distribute(io, M.x); communicate({a, B, c}, io)",
+    "nonzero": "fuse(i, j, f); divide(f, fo, fi, B.pos, M.x); distribute(fo, M.x); communicate({a, B, c}, fo)",
+}
+LEDGER_TDN = {
+    "row": "B(x, y) onto M(x)",
+    "nonzero": "B(x, y) fuse(x, y -> f) onto M(~f)",
+    "replicated": "B(x, y) onto M(z)",
+}
+
+
+@pytest.mark.parametrize("need", ["row", "nonzero"])
+@pytest.mark.parametrize("held", ["row", "nonzero", "replicated"])
+@pytest.mark.parametrize("pieces", [1, 2, 3, 5])
+def test_ledger_bytes_match_reference(ctx, need, held, pieces):
+    """bytes_by_tensor['B'] of the reference's execute with TDN placements
+    (use_placements) equals spd_ledger_bytes, on power-law matrices with
+    empty rows; matched placements charge 0."""
+    import json
+
+    import oracle_bind as ob
+    from paper_2207_13901_b200 import host as H
+    from paper_2207_13901_b200.host import SparseTensor, parse_format
+
+    rng = np.random.default_rng(pieces * 31 + len(need) * 7 + len(held))
+    for _ in range(3):
+        n, m = int(rng.integers(5, 60)), int(rng.integers(5, 40))
+        cnt = int(rng.integers(1, 3 * n))
+        rows = (rng.pareto(1.0, cnt) * 3).astype(np.int64) % n
+        cols = rng.integers(0, m, cnt)
+        B = SparseTensor.pack((n, m), parse_format("ds"), np.stack([rows, cols], 1),
+                              rng.integers(1, 5, cnt).astype(float))
+        c = K.dense(rng, (m,), "d")
+        run = ob.RefRun("a(i) = B(i, j) * c(j)", LEDGER_SCHED[need], pieces, "d",
+                        {"B": (B, "ds", LEDGER_TDN[held]), "c": (c, "d", "c(x) onto M(z)")},
+                        use_placements=True).ok()
+        st = json.loads(run.L.ref_stats_json(run.h).decode())
+        want = [w["bytes_by_tensor"]["B"] for w in st["per_worker"]]
+        dev = H.DeviceTensor.upload(ctx, B)
+        try:
+            got = H.ledger_bytes(ctx, dev, need, held, pieces)
+        finally:
+            dev.close()
+        assert got == want, (need, held, pieces, got, want)
+        if need == held:
+            assert got == [0] * pieces
