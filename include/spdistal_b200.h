@@ -133,6 +133,15 @@ int spd_tensor_upload(spd_context* ctx, int order, const int64_t* dims, const in
  * position count that differs returns SPD_ERR_VALIDATION. */
 int spd_tensor_restage(spd_context* ctx, spd_tensor* t, const int64_t* const* pos_pairs,
                        const int64_t* const* crd, const double* vals);
+/* Mismatched placement: moves a piece (spd_tensor_place /
+ * spd_tensor_upload_piece, split 1 rows or 2 nonzeros) to colour `rank` of
+ * the compute partition need_split -- the data the reference's ledger
+ * charges (spd_ledger_bytes).  Every GPU derives every GPU's held and needed
+ * leaf position spans from the row pointer it holds; the overlaps travel as
+ * grouped NCCL send/recv of crd and vals.  Collective over the communicator.
+ * *bytes_in = crd + vals bytes this GPU received. */
+int spd_tensor_repartition(spd_context* ctx, const spd_tensor* piece, int need_split,
+                           spd_tensor** out, int64_t* bytes_in);
 /* The reference's communication ledger for a CSR-like tensor (transfer_bytes,
  * sim.cpp:134-147, over residency_from_placements :547-566; 16 B per pos
  * range, 8 B per crd, 8 B per val, sim.hpp:21-23): bytes_out[w] for worker w

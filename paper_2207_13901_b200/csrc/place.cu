@@ -76,6 +76,7 @@ void run_place(spd_context* ctx, int root, const spd_tensor* whole, int split, s
     SPD_NCCL(ncclBroadcast(L.rowptr, L.rowptr, nrows + 1, ncclInt64, root, ctx->comm, s));
     t->nvals = nnz;
     t->piece = true;
+    t->piece_split = split;
     set_whole_span(t);
     // the compute partition, the same on every GPU (one colour per GPU)
     const int rc = split == 1 ? spd_partition_universe(ctx, t, ctx->world, nullptr)
@@ -118,6 +119,103 @@ void run_place(spd_context* ctx, int root, const spd_tensor* whole, int split, s
     throw;
   }
   *out = t;
+}
+
+// Moves a piece to another compute partition: every GPU computes, from the
+// whole row pointer it holds, every GPU's held range (the piece's own split)
+// and needed range (need_split) -- contiguous leaf position spans -- and the
+// overlaps travel as grouped NCCL send/recv of crd and vals; the local
+// overlap is a device copy.  The result is a new piece for colour `rank` of
+// need_split; *bytes_in = crd + vals bytes received over NCCL.
+void run_repartition(spd_context* ctx, const spd_tensor* t, int need_split, spd_tensor** out, int64_t* bytes_in) {
+  checked(ctx);
+  if (!t || !out) throw ValidationError("null argument");
+  if (!ctx->comm) throw ValidationError("spd_tensor_repartition needs a communicator");
+  if (!t->piece || (t->piece_split != 1 && t->piece_split != 2))
+    throw ValidationError("spd_tensor_repartition moves a piece (spd_tensor_place / spd_tensor_upload_piece)");
+  if (need_split != 1 && need_split != 2) throw ValidationError("need_split must be 1 (rows) or 2 (nonzeros)");
+  activate(ctx);
+  cudaStream_t s = ctx->stream;
+  spd_tensor* tm = const_cast<spd_tensor*>(t);
+  const int W = ctx->world;
+  auto colours = [&](int split) {
+    const int rc = split == 1 ? spd_partition_universe(ctx, tm, W, nullptr)
+                              : spd_partition_nonzero(ctx, tm, 1, W, nullptr);
+    if (rc != SPD_OK) throw ValidationError(spd_last_error());
+    std::vector<spd_range> q;
+    for (const auto& c : host_colors(ctx)) q.push_back(c.q);
+    return q;
+  };
+  const std::vector<spd_range> held = colours(t->piece_split);
+  const std::vector<spd_range> need = colours(need_split);
+  const int me = ctx->rank;
+  if (held[me].lo != t->piece_lo || (held[me].lo <= held[me].hi && held[me].hi != t->piece_hi))
+    throw ValidationError("spd_tensor_repartition: the piece does not hold its split's colour");
+  const spd_level_store& L = t->levels[1];
+  const int64_t nrows = L.parent_positions, nnz = L.positions;
+  const int64_t dims[2] = {t->dims[0], t->dims[1]};
+  const int kinds[2] = {SPD_DENSE, SPD_COMPRESSED};
+  const int mo[2] = {t->mode_order[0], t->mode_order[1]};
+  spd_tensor* r = make_skeleton(ctx, 2, dims, kinds, mo);
+  try {
+    r->levels[0].kind = SPD_DENSE;
+    r->levels[0].dom = {nrows};
+    r->levels[0].positions = nrows;
+    spd_level_store& R = r->levels[1];
+    R.kind = SPD_COMPRESSED;
+    R.parent_positions = nrows;
+    R.positions = nnz;
+    R.rowptr = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (nrows + 1));
+    SPD_CUDA(cudaMemcpyAsync(R.rowptr, L.rowptr, sizeof(int64_t) * (nrows + 1), cudaMemcpyDeviceToDevice, s));
+    r->nvals = nnz;
+    r->piece = true;
+    r->piece_split = need_split;
+    set_whole_span(r);
+    const spd_range mine = need[me];
+    const int64_t cnt = std::max<int64_t>(mine.hi - mine.lo + 1, 0);
+    r->piece_lo = mine.lo;
+    r->piece_hi = mine.hi;
+    r->piece_cap = std::max<int64_t>(cnt, 1);
+    r->piece_crd = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * r->piece_cap);
+    r->piece_vals = (double*)dev_alloc(ctx, sizeof(double) * r->piece_cap);
+    R.crd = r->piece_crd - mine.lo;
+    r->vals = r->piece_vals - mine.lo;
+    auto overlap = [](spd_range a, spd_range b) {
+      return spd_range{std::max(a.lo, b.lo), std::min(a.hi, b.hi)};
+    };
+    int64_t received = 0;
+    const spd_range local = overlap(held[me], mine);
+    if (local.lo <= local.hi) {
+      const int64_t c = local.hi - local.lo + 1;
+      SPD_CUDA(cudaMemcpyAsync(R.crd + local.lo, L.crd + local.lo, sizeof(int64_t) * c, cudaMemcpyDeviceToDevice, s));
+      SPD_CUDA(cudaMemcpyAsync(r->vals + local.lo, t->vals + local.lo, sizeof(double) * c, cudaMemcpyDeviceToDevice,
+                               s));
+    }
+    SPD_NCCL(ncclGroupStart());
+    for (int p = 0; p < W; p++) {
+      if (p == me) continue;
+      const spd_range snd = overlap(held[me], need[p]);  // what p needs from my piece
+      if (snd.lo <= snd.hi) {
+        const int64_t c = snd.hi - snd.lo + 1;
+        SPD_NCCL(ncclSend(L.crd + snd.lo, c, ncclInt64, p, ctx->comm, s));
+        SPD_NCCL(ncclSend(t->vals + snd.lo, c, ncclFloat64, p, ctx->comm, s));
+      }
+      const spd_range rcv = overlap(held[p], mine);  // what I need from p's piece
+      if (rcv.lo <= rcv.hi) {
+        const int64_t c = rcv.hi - rcv.lo + 1;
+        SPD_NCCL(ncclRecv(R.crd + rcv.lo, c, ncclInt64, p, ctx->comm, s));
+        SPD_NCCL(ncclRecv(r->vals + rcv.lo, c, ncclFloat64, p, ctx->comm, s));
+        received += 16 * c;
+      }
+    }
+    SPD_NCCL(ncclGroupEnd());
+    SPD_CUDA(cudaStreamSynchronize(s));
+    if (bytes_in) *bytes_in = received;
+  } catch (...) {
+    spd_tensor_destroy(r);
+    throw;
+  }
+  *out = r;
 }
 
 // The reference's communication ledger for one CSR-like tensor
@@ -201,6 +299,11 @@ void run_ledger(spd_context* ctx, const spd_tensor* t, int need_split, int held_
 }  // namespace spd
 
 using namespace spd;
+
+extern "C" int spd_tensor_repartition(spd_context* ctx, const spd_tensor* piece, int need_split,
+                                      spd_tensor** out, int64_t* bytes_in) {
+  return guarded([&] { run_repartition(ctx, piece, need_split, out, bytes_in); });
+}
 
 extern "C" int spd_ledger_bytes(spd_context* ctx, const spd_tensor* t, int need_split, int held_split,
                                 int64_t pieces, int64_t* bytes_out) {

@@ -443,6 +443,15 @@ class DeviceTensor:
                                               1 if split == "row" else 2, C.byref(h)))
         return DeviceTensor(ctx, h, t.dims, t.format)
 
+    def repartition(self, split: str):
+        """Collective spd_tensor_repartition: this piece moved to colour `rank`
+        of the compute split ("row" | "nonzero").  Returns (piece, bytes in)."""
+        h = C.c_void_p()
+        b = C.c_int64()
+        check(N.lib().spd_tensor_repartition(self.ctx.h, self.h, 1 if split == "row" else 2, C.byref(h),
+                                             C.byref(b)))
+        return DeviceTensor(self.ctx, h, self.dims, self.format), b.value
+
     def piece_span(self):
         lo, hi = C.c_int64(), C.c_int64()
         check(N.lib().spd_tensor_piece_span(self.h, C.byref(lo), C.byref(hi)))

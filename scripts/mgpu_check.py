@@ -173,6 +173,43 @@ def main():
                 failures += 0 if ok else 1
         piece.close()
 
+    # Mismatched placement: a piece placed by one split moved to the other
+    # (spd_tensor_repartition); SpMM on the moved piece; bytes received equal
+    # the crd + vals part of the reference ledger (16 B per missing position).
+    for held, need in (("row", "nonzero"), ("nonzero", "row")):
+        rng = np.random.default_rng(808)
+        n, m = 3000, 2500
+        rows = np.concatenate([np.full(20000, 11), (rng.pareto(1.1, 60000) * 40).astype(np.int64) % n])
+        cols = rng.integers(0, m, rows.shape[0])
+        B = H.SparseTensor.pack((n, m), H.parse_format("ds"), np.stack([rows, cols], 1),
+                                rng.uniform(0.5, 1.5, rows.shape[0]))
+        Cm = K.dense(rng, (m, 32), "dd", False)
+        Cd = torch.from_numpy(Cm.vals).to(dev)
+        piece = H.DeviceTensor.upload_piece(ctx, B, held)
+        moved, nbytes = piece.repartition(need)
+        lo, hi = moved.piece_span()
+        out = torch.zeros(n * 32, dtype=torch.float64, device=dev)
+        cols_ = (H.partition_universe(ctx, moved, world) if need == "row"
+                 else H.partition_nonzero(ctx, moved, 1, world))
+        H.spmm(ctx, moved, Cd, 32, out, first=rank, count=1, pieces=world)
+        W = owned_rows(cols_, B.levels[1].rowptr(), need, n)
+        gathered = [torch.zeros_like(out) for _ in range(world)]
+        dist.all_gather(gathered, out)
+        # expected bytes: positions of my needed span outside my held span
+        hl, hh = piece.piece_span()
+        exp = 16 * max(hi - lo + 1, 0) - 16 * max(min(hi, hh) - max(lo, hl) + 1, 0)
+        okb = torch.tensor([int(nbytes == exp)], device=dev)
+        dist.all_reduce(okb, op=dist.ReduceOp.MIN)
+        if rank == 0:
+            got = assemble([x.cpu().numpy() for x in gathered], W, 32, n)
+            want = np.asarray(oracle_exec.oracle_execute("spmm", {"B": B, "C": Cm}, need, world)["out"]).reshape(n, 32)
+            ok = np.all(np.abs(got - want) <= 1e-10 * np.maximum(np.abs(want), 1e-300)) and bool(okb.item())
+            print(f"[mgpu world={world}] repartition {held}->{need}: spmm {'OK' if ok else 'MISMATCH'} "
+                  f"bytes_in(rank0)={nbytes}", flush=True)
+            failures += 0 if ok else 1
+        moved.close()
+        piece.close()
+
     # SpDISTAL-Batched SpMM on a 2-D grid of the GPUs (x = rows, y = column
     # slabs of C / A): every GPU holds only its slab of C, no combine.
     BATCHED = ("divide(i, io, ii, M.x); divide(j, jo, ji, M.y); reorder(io, jo, ii, ji, k); "
