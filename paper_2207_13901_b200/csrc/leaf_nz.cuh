@@ -299,7 +299,8 @@ __device__ __forceinline__ double row_dot_serial(const int64_t* __restrict__ crd
   return sum;
 }
 
-__global__ void __launch_bounds__(kBlock, 4) k_spmv_rows(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
+template <int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_spmv_rows(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
                                                       const double* __restrict__ vals,
                                                       const double* __restrict__ x, double* __restrict__ y,
                                                       ChunkRecs rec, const int64_t* __restrict__ counters) {

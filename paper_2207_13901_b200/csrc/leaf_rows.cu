@@ -1156,7 +1156,11 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
       const int64_t H = Bm->hot_n;
       double* Chot = (double*)ctx->scratch[6].reserve(sizeof(double) * 32 * (H > 0 ? H : 1));
       const int64_t win = H * 256;
-      const int64_t setaside = persist_setaside(ctx, win);
+      static const bool persist = [] {
+        const char* e = getenv("SPD_PERSIST");
+        return e ? atoi(e) != 0 : true;
+      }();
+      const int64_t setaside = persist ? persist_setaside(ctx, win) : 0;
       cudaLaunchAttribute attr[1];
       int nattr = 0;
       if (setaside > 0 && win > 0) {
@@ -1213,8 +1217,25 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
                                                        col.counters);
     } else if (spmv_rows_mode(nnz, z.m)) {  // short rows: a lane per row
       static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmv_rows);
-      k_spmv_rows<<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      // 6 CTAs/SM (40 registers, a few spills) wins on large matrices
+      // (R-MAT leaf 1.11 -> 1.045 ms), 4 on small ones (C1 / C4)
+      static int minb_env = [] {
+        const char* e = getenv("SPD_SPMV_MINB");
+        return e ? atoi(e) : 0;
+      }();
+      const int minb = minb_env ? minb_env : (nnz >= (int64_t(1) << 26) ? 6 : 4);
+      if (minb == 6) {
+        static int grid6 = 0;
+        if (!grid6) grid6 = occupancy_grid(ctx, k_spmv_rows<6>);
+        k_spmv_rows<6><<<grid6, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      } else if (minb == 8) {
+        static int grid8 = 0;
+        if (!grid8) grid8 = occupancy_grid(ctx, k_spmv_rows<8>);
+        k_spmv_rows<8><<<grid8, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      } else {
+        if (!grid) grid = occupancy_grid(ctx, k_spmv_rows<4>);
+        k_spmv_rows<4><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      }
     } else {
       static int grid = 0;
       if (!grid) grid = occupancy_grid(ctx, k_spmv_nz);
