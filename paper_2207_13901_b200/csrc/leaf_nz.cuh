@@ -551,11 +551,17 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
 // code small), flushing the finished row -- the sub-lane partials summed by
 // an xor butterfly over the sub index -- at each start.  Chunk tickets,
 // records and ownership as k_spmm32_nz.
-template <int N, int UNR, int MINB>
+//
+// MT: SpMTTKRP instead (R = N): C is D(k,:) gathered by the leaf crd, and a
+// second gather Cj(j,:) by jleaf; the value is (B * C(j,l)) * D(k,l) as the
+// reference multiplies (sim.cpp:328-337), added with a unit FMA.
+template <int N, int UNR, int MINB, bool MT = false>
 __global__ void __launch_bounds__(kBlock, MINB) k_spmm_nzv(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
                                                      const double* __restrict__ vals,
                                                      const double* __restrict__ C, double* __restrict__ A,
-                                                     ChunkRecs rec, const int64_t* __restrict__ counters) {
+                                                     ChunkRecs rec, const int64_t* __restrict__ counters,
+                                                     const int32_t* __restrict__ jleaf = nullptr,
+                                                     const double* __restrict__ Cj = nullptr) {
   constexpr int LP = N / 2 < 32 ? N / 2 : 32;  // lanes per position
   constexpr int VPL = N / 64 > 1 ? N / 64 : 1;  // double2 per lane
   constexpr int PPI = 32 / LP;                 // positions per warp instruction
@@ -567,6 +573,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm_nzv(WalkGeom g, NzView z,
   const uint64_t pol_keep = l2_policy_evict_last();
   const uint64_t pol_stream = l2_policy_evict_first();
   const double* Cl = C + 2 * sl;
+  const double* Cjl = MT ? Cj + 2 * sl : nullptr;
   const int64_t tmax = end - begin;
   for (int64_t t = chunk_ticket(counters); t < tmax; t = chunk_ticket(counters)) {
     const int64_t v = begin + t;
@@ -608,19 +615,21 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm_nzv(WalkGeom g, NzView z,
 #pragma unroll
       for (int w = 0; w < VPL; w++) acc[w] = make_double2(0.0, 0.0);
     };
-    int kn = 0;
+    int kn = 0, jn = 0;
     double vn = 0.0;
     if (lane <= e - s) {
       kn = (int)ld_i64_hint(crd + s + lane, pol_stream);
+      if (MT) jn = ld_i32_hint(jleaf + s + lane, pol_stream);
       vn = ld_f64_hint(vals + s + lane, pol_stream);
     }
     for (int64_t base = s; base <= e; base += 32) {
       const int last_off = (int)min((int64_t)31, e - base);
       const int cnt = last_off + 1;
-      const int my_k = kn;
+      const int my_k = kn, my_j = jn;
       const double my_v = vn;
       if (base + 32 + lane <= e) {
         kn = (int)ld_i64_hint(crd + base + 32 + lane, pol_stream);
+        if (MT) jn = ld_i32_hint(jleaf + base + 32 + lane, pol_stream);
         vn = ld_f64_hint(vals + base + 32 + lane, pol_stream);
       }
       const unsigned bm = nz_window_mask(c, base, base + last_off);
@@ -638,6 +647,16 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm_nzv(WalkGeom g, NzView z,
 #pragma unroll
           for (int w = 0; w < VPL; w++)
             cv[i][w] = p < cnt ? ld_f64x2_hint(src + w * 64, pol_keep) : make_double2(0.0, 0.0);
+          if (MT) {
+            const int jj = __shfl_sync(FULL, my_j, p & 31);
+            const double* srcj = Cjl + (int64_t)jj * N;
+#pragma unroll
+            for (int w = 0; w < VPL; w++) {
+              const double2 cj = p < cnt ? ld_f64x2_hint(srcj + w * 64, pol_keep) : make_double2(0.0, 0.0);
+              cv[i][w] = make_double2((bv[i] * cj.x) * cv[i][w].x, (bv[i] * cj.y) * cv[i][w].y);
+            }
+            bv[i] = 1.0;
+          }
         }
         const unsigned gm = GP == 32 ? (bm >> u) : ((bm >> u) & ((1u << GP) - 1u));
         if (gm == 0u) {

@@ -1078,7 +1078,9 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   const spd_level_store& leaf = B->levels[nl - 1];
   const bool mttkrp32 = a.op == Op::SpMTTKRP && a.W == 32 && B->dims[1] < (int64_t(1) << 31) &&
                         B->dims[2] < (int64_t(1) << 31);
-  const bool use_nz = nz_enabled() && (a.op == Op::SpMV || a.op == Op::SpTTV || mttkrp32 ||
+  const bool mttkrpv = a.op == Op::SpMTTKRP && (a.W == 8 || a.W == 16 || a.W == 64 || a.W == 128) &&
+                       B->dims[1] < (int64_t(1) << 31) && B->dims[2] < (int64_t(1) << 31) && spmmv_enabled();
+  const bool use_nz = nz_enabled() && (a.op == Op::SpMV || a.op == Op::SpTTV || mttkrp32 || mttkrpv ||
                                        spmm32 || spmmv);
   NzView z{nullptr, nullptr, 0};
   bool zero_joined = false;
@@ -1129,10 +1131,28 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
         SPD_CHECK_LAUNCH();
         ctx->launches++;
       }
-      static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_mttkrp32_nz<4, 3, false>);
-      k_mttkrp32_nz<4, 3, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->jleaf, a.x, B->vals, a.D, a.out, rec,
-                                                         col.counters);
+      if (mttkrpv) {  // R in {8, 16, 64, 128}
+        switch (a.W) {
+#define SPD_MTV(NN, UU, MB)                                                                              \
+  case NN: {                                                                                             \
+    static int grid = 0;                                                                                 \
+    if (!grid) grid = occupancy_grid(ctx, k_spmm_nzv<NN, UU, MB, true>);                                \
+    k_spmm_nzv<NN, UU, MB, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.D, a.out, rec,     \
+                                                          col.counters, B->jleaf, a.x);                  \
+    break;                                                                                               \
+  }
+          SPD_MTV(8, 4, 3)
+          SPD_MTV(16, 4, 3)
+          SPD_MTV(64, 4, 3)
+          SPD_MTV(128, 2, 3)
+#undef SPD_MTV
+        }
+      } else {
+        static int grid = 0;
+        if (!grid) grid = occupancy_grid(ctx, k_mttkrp32_nz<4, 3, false>);
+        k_mttkrp32_nz<4, 3, false><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->jleaf, a.x, B->vals, a.D, a.out,
+                                                           rec, col.counters);
+      }
     } else if (spmmv) {  // N in {8, 16, 64, 128}
       switch (a.W) {
 #define SPD_SPMMV(NN, UU, MB)                                                                        \

@@ -6,7 +6,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import bench  # noqa
 from paper_2207_13901_b200 import _native as N  # noqa
-ap = argparse.ArgumentParser(); ap.add_argument("--steps", type=int, default=3); ap.add_argument("--kernel", default="spmttkrp")
+ap = argparse.ArgumentParser(); ap.add_argument("--steps", type=int, default=3); ap.add_argument("--kernel", default="spmttkrp"); ap.add_argument("--rank", type=int, default=32)
 a = ap.parse_args()
 import torch  # noqa
 from paper_2207_13901_b200 import host as H  # noqa
@@ -20,7 +20,7 @@ F = int(F[0]); crd1, rp2, crd2, vals = crd1[:F], rp2[:F + 1], crd2[:nnz], vals[:
 ctx = H.Context(0)
 Bt = H.DeviceTensor.upload_rowptr(ctx, (I, J, Kd), H.parse_format("dss"), [rp1, rp2], [crd1, crd2], vals)
 dev = torch.device("cuda", 0)
-R = 32
+R = a.rank
 C_d = torch.from_numpy(bench.dense_vals(J * R, 47)).to(dev); D_d = torch.from_numpy(bench.dense_vals(Kd * R, 48)).to(dev)
 c_d = torch.from_numpy(bench.dense_vals(Kd, 46)).to(dev)
 A_d = torch.empty(I * R, dtype=torch.float64, device=dev); Av = torch.empty(F, dtype=torch.float64, device=dev)

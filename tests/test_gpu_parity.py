@@ -426,3 +426,33 @@ def test_ledger_bytes_match_reference(ctx, need, held, pieces):
         assert got == want, (need, held, pieces, got, want)
         if need == held:
             assert got == [0] * pieces
+
+
+@pytest.mark.parametrize("R", [8, 16, 64, 128])
+@pytest.mark.parametrize("fmt", ["dss", "sss"])
+@pytest.mark.parametrize("schedule,pieces", [("nonzero", 1), ("nonzero", 3), ("row", 2)])
+def test_spmttkrp_ranks_match_restatement(ctx, R, fmt, schedule, pieces):
+    """The compacted-row SpMTTKRP for R in {8, 16, 64, 128} (k_spmm_nzv<R, ...,
+    true>) against the reference (dss and sss trees)."""
+    import oracle_bind as ob
+    from paper_2207_13901_b200.execute import execute
+
+    if fmt == "sss" and schedule == "row" and pieces > 1:
+        pytest.skip("the reference's own sss row split at P > 1 raises a closure violation")
+    rng = np.random.default_rng(R + pieces)
+    spec = K.KERNELS["spmttkrp"]
+    for integers in (True, False):
+        I, J, Kd = 40, 30, 50
+        B = K.random_sparse(rng, (I, J, Kd), fmt, 0.05, integers)
+        t = {"B": B, "C": K.dense(rng, (J, R), "dd", integers), "D": K.dense(rng, (Kd, R), "dd", integers)}
+        fm = dict(spec["formats"], B=fmt)
+        run = ob.RefRun(spec["expr"], K.ROW if schedule == "row" else spec["nonzero"], pieces, "dd",
+                        {nm: (x, fm[nm]) for nm, x in t.items()}).ok()
+        _, want = run.output()
+        out, st, _ = execute("spmttkrp", t, schedule, pieces, ctx)
+        got = np.asarray(out).reshape(-1)
+        if integers:
+            assert np.array_equal(got, want)
+        else:
+            assert np.all(np.abs(got - want) <= 1e-10 * np.maximum(np.abs(want), 1e-300))
+        assert st.work == run.stats()["work"]
