@@ -971,6 +971,12 @@ namespace spd {
 // with one butterfly (2+1+3 shuffles instead of 4 x 5).  Row ids of the
 // positions come from the window's row-start mask, so no row-pointer loads
 // sit on the critical path.
+__device__ __forceinline__ double ld_f64_keep(const double* ptr, uint64_t pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(ptr), "l"(pol));
+  return v;
+}
+
 template <int KT, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) k_sddmm_nz(WalkGeom g, NzView z, const int32_t* __restrict__ crd32h,
                                                       const double* __restrict__ vals,
@@ -978,7 +984,10 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sddmm_nz(WalkGeom g, NzView z,
                                                       const double* __restrict__ D, int64_t K,
                                                       double* __restrict__ Avals,
                                                       const int64_t* __restrict__ counters) {
-  static_assert(KT == 4, "the vectorised layout assumes 4 k per lane");
+  // lane l owns k in [KT*l, KT*l + KT): NV 128-bit loads of D (and C) per
+  // position (a single 64-bit load when KT == 1)
+  static_assert(KT == 1 || KT == 2 || KT == 4 || KT == 8, "K must be 32, 64, 128 or 256");
+  constexpr int NV = KT >= 2 ? KT / 2 : 1;
   const int lane = lane_id();
   const int64_t begin = counters[1], end = counters[2];
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -993,7 +1002,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sddmm_nz(WalkGeom g, NzView z,
     NzCursor c;
     nz_start(z, c, s);
     int64_t cur_i = -1;
-    double2 cr0 = make_double2(0.0, 0.0), cr1 = cr0;
+    double2 cr[NV];
+#pragma unroll
+    for (int w = 0; w < NV; w++) cr[w] = make_double2(0.0, 0.0);
     for (int64_t base = s; base <= e; base += 32) {
       const int cnt = (int)min((int64_t)32, e - base + 1);
       // crd with the hot-column bit (hot_crd): D columns referenced often
@@ -1012,21 +1023,23 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sddmm_nz(WalkGeom g, NzView z,
       double res = 0.0;
 #pragma unroll 1
       for (int g4 = 0; g4 < cnt; g4 += 4) {
-        double2 d0[4], d1[4];
+        double2 dd[4][NV];
 #pragma unroll
         for (int u = 0; u < 4; u++) {
           const int p = g4 + u;
           const int jh = __shfl_sync(FULL, my_j, p & 31);
           const int64_t j = jh & 0x7fffffff;
-          const double2* dp = reinterpret_cast<const double2*>(D + j * K + 4 * lane);
-          if (p < cnt && jh < 0) {
-            d0[u] = ld_f64x2_hint(reinterpret_cast<const double*>(dp), pol_keep);
-            d1[u] = ld_f64x2_hint(reinterpret_cast<const double*>(dp + 1), pol_keep);
-          } else if (p < cnt) {
-            d0[u] = ld_f64x2_hint(reinterpret_cast<const double*>(dp), pol_stream);
-            d1[u] = ld_f64x2_hint(reinterpret_cast<const double*>(dp + 1), pol_stream);
-          } else {
-            d0[u] = d1[u] = make_double2(0.0, 0.0);
+          const double* dp = D + j * K + KT * lane;
+          // one column per load instruction: the policy is uniform per branch
+#pragma unroll
+          for (int w = 0; w < NV; w++) {
+            if (p < cnt && jh < 0)
+              dd[u][w] = KT == 1 ? make_double2(ld_f64_keep(dp, pol_keep), 0.0) : ld_f64x2_hint(dp + 2 * w, pol_keep);
+            else if (p < cnt)
+              dd[u][w] = KT == 1 ? make_double2(ld_f64_keep(dp, pol_stream), 0.0)
+                                 : ld_f64x2_hint(dp + 2 * w, pol_stream);
+            else
+              dd[u][w] = make_double2(0.0, 0.0);
           }
         }
         double part[4];
@@ -1035,12 +1048,21 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sddmm_nz(WalkGeom g, NzView z,
           const int p = g4 + u;
           const int64_t i = __shfl_sync(FULL, my_i, p & 31);
           if (i != cur_i && p < cnt) {  // uniform: a new row's C slice
-            const double* cp = C + i * K + 4 * lane;
-            cr0 = ld_f64x2_hint(cp, pol_stream);
-            cr1 = ld_f64x2_hint(cp + 2, pol_stream);
+            const double* cp = C + i * K + KT * lane;
+#pragma unroll
+            for (int w = 0; w < NV; w++)
+              cr[w] = KT == 1 ? make_double2(ld_f64_hint(cp, pol_stream), 0.0) : ld_f64x2_hint(cp + 2 * w, pol_stream);
             cur_i = i;
           }
-          part[u] = fma(cr0.x, d0[u].x, fma(cr0.y, d0[u].y, fma(cr1.x, d1[u].x, cr1.y * d1[u].y)));
+          // the k's of this lane in ascending order, accumulated from the last
+          double acc = cr[NV - 1].y * dd[u][NV - 1].y;
+          acc = fma(cr[NV - 1].x, dd[u][NV - 1].x, acc);
+#pragma unroll
+          for (int w = NV - 2; w >= 0; w--) {
+            acc = fma(cr[w].y, dd[u][w].y, acc);
+            acc = fma(cr[w].x, dd[u][w].x, acc);
+          }
+          part[u] = acc;
         }
         // butterfly: four warp sums at once
         double a0 = b4 ? part[2] : part[0], a1 = b4 ? part[3] : part[1];

@@ -944,14 +944,28 @@ static bool nz_enabled() {
 bool sddmm_nz_launch(spd_context* ctx, const spd_tensor* B, const WalkGeom& g, const double* C,
                      const double* D, int64_t K, int64_t dk, int64_t dj, double* Avals,
                      const int64_t* counters) {
-  if (!nz_enabled() || K != 128 || dk != 1 || dj != 128 || B->dims[1] >= (int64_t(1) << 31)) return false;
+  if (!nz_enabled() || (K != 32 && K != 64 && K != 128 && K != 256) || dk != 1 || dj != K ||
+      B->dims[1] >= (int64_t(1) << 31))
+    return false;
   NzView z = nz_view(ctx, const_cast<spd_tensor*>(B), g.R, g.nrows);
   const int32_t* h = hot_crd(ctx, const_cast<spd_tensor*>(B), K * 8);
   static int minb = [] {
     const char* e = getenv("SPD_SDDMM_MINB");
     return e ? atoi(e) : 3;
   }();
-  if (minb == 4) {
+  if (K == 32) {
+    static int grid = 0;
+    if (!grid) grid = occupancy_grid(ctx, k_sddmm_nz<1, 4>);
+    k_sddmm_nz<1, 4><<<grid, kBlock, 0, ctx->stream>>>(g, z, h, B->vals, C, D, K, Avals, counters);
+  } else if (K == 64) {
+    static int grid = 0;
+    if (!grid) grid = occupancy_grid(ctx, k_sddmm_nz<2, 4>);
+    k_sddmm_nz<2, 4><<<grid, kBlock, 0, ctx->stream>>>(g, z, h, B->vals, C, D, K, Avals, counters);
+  } else if (K == 256) {
+    static int grid = 0;
+    if (!grid) grid = occupancy_grid(ctx, k_sddmm_nz<8, 2>);
+    k_sddmm_nz<8, 2><<<grid, kBlock, 0, ctx->stream>>>(g, z, h, B->vals, C, D, K, Avals, counters);
+  } else if (minb == 4) {
     static int grid = 0;
     if (!grid) grid = occupancy_grid(ctx, k_sddmm_nz<4, 4>);
     k_sddmm_nz<4, 4><<<grid, kBlock, 0, ctx->stream>>>(g, z, h, B->vals, C, D, K, Avals, counters);

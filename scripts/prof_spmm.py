@@ -13,10 +13,12 @@ import bench  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--scale", type=int, default=24)
-ap.add_argument("--cols", type=int, default=32)
+ap.add_argument("--cols", type=int, default=None, help="N (SpMM, default 32) or K (SDDMM, default 128)")
 ap.add_argument("--kernel", default="spmm", choices=["spmm", "spmv", "sddmm"])
 ap.add_argument("--slice", default=None, help="q/P: only the rows of nonzero colour q of P (whole rows)")
 a = ap.parse_args()
+if a.cols is None:
+    a.cols = 128 if a.kernel == "sddmm" else 32
 
 import torch  # noqa: E402
 
@@ -37,7 +39,7 @@ m = n
 n = len(rp) - 1
 dev = torch.device("cuda", 0)
 rp_d, crd_d, vals_d = (torch.from_numpy(x).to(dev) for x in (rp, crd, vals))
-N = a.cols if a.kernel == "spmm" else (128 if a.kernel == "sddmm" else 1)
+N = a.cols if a.kernel in ("spmm", "sddmm") else 1  # SDDMM: K (C2 configs use 128)
 C_d = torch.from_numpy(bench.dense_vals(m * N, 43)).to(dev)
 A_d = torch.empty(n * N if a.kernel != "sddmm" else len(crd), dtype=torch.float64, device=dev)
 if a.kernel == "sddmm":

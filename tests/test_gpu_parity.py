@@ -456,3 +456,25 @@ def test_spmttkrp_ranks_match_restatement(ctx, R, fmt, schedule, pieces):
         else:
             assert np.all(np.abs(got - want) <= 1e-10 * np.maximum(np.abs(want), 1e-300))
         assert st.work == run.stats()["work"]
+
+
+@pytest.mark.parametrize("Kd", [32, 64, 128, 256])
+@pytest.mark.parametrize("schedule,pieces", [("nonzero", 1), ("nonzero", 5), ("row", 3)])
+def test_sddmm_ranks_match_restatement(ctx, Kd, schedule, pieces):
+    """The compacted-row SDDMM for K in {32, 64, 128, 256} (k_sddmm_nz<K/32>)
+    with D stored j-major, on power-law rows, against the oracle."""
+    from paper_2207_13901_b200.execute import execute
+    from paper_2207_13901_b200.host import SparseTensor, parse_format
+
+    rng = np.random.default_rng(Kd + pieces)
+    n, m = 500, 400
+    rows = np.concatenate([np.full(2000, 7), (rng.pareto(1.2, 12000) * 20).astype(np.int64) % n])
+    cols = rng.integers(0, m, rows.shape[0])
+    for integers in (True, False):
+        vals = rng.integers(1, 5, rows.shape[0]).astype(float) if integers else rng.uniform(0.5, 1.5, rows.shape[0])
+        B = SparseTensor.pack((n, m), parse_format("ds"), np.stack([rows, cols], 1), vals)
+        t = {"B": B, "C": K.dense(rng, (n, Kd), "dd", integers), "D": K.dense(rng, (Kd, m), "dd:1,0", integers)}
+        want = oracle_execute("sddmm", t, schedule, pieces)
+        out, st, _ = execute("sddmm", t, schedule, pieces, ctx)
+        assert_close("sddmm", out, want["out"], integers)
+        assert st.work == want["work"] and st.combines == want["combines"]
