@@ -364,10 +364,22 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmv_rows(WalkGeom g, NzView z
         } else {
           y[id] = sum;
         }
-        if (ends_here) {  // empty rows up to the next non-empty one (bounded by W_c at a chunk end)
-          const int64_t stop = rend == e ? (nid < 0 ? ci.w_hi : min(nid - 1, ci.w_hi)) : nid - 1;
-          for (int64_t rr = id + 1; rr <= stop; rr++) y[rr] = 0.0;
-        }
+      }
+      // empty rows up to the next non-empty one (bounded by W_c at a chunk
+      // end): short gaps by their lane, long ones by the whole warp
+      int64_t glo = 1, ghi = 0;
+      if (act && rend <= e) {
+        glo = id + 1;
+        ghi = rend == e ? (nid < 0 ? ci.w_hi : min(nid - 1, ci.w_hi)) : nid - 1;
+      }
+      const bool long_gap = ghi - glo + 1 > 64;
+      if (!long_gap)
+        for (int64_t rr = glo; rr <= ghi; rr++) y[rr] = 0.0;
+      unsigned gaps = __ballot_sync(FULL, long_gap);
+      while (gaps) {
+        const int t = __ffs(gaps) - 1;
+        gaps &= gaps - 1;
+        zero_gap(y, 1, __shfl_sync(FULL, glo, t), __shfl_sync(FULL, ghi, t));
       }
     }
     // records of the chunk's first (head) and last (tail) rows

@@ -478,3 +478,23 @@ def test_sddmm_ranks_match_restatement(ctx, Kd, schedule, pieces):
         out, st, _ = execute("sddmm", t, schedule, pieces, ctx)
         assert_close("sddmm", out, want["out"], integers)
         assert st.work == want["work"] and st.combines == want["combines"]
+
+
+@pytest.mark.parametrize("schedule,pieces", [("nonzero", 1), ("nonzero", 3), ("row", 4)])
+def test_spmv_long_empty_gaps(ctx, schedule, pieces):
+    """Few non-empty rows among 300k: the empty gaps (warp-zeroed when long)
+    and the empty tail of the last colour are exactly 0.0."""
+    from paper_2207_13901_b200.execute import execute
+    from paper_2207_13901_b200.host import SparseTensor, parse_format
+
+    rng = np.random.default_rng(17)
+    n, m = 300_000, 500
+    rows = np.sort(rng.choice(n // 2, 60, replace=False))
+    rows = np.repeat(rows, 7)
+    cols = rng.integers(0, m, rows.shape[0])
+    B = SparseTensor.pack((n, m), parse_format("ds"), np.stack([rows, cols], 1),
+                          rng.integers(1, 5, rows.shape[0]).astype(float))
+    t = {"B": B, "c": K.dense(rng, (m,), "d")}
+    want = oracle_execute("spmv", t, schedule, pieces)
+    out, st, _ = execute("spmv", t, schedule, pieces, ctx)
+    assert np.array_equal(np.asarray(out), np.asarray(want["out"]))
