@@ -18,6 +18,7 @@
 //   against plan.loops[0].color_bounds (a mismatch is a logic_error);
 // * runs the leaf + deterministic combine and rebuilds the output with
 //   SparseTensor::from_parts, so ExecResult / Stats are drop-in.
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -102,16 +103,93 @@ std::string kernel_of(const Plan& plan) {
       fmt(lhs.tensor) == "dd")
     return "spmm";
   if (t.size() == 3 && fmt(t[0].tensor) == "ds" && fmt(lhs.tensor) == "ds") return "sddmm";
-  if (t.size() == 2 && fmt(t[0].tensor) == "dss" && fmt(t[1].tensor) == "d") return "spttv";
-  if (t.size() == 3 && fmt(t[0].tensor) == "dss" && fmt(lhs.tensor) == "dd") return "spmttkrp";
+  const bool csf = fmt(t[0].tensor) == "dss" || fmt(t[0].tensor) == "sss";
+  if (t.size() == 2 && csf && fmt(t[1].tensor) == "d") return "spttv";
+  if (t.size() == 3 && csf && fmt(lhs.tensor) == "dd") return "spmttkrp";
   throw ValidationError("unsupported on gpu: " + s);
 }
 
 }  // namespace
 
+// SpDISTAL-Batched SpMM: loop 0 divides the rows of B
+// / A (a universe split), loop 1 the columns j of C / A (dense).  Every
+// (x, y) tuple runs spd_spmm on B's row colour x with the column slab y of C
+// (staged contiguous), its block scattered into A; worker ids follow
+// tuple_worker (sim.cpp:535-544, machine.cpp:88-92).
+ExecResult execute_batched_spmm(const Plan& plan, const TensorSet& tensors, const MachineGrid& machine) {
+  const PlanLoop& lx = plan.loops[0];
+  const PlanLoop& ly = plan.loops[1];
+  const auto& t = plan.stmt.terms[0];
+  const std::string out_name = plan.stmt.lhs.tensor;
+  const SparseTensor& Bt = tensors.at(t[0].tensor);
+  const SparseTensor& Ct = tensors.at(t[1].tensor);
+  if (lx.position_space || ly.position_space || plan.combine)
+    throw ValidationError("unsupported on gpu: batched SpMM needs two universe loops and no combine");
+  const std::vector<int64_t>& od = plan.dims.at(out_name);
+  const int64_t n = od[0], N = od[1], K = Ct.dims()[0];
+  Ctx ctx;
+  DevTensor B;
+  upload(ctx, Bt, B);
+  std::vector<spd_color> cols(lx.pieces);
+  check(spd_partition_universe(ctx.h, B.h, lx.pieces, cols.data()));
+  for (int64_t c = 0; c < lx.pieces; c++) {
+    const CoordRange& want = lx.color_bounds[c];
+    const bool same = cols[c].color.lo == want.lo && cols[c].color.hi == want.hi;
+    if (!same && !(cols[c].color.lo > cols[c].color.hi && want.empty()))
+      throw std::logic_error("gpu partition differs from plan() colour bounds");
+  }
+  const std::vector<double>& cv = Ct.vals().scalar_values();
+  std::vector<double> out(static_cast<size_t>(n * N), 0.0);
+  ExecResult r;
+  r.stats.workers = machine.total_workers();
+  r.stats.per_worker.resize(r.stats.workers);
+  for (auto& w : r.stats.per_worker)
+    for (const auto& nm : plan.stmt.tensor_names()) w.bytes_by_tensor[nm] = 0;
+  for (int64_t y = 0; y < ly.pieces; y++) {
+    const CoordRange& slab = ly.color_bounds[y];
+    const int64_t w = slab.empty() ? 0 : slab.hi - slab.lo + 1;
+    std::vector<double> cy(static_cast<size_t>(K * std::max<int64_t>(w, 1)));
+    for (int64_t k = 0; k < K; k++)
+      for (int64_t j = 0; j < w; j++) cy[k * w + j] = cv[k * N + slab.lo + j];
+    std::vector<int64_t> work(lx.pieces, 0);
+    if (w > 0) {
+      const int64_t dims[2] = {K, w};
+      const int kinds[2] = {SPD_DENSE, SPD_DENSE}, order[2] = {0, 1};
+      DevTensor Cy, Ay;
+      check(spd_tensor_upload(ctx.h, 2, dims, kinds, order, nullptr, nullptr, cy.data(), &Cy.h));
+      const int64_t adims[2] = {n, w};
+      std::vector<double> ay(static_cast<size_t>(n * w), 0.0);
+      check(spd_tensor_upload(ctx.h, 2, adims, kinds, order, nullptr, nullptr, ay.data(), &Ay.h));
+      spd_stats st{};
+      check(spd_spmm(ctx.h, B.h, dense_vals_dev(Cy.h), w, const_cast<double*>(dense_vals_dev(Ay.h)), 0,
+                     lx.pieces, &st));
+      check(spd_last_work(ctx.h, work.data(), lx.pieces));
+      check(spd_tensor_download_vals(Ay.h, ay.data()));
+      for (int64_t i = 0; i < n; i++)
+        for (int64_t j = 0; j < w; j++) out[i * N + slab.lo + j] = ay[i * w + j];
+    }
+    for (int64_t x = 0; x < lx.pieces; x++) {
+      std::vector<int64_t> coords(machine.rank(), 0);
+      coords[machine.dim_index(lx.machine_dim)] = x;
+      coords[machine.dim_index(ly.machine_dim)] = y;
+      r.stats.per_worker[machine.worker_id(coords)].work = work[x];
+    }
+  }
+  int64_t total = 0, mx = 0;
+  for (const auto& w : r.stats.per_worker) total += w.work, mx = std::max(mx, w.work);
+  r.stats.imbalance = total == 0 ? 1.0 : (double)mx * (double)r.stats.workers / (double)total;
+  r.stats.combines = 0;
+  const SparseTensor& outstub = tensors.at(out_name);
+  std::vector<LevelStorage> levels;
+  for (int l = 0; l < outstub.num_levels(); l++) levels.push_back(outstub.level(l));
+  r.output = SparseTensor::from_parts(od, plan.formats.at(out_name), std::move(levels), std::move(out));
+  return r;
+}
+
 ExecResult execute_gpu(const Plan& plan, const TensorSet& tensors, const MachineGrid& machine) {
+  if (plan.loops.size() == 2 && kernel_of(plan) == "spmm") return execute_batched_spmm(plan, tensors, machine);
   if (plan.loops.size() != 1)
-    throw ValidationError("unsupported on gpu: exactly one distributed loop is implemented");
+    throw ValidationError("unsupported on gpu: one distributed loop, or the batched two-loop SpMM");
   const PlanLoop& loop = plan.loops[0];
   const std::string kernel = kernel_of(plan);
   const auto& terms = plan.stmt.terms;
