@@ -128,3 +128,79 @@ def test_owned_rows_edge_cases():
     cols = [Colour((0, -1), (0, -1), (0, -1), (0, -1))] * 3
     W = owned_rows(cols, np.zeros(5, np.int64), "nonzero", 4)
     assert all(lo > hi for lo, hi in W[:2]) and W[2] == (0, 3)
+
+
+def test_divide_bounds_host_mirror_matches_oracle():
+    """host.divide_bounds (used by the batched grid's column slabs) is the
+    reference's divide_bounds (planner.cpp:10-20) as the oracle restates it."""
+    import oracle_bind as ob
+    from paper_2207_13901_b200.host import divide_bounds
+
+    for n in (0, 1, 5, 7, 32, 100, 16777216):
+        for p in (1, 2, 3, 4, 7, 8, 9):
+            assert divide_bounds(n, p) == ob.divide_bounds(n, p)
+
+
+def _batched_worker(rank, port, grid, q):
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path[:0] = [root, os.path.join(root, "tests")]
+    import torch.distributed as dist
+
+    import oracle_bind as ob
+    import spd_kernels as K
+    from paper_2207_13901_b200.host import divide_bounds
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    Px, Py = grid
+    rng = np.random.default_rng(3)
+    n, m, N = 60, 40, 10
+    B = K.random_sparse(rng, (n, m), "ds", 0.2, True)
+    Cm = K.dense(rng, (m, N), "dd", True)
+    rp, crd, v = B.levels[1].rowptr(), B.levels[1].crd, B.vals
+    # rank -> worker (x, y) (machine.cpp:88-92); rows of colour x, slab y of C
+    x, y = divmod(rank, Py)
+    (r0, r1) = divide_bounds(n, Px)[x]
+    (c0, c1) = divide_bounds(N, Py)[y]
+    C = Cm.vals.reshape(m, N)[:, c0:c1 + 1]  # the only part of C this rank holds
+    blk = np.zeros((max(r1 - r0 + 1, 0), c1 - c0 + 1))
+    for i in range(r0, r1 + 1):
+        for p in range(rp[i], rp[i + 1]):
+            blk[i - r0] += v[p] * C[crd[p]]
+    work = int(rp[r1 + 1] - rp[r0]) * (c1 - c0 + 1) if r0 <= r1 else 0
+    got = [None] * WORLD
+    dist.all_gather_object(got, (r0, r1, c0, c1, blk, work))
+    if rank == 0:
+        A = np.zeros((n, N))
+        works = [0] * WORLD
+        for w, (a, b, lo, hi, bl, wk) in enumerate(got):
+            A[a:b + 1, lo:hi + 1] = bl
+            works[w] = wk
+        run = ob.RefRun("A(i, j) = B(i, k) * C(k, j)",
+                        "divide(i, io, ii, M.x); divide(j, jo, ji, M.y); reorder(io, jo, ii, ji, k); "
+                        "distribute(io, M.x); distribute(jo, M.y); communicate({B}, io); communicate({A, C}, jo)",
+                        f"x={Px},y={Py}", "dd", K.ref_inputs("spmm", {"B": B, "C": Cm})).ok()
+        ok = np.array_equal(A.reshape(-1), run.output()[1]) and works == run.stats()["work"]
+        q.put(ok)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("grid", [(1, 2), (2, 1)])
+def test_two_rank_batched_grid(grid):
+    """SpDISTAL-Batched on a 2-rank grid: each rank holds only its column
+    slab of C; the assembled blocks and per-worker work equal the
+    reference's plan + execute with the same grid."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_batched_worker, args=(r, port, grid, q)) for r in range(WORLD)]
+    for p in procs:
+        p.start()
+    ok = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+    assert ok
