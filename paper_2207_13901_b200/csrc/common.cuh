@@ -182,6 +182,7 @@ struct spd_tensor {
   // Hot-copy index (SpMM leaf, HOT == 2): leaf crd as int32 where a hot
   // column is 0x80000000 | slot, its row read from a per-call compact copy
   // of the hot rows (hot_ids[slot] = column); built for one dense-row size.
+  int32_t* crd32p = nullptr;  // plain int32 copy of the leaf crd (SpMM HOT == 3)
   int32_t* crd32x = nullptr;
   int32_t* crd32x_alloc = nullptr;
   int32_t* hot_ids = nullptr;

@@ -598,6 +598,8 @@ static void restage_piece(spd_context* ctx, spd_tensor* t, const int64_t* const*
   t->crd32h_rowbytes = 0;
   t->crd32x = nullptr;
   t->crd32x_rowbytes = 0;
+  dev_free(ctx, t->crd32p);
+  t->crd32p = nullptr;
   stage_piece(ctx, t, pos_pairs[1], crd ? crd[1] : nullptr, vals, t->piece_split, false);
 }
 
@@ -707,6 +709,8 @@ int spd_tensor_restage(spd_context* ctx, spd_tensor* t, const int64_t* const* po
     t->crd32h_rowbytes = 0;
     t->crd32x = nullptr;
     t->crd32x_rowbytes = 0;
+    dev_free(ctx, t->crd32p);
+    t->crd32p = nullptr;
     dev_free(ctx, t->jleaf);
     t->jleaf = nullptr;
     dev_free(ctx, t->leaf_rowptr);
@@ -799,6 +803,7 @@ int spd_tensor_destroy(spd_tensor* t) {
     dev_free(ctx, t->leaf_rowptr);
     dev_free(ctx, t->crd32h_alloc);
     dev_free(ctx, t->crd32x_alloc);
+    dev_free(ctx, t->crd32p);
     dev_free(ctx, t->hot_ids);
     dev_free(ctx, t->stage_pairs);
     dev_free(ctx, t->stage_flags);

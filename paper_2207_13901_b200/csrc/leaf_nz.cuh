@@ -409,7 +409,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmv_rows(WalkGeom g, NzView z
 //      rows evict_first (two predicated uniform-policy loads);
 //   2  int32 crd with hot-copy slots (crd32x): a hot column reads its row from
 //      Chot, the per-call compact copy of the hot rows that the launch's L2
-//      access-policy window marks persisting; one plain load per position.
+//      access-policy window marks persisting; one plain load per position;
+//   3  plain int32 crd (crd32p), every C row evict_last (mode 0 with half
+//      the index bytes).
 template <int UNR, int MINB, int HOT, bool DYN = false>
 __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
                                                       const int32_t* __restrict__ crd32h,
@@ -479,7 +481,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
           if (HOT == 2) {
             const double* hsrc = (kk < 0 ? Hl : Cl) + (int64_t)(kk & 0x7fffffff) * 32;
             cv[i] = p < cnt ? __ldg(reinterpret_cast<const double2*>(hsrc)) : make_double2(0.0, 0.0);
-          } else if (HOT) {  // two uniform-policy loads instead of a per-lane policy
+          } else if (HOT == 1) {  // two uniform-policy loads instead of a per-lane policy
             cv[i] = make_double2(0.0, 0.0);
             if (p < cnt && kk < 0) cv[i] = ld_f64x2_hint(src, pol_keep);
             if (p < cnt && kk >= 0) cv[i] = ld_f64x2_hint(src, pol_stream);
@@ -932,6 +934,11 @@ __global__ void k_crd32h(const int64_t* __restrict__ crd, int64_t nnz, const int
 __global__ void k_iota32(int32_t* __restrict__ a, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     a[i] = (int32_t)i;
+}
+
+__global__ void k_crd_to_i32(const int64_t* __restrict__ crd, int64_t n, int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (int32_t)crd[i];
 }
 
 // Hot-copy index: the first H entries of the columns sorted by descending

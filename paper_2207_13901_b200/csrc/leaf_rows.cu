@@ -1182,6 +1182,18 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
         SPD_SPMMV(128, 2, 4)
 #undef SPD_SPMMV
       }
+    } else if (a.op == Op::SpMM && hot_enabled() == 3 && !B->piece) {  // int32 crd, no hot set
+      spd_tensor* Bm = const_cast<spd_tensor*>(B);
+      if (!Bm->crd32p) {
+        SPD_CUDA(cudaMallocAsync((void**)&Bm->crd32p, sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
+        k_crd_to_i32<<<(unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(nnz, 256), 1), ctx->num_sms * 16), 256,
+                       0, s>>>(leaf.crd, nnz, Bm->crd32p);
+        SPD_CHECK_LAUNCH();
+      }
+      static int grid = 0;
+      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, 3, true>);
+      k_spmm32_nz<4, 4, 3, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, Bm->crd32p, B->vals, a.x, a.out, rec,
+                                                         col.counters);
     } else if (a.op == Op::SpMM && hot_enabled() == 2) {
       // hot-copy leaf: gather the hot rows of C into a compact buffer that
       // an L2 access-policy window keeps persisting across the leaf
