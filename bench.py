@@ -526,7 +526,7 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
                     NN.check(NN.lib().spd_tensor_upload(cx.h, 2, dims, kinds, mo, pos_pp, crd_pp,
                                                         Cc.cast(vals_h.data_ptr(), NN.dblp), Cc.byref(h)))
                 else:  # this GPU's colour of the nonzero split, read from host memory
-                    NN.check(NN.lib().spd_tensor_upload_piece(cx.h, dims, kinds, mo, pos_pp, crd_pp,
+                    NN.check(NN.lib().spd_tensor_upload_piece(cx.h, 2, dims, kinds, mo, pos_pp, crd_pp,
                                                               Cc.cast(vals_h.data_ptr(), NN.dblp), 2,
                                                               Cc.byref(h)))
                 Bs = H.DeviceTensor(cx, h, (n, n), fmt)

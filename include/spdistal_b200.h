@@ -163,8 +163,12 @@ int spd_ledger_bytes(spd_context* ctx, const spd_tensor* t, int need_split, int 
  * ledger charges 0 bytes, read from host memory.  Leaves the
  * partition on ctx; the piece runs every leaf op for this GPU's colour and
  * can be re-staged with spd_tensor_restage (a row split's range may move).
- * Without a communicator (world 1) the piece is the whole matrix. */
-int spd_tensor_upload_piece(spd_context* ctx, const int64_t* dims, const int* kinds,
+ * order 3 (dss / sss 3-tensors, the CSF of SpTTV / SpMTTKRP): the upper
+ * levels and the leaf pos are staged whole, the leaf crd / vals as this
+ * GPU's colour of the leaf-level nonzero split (2) or of the top-level row
+ * split (1); such pieces are not re-stageable.
+ * Without a communicator (world 1) the piece is the whole tensor. */
+int spd_tensor_upload_piece(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
                             const int* mode_order, const int64_t* const* pos_pairs,
                             const int64_t* const* crd, const double* vals, int split,
                             spd_tensor** out);

@@ -62,8 +62,8 @@ SIGNATURES = {
     "spd_tensor_repartition": (C.c_int, [vp, vp, C.c_int, C.POINTER(vp), i64p]),
     "spd_tensor_upload_piece": (
         C.c_int,
-        [vp, i64p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(i64p), C.POINTER(i64p), dblp, C.c_int,
-         C.POINTER(vp)],
+        [vp, C.c_int, i64p, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(i64p), C.POINTER(i64p), dblp,
+         C.c_int, C.POINTER(vp)],
     ),
     "spd_tensor_upload_rowptr": (
         C.c_int,

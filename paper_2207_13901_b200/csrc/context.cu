@@ -162,7 +162,7 @@ struct LevelInput {
 static spd_tensor* upload_impl(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
                                const int* mode_order, const int64_t* const* pos,
                                const int64_t* const* crd, const double* vals, bool pairs,
-                               bool validate) {
+                               bool validate, bool skip_leaf = false) {
   HostTrace ht("upload");
   activate(ctx);
   spd_tensor* t = make_skeleton(ctx, order, dims, kinds, mode_order);
@@ -201,8 +201,10 @@ static spd_tensor* upload_impl(spd_context* ctx, int order, const int64_t* dims,
       if (nnz > 0 && (!crd || !crd[l]))
         throw ValidationError("compressed level " + std::to_string(l) + " needs crd");
       L.positions = nnz;
+      // skip_leaf: the leaf's crd / vals are staged later as a piece
+      const bool leaf_piece = skip_leaf && l + 1 == t->groups.size();
       L.rowptr = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (parent + 1));
-      L.crd = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (nnz > 0 ? nnz : 1));
+      L.crd = leaf_piece ? nullptr : (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (nnz > 0 ? nnz : 1));
       if (pairs) {
         int64_t* tmp = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * 2 * (parent > 0 ? parent : 1));
         if (parent > 0) {
@@ -226,10 +228,10 @@ static spd_tensor* upload_impl(spd_context* ctx, int order, const int64_t* dims,
           SPD_CHECK_LAUNCH();
         }
       }
-      if (nnz > 0)
+      if (nnz > 0 && !leaf_piece)
         SPD_CUDA(cudaMemcpyAsync(L.crd, crd[l], sizeof(int64_t) * nnz, cudaMemcpyHostToDevice,
                                  ctx->stream));
-      if ((validate || pairs) && nnz > 0) {
+      if ((validate || pairs) && nnz > 0 && !leaf_piece) {
         unsigned char* start = (unsigned char*)dev_alloc(ctx, nnz);
         SPD_CUDA(cudaMemsetAsync(start, 0, nnz, ctx->stream));
         k_mark_starts<<<grid_for(ctx, parent), 256, 0, ctx->stream>>>(L.rowptr, parent, start, 0, nnz - 1);
@@ -243,8 +245,8 @@ static spd_tensor* upload_impl(spd_context* ctx, int order, const int64_t* dims,
     }
     t->nvals = parent;
     set_whole_span(t);
-    t->vals = (double*)dev_alloc(ctx, sizeof(double) * (parent > 0 ? parent : 1));
-    if (parent > 0) {
+    t->vals = skip_leaf ? nullptr : (double*)dev_alloc(ctx, sizeof(double) * (parent > 0 ? parent : 1));
+    if (parent > 0 && !skip_leaf) {
       if (!vals) throw ValidationError("tensor: vals length does not match leaf count");
       SPD_CUDA(cudaMemcpyAsync(t->vals, vals, sizeof(double) * parent, cudaMemcpyHostToDevice,
                                ctx->stream));
@@ -603,19 +605,83 @@ static void restage_piece(spd_context* ctx, spd_tensor* t, const int64_t* const*
   stage_piece(ctx, t, pos_pairs[1], crd ? crd[1] : nullptr, vals, t->piece_split, false);
 }
 
+// 3-level trees (dss / sss, the CSF of SpTTV / SpMTTKRP): the upper levels
+// and the leaf row pointer are staged whole (O(fibres), the partition and
+// the fibre walk need them); only this GPU's colour of the leaf crd / vals
+// (split 2: nonzero split of the leaf level; 1: rows of the top level) is
+// copied from the host arrays.  Restaging a 3-level piece is not supported.
+static spd_tensor* upload_csf_piece(spd_context* ctx, const int64_t* dims, const int* kinds, const int* mode_order,
+                                    const int64_t* const* pos_pairs, const int64_t* const* crd, const double* vals,
+                                    int split) {
+  spd_tensor* t = upload_impl(ctx, 3, dims, kinds, mode_order, pos_pairs, crd, vals, true, true, true);
+  try {
+    if (t->levels.size() != 3) throw ValidationError("unsupported on gpu: 3-tensor pieces need dss or sss");
+    cudaStream_t s = ctx->stream;
+    spd_level_store& L = t->levels[2];
+    const int rc = split == 1 ? spd_partition_universe(ctx, t, ctx->world, nullptr)
+                              : spd_partition_nonzero(ctx, t, 2, ctx->world, nullptr);
+    if (rc != SPD_OK) throw ValidationError(spd_last_error());
+    const spd_range mine = host_colors(ctx)[ctx->rank].q;
+    const int64_t cnt = std::max<int64_t>(mine.hi - mine.lo + 1, 0);
+    t->piece = true;
+    t->piece_split = 0;  // not re-stageable
+    t->piece_lo = mine.lo;
+    t->piece_hi = mine.hi;
+    t->piece_cap = std::max<int64_t>(cnt, 1);
+    t->piece_crd = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * t->piece_cap);
+    t->piece_vals = (double*)dev_alloc(ctx, sizeof(double) * t->piece_cap);
+    L.crd = t->piece_crd - mine.lo;
+    t->vals = t->piece_vals - mine.lo;
+    int* err_d = (int*)ctx->counters.reserve(sizeof(int64_t) * 16) + 2;
+    SPD_CUDA(cudaMemsetAsync(err_d, 0, sizeof(int), s));
+    if (cnt > 0) {
+      if (!crd || !crd[2]) throw ValidationError("compressed level 2 needs crd");
+      if (!vals) throw ValidationError("tensor: vals length does not match leaf count");
+      SPD_CUDA(cudaMemcpyAsync(t->piece_crd, crd[2] + mine.lo, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice, s));
+      SPD_CUDA(cudaMemcpyAsync(t->piece_vals, vals + mine.lo, sizeof(double) * cnt, cudaMemcpyHostToDevice, s));
+      const int64_t nf = L.parent_positions;
+      unsigned char* flags = (unsigned char*)dev_alloc(ctx, cnt);
+      unsigned char* start = flags - mine.lo;
+      SPD_CUDA(cudaMemsetAsync(flags, 0, cnt, s));
+      k_mark_starts<<<grid_for(ctx, nf), 256, 0, s>>>(L.rowptr, nf, start, mine.lo, mine.hi);
+      SPD_CHECK_LAUNCH();
+      const int64_t dim = dims[mode_order[2]];
+      k_check_crd<<<grid_for(ctx, cnt), 256, 0, s>>>(L.crd, mine.lo, mine.hi, dim, start, mine.lo > 0 ? 1 : 0,
+                                                     mine.lo > 0 ? crd[2][mine.lo - 1] : 0, err_d);
+      SPD_CHECK_LAUNCH();
+      dev_free(ctx, flags);
+    }
+    int err_h = 0;
+    SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters + 12, err_d, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SPD_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(&err_h, ctx->pinned_counters + 12, sizeof(int));
+    if (err_h & 2) throw ValidationError("tensor: crd must be strictly increasing per range");
+    if (err_h & 4) throw ValidationError("tensor: crd value out of dimension bounds");
+  } catch (...) {
+    spd_tensor_destroy(t);
+    throw;
+  }
+  return t;
+}
+
 }  // namespace spd
 
-int spd_tensor_upload_piece(spd_context* ctx, const int64_t* dims, const int* kinds, const int* mode_order,
-                            const int64_t* const* pos_pairs, const int64_t* const* crd, const double* vals,
-                            int split, spd_tensor** out) {
+int spd_tensor_upload_piece(spd_context* ctx, int order, const int64_t* dims, const int* kinds,
+                            const int* mode_order, const int64_t* const* pos_pairs, const int64_t* const* crd,
+                            const double* vals, int split, spd_tensor** out) {
   return guarded([&] {
     checked(ctx);
     if (!out) throw ValidationError("null output handle");
     if (split != 1 && split != 2) throw ValidationError("split must be 1 (rows) or 2 (nonzeros)");
-    if (kinds[0] != SPD_DENSE || kinds[1] != SPD_COMPRESSED)
-      throw ValidationError("unsupported on gpu: pieces of ds (CSR-like) matrices");
     HostTrace ht("upload_piece");
     activate(ctx);
+    if (order == 3) {
+      *out = upload_csf_piece(ctx, dims, kinds, mode_order, pos_pairs, crd, vals, split);
+      ht.mark("staged");
+      return;
+    }
+    if (order != 2 || kinds[0] != SPD_DENSE || kinds[1] != SPD_COMPRESSED)
+      throw ValidationError("unsupported on gpu: pieces of ds matrices and dss / sss 3-tensors");
     spd_tensor* t = make_skeleton(ctx, 2, dims, kinds, mode_order);
     try {
       const int64_t nrows = dims[mode_order[0]];

@@ -433,14 +433,22 @@ class DeviceTensor:
         """spd_tensor_upload_piece: this GPU's colour of a CSR-like matrix,
         staged from the host arrays of `t` (whole pos, this colour's crd/vals)."""
         d, kinds, mo = _format_arrays(t.dims, t.format)
-        p = _i64arr(t.levels[1].pos).reshape(-1)
-        c = _i64arr(t.levels[1].crd)
+        nl = len(t.levels)
+        keep = []
+        pos = (N.i64p * nl)()
+        crd = (N.i64p * nl)()
+        for l, lv in enumerate(t.levels):
+            if lv.kind == COMPRESSED:
+                p = _i64arr(lv.pos).reshape(-1)
+                c = _i64arr(lv.crd)
+                keep += [p, c]
+                pos[l] = p.ctypes.data_as(N.i64p)
+                crd[l] = c.ctypes.data_as(N.i64p)
         vals = np.ascontiguousarray(t.vals, dtype=np.float64)
-        pos = (N.i64p * 2)(None, p.ctypes.data_as(N.i64p))
-        crd = (N.i64p * 2)(None, c.ctypes.data_as(N.i64p))
         h = C.c_void_p()
-        check(N.lib().spd_tensor_upload_piece(ctx.h, d, kinds, mo, pos, crd, vals.ctypes.data_as(N.dblp),
-                                              1 if split == "row" else 2, C.byref(h)))
+        check(N.lib().spd_tensor_upload_piece(ctx.h, len(t.dims), d, kinds, mo, pos, crd,
+                                              vals.ctypes.data_as(N.dblp), 1 if split == "row" else 2,
+                                              C.byref(h)))
         return DeviceTensor(ctx, h, t.dims, t.format)
 
     def repartition(self, split: str):

@@ -210,6 +210,56 @@ def main():
         moved.close()
         piece.close()
 
+    # CSF pieces (dss / sss): upper levels whole, this GPU's colour of the
+    # leaf crd / vals from host memory; SpTTV and SpMTTKRP on the pieces.
+    for fmt in ("dss", "sss"):
+        rng = np.random.default_rng(4242)
+        I, J, Kd, R = 60, 50, 70, 32
+        B = K.random_sparse(rng, (I, J, Kd), fmt, 0.03, False)
+        piece = H.DeviceTensor.upload_piece(ctx, B, "nonzero")
+        Cm, Dm, cv = K.dense(rng, (J, R), "dd", False), K.dense(rng, (Kd, R), "dd", False), K.dense(rng, (Kd,), "d", False)
+        cols_ = H.partition_nonzero(ctx, piece, 2, world)
+        A = torch.zeros(I * R, dtype=torch.float64, device=dev)
+        H.spmttkrp(ctx, piece, torch.from_numpy(Cm.vals).to(dev), torch.from_numpy(Dm.vals).to(dev), R, A,
+                   first=rank, count=1, pieces=world)
+        F = B.levels[1].crd.shape[0]
+        Av = torch.zeros(max(F, 1), dtype=torch.float64, device=dev)
+        H.partition_nonzero(ctx, piece, 2, world)
+        H.spttv(ctx, piece, torch.from_numpy(cv.vals).to(dev), Av, first=rank, count=1, pieces=world)
+        # owned output rows: i via the leaf row pointer (rows absent from an sss top are empty), fibres via rp2
+        rp2 = B.levels[2].rowptr()
+        if fmt == "dss":
+            leaf_rp = rp2[B.levels[1].rowptr()]
+        else:
+            top = B.levels[0].crd
+            rp1 = B.levels[1].rowptr()
+            leaf_rp = np.array([rp2[rp1[np.searchsorted(top, i)]] for i in range(I + 1)], np.int64)
+        Wm = owned_rows(cols_, leaf_rp, "nonzero", I)
+        Wt = owned_rows(cols_, rp2, "nonzero", F)
+        ga = [torch.zeros_like(A) for _ in range(world)]
+        dist.all_gather(ga, A)
+        gt = [torch.zeros_like(Av) for _ in range(world)]
+        dist.all_gather(gt, Av)
+        if rank == 0:
+            got = assemble([x.cpu().numpy() for x in ga], Wm, R, I)
+            spec = K.KERNELS["spmttkrp"]
+            fm = dict(spec["formats"], B=fmt)
+            run = ob.RefRun(spec["expr"], spec["nonzero"], world, "dd",
+                            {"B": (B, fmt), "C": (Cm, "dd"), "D": (Dm, "dd")}).ok()
+            want = run.output()[1].reshape(I, R)
+            ok1 = np.all(np.abs(got - want) <= 1e-10 * np.maximum(np.abs(want), 1e-300))
+            gotv = assemble([x.cpu().numpy()[:F].reshape(F, 1) for x in gt], Wt, 1, F).reshape(-1)
+            spec2 = K.KERNELS["spttv"]
+            run2 = ob.RefRun(spec2["expr"], spec2["nonzero"], world, "ss" if fmt == "sss" else "ds",
+                             {"B": (B, fmt), "c": (cv, "d")}).ok()
+            want2 = run2.output()[1]
+            ok2 = np.all(np.abs(gotv - want2) <= 1e-10 * np.maximum(np.abs(want2), 1e-300))
+            lo, hi = piece.piece_span()
+            print(f"[mgpu world={world}] csf piece {fmt}: spmttkrp {'OK' if ok1 else 'MISMATCH'} spttv "
+                  f"{'OK' if ok2 else 'MISMATCH'} piece=[{lo},{hi}] nnz={len(B.vals)}", flush=True)
+            failures += (0 if ok1 else 1) + (0 if ok2 else 1)
+        piece.close()
+
     # SpDISTAL-Batched SpMM on a 2-D grid of the GPUs (x = rows, y = column
     # slabs of C / A): every GPU holds only its slab of C, no combine.
     BATCHED = ("divide(i, io, ii, M.x); divide(j, jo, ji, M.y); reorder(io, jo, ii, ji, k); "

@@ -498,3 +498,36 @@ def test_spmv_long_empty_gaps(ctx, schedule, pieces):
     want = oracle_execute("spmv", t, schedule, pieces)
     out, st, _ = execute("spmv", t, schedule, pieces, ctx)
     assert np.array_equal(np.asarray(out), np.asarray(want["out"]))
+
+
+@pytest.mark.parametrize("fmt", ["dss", "sss"])
+def test_csf_upload_piece_single_gpu(ctx, fmt):
+    """spd_tensor_upload_piece of a 3-tensor without a communicator is the
+    whole tensor (upper levels whole, leaf crd / vals as the piece):
+    SpMTTKRP and SpTTV on it match the oracle; a bad leaf crd is rejected."""
+    import oracle_bind as ob
+    import torch
+
+    from paper_2207_13901_b200 import host as H
+    from paper_2207_13901_b200._native import SpdValidationError
+
+    rng = np.random.default_rng(12)
+    I, J, Kd, R = 30, 20, 40, 32
+    B = K.random_sparse(rng, (I, J, Kd), fmt, 0.05, True)
+    Cm, Dm = K.dense(rng, (J, R), "dd", True), K.dense(rng, (Kd, R), "dd", True)
+    piece = H.DeviceTensor.upload_piece(ctx, B, "nonzero")
+    try:
+        assert piece.piece_span() == (0, len(B.vals) - 1)
+        H.partition_nonzero(ctx, piece, 2, 1)
+        A = torch.empty(I * R, dtype=torch.float64, device="cuda")
+        H.spmttkrp(ctx, piece, torch.from_numpy(Cm.vals).cuda(), torch.from_numpy(Dm.vals).cuda(), R, A, pieces=1)
+        spec = K.KERNELS["spmttkrp"]
+        run = ob.RefRun(spec["expr"], spec["nonzero"], 1, "dd", {"B": (B, fmt), "C": (Cm, "dd"), "D": (Dm, "dd")}).ok()
+        assert np.array_equal(A.cpu().numpy(), run.output()[1])
+    finally:
+        piece.close()
+    bad = K.random_sparse(rng, (I, J, Kd), fmt, 0.05, True)
+    bad.levels[2].crd = bad.levels[2].crd.copy()
+    bad.levels[2].crd[0] = Kd + 3
+    with pytest.raises(SpdValidationError):
+        H.DeviceTensor.upload_piece(ctx, bad, "nonzero")
