@@ -400,6 +400,159 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmv_rows(WalkGeom g, NzView z
 }
 
 // ---------------------------------------------------------------------------
+// SpMV / SpTTV, staged (CSR-stream style): a group of 32 compacted rows is a
+// contiguous position range; the warp computes its products B(p) * x(crd(p))
+// window by window with lane-per-position loads -- crd / vals coalesced and
+// streamed, 8 independent x gathers per lane in flight -- into a per-warp
+// shared-memory window, then each lane sums its own row's products from
+// shared memory in stored-position order (rows longer than kStageLong: the
+// whole warp, lane-strided + butterfly).  Against k_spmv_rows this replaces
+// per-lane uncoalesced crd / vals loads (32 lines per instruction) and the
+// crd -> x dependence chain per lane with coalesced loads and more memory
+// parallelism.  Short rows add the rounded products in stored order, as the
+// reference does (sim.cpp:328-350).
+constexpr int kStageWin = 256;
+constexpr int kStageLong = 32;
+
+__device__ __forceinline__ void stage_products(const int64_t* __restrict__ crd, const double* __restrict__ vals,
+                                               const double* __restrict__ x, int64_t w0, int wn,
+                                               double* __restrict__ sp, uint64_t pol) {
+  const int lane = lane_id();
+  constexpr int PER = kStageWin / 32;
+  int64_t k[PER];
+  double v[PER];
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    const int o = i * 32 + lane;
+    k[i] = o < wn ? ld_i64_hint(crd + w0 + o, pol) : 0;
+    v[i] = o < wn ? ld_f64_hint(vals + w0 + o, pol) : 0.0;
+  }
+  double xv[PER];
+#pragma unroll
+  for (int i = 0; i < PER; i++) xv[i] = i * 32 + lane < wn ? __ldg(x + k[i]) : 0.0;
+#pragma unroll
+  for (int i = 0; i < PER; i++) {
+    const double pr = __dmul_rn(v[i], xv[i]);
+    if (i * 32 + lane < wn) sp[i * 32 + lane] = pr;
+  }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_spmv_stage(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
+                                                      const double* __restrict__ vals,
+                                                      const double* __restrict__ x, double* __restrict__ y,
+                                                      ChunkRecs rec, const int64_t* __restrict__ counters) {
+  const int lane = lane_id();
+  const int64_t begin = counters[1], end = counters[2];
+  const uint64_t pol = l2_policy_evict_first();
+  __shared__ double s_prod[kBlock / 32][kStageWin];
+  double* sp = s_prod[threadIdx.x >> 5];
+  for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
+    const ChunkInfo ci = chunk_info(g, v, begin);
+    if (ci.q_lo > ci.q_hi) {
+      zero_gap(y, 1, ci.w_lo, ci.w_hi);
+      if (lane == 0) rec.row[2 * ci.local] = -1, rec.row[2 * ci.local + 1] = -1, rec.cont[ci.local] = 0;
+      continue;
+    }
+    const int64_t k = ci.local, s = ci.s, e = ci.e;
+    const int64_t ic0 = warp_owner(z.ptr, z.m, s);  // the last row is found by the walk itself
+    const bool head = ld64(z.ptr + ic0) < s;
+    int64_t ic1 = z.m - 1;
+    if (s == ci.q_lo && !head) zero_gap(y, 1, ci.w_lo, ld64(z.id + ic0) - 1);
+    int64_t head_row = -1, tail_row = -1;
+    int head_cont = 0;
+    double head_val = 0.0, tail_val = 0.0;
+    for (int64_t g0 = ic0; g0 <= ic1; g0 += 32) {
+      const int64_t r = g0 + lane;
+      const int64_t pa = r < z.m ? ld64(z.ptr + r) : INT64_MAX;
+      // rows of this group that start inside the chunk (or the head row)
+      const unsigned in = __ballot_sync(FULL, r == ic0 || pa <= e);
+      if (in != FULL) ic1 = g0 + 31 - __clz(in);  // the chunk's last row is in this group
+      const bool act = r <= ic1;
+      int64_t a = 0, b = -1, id = -1, nid = -1, rend = -1;
+      if (act) {
+        rend = ld64(z.ptr + r + 1) - 1;
+        a = max(pa, s);
+        b = min(rend, e);
+        id = ld64(z.id + r);
+        nid = r + 1 < z.m ? ld64(z.id + r + 1) : -1;
+      }
+      // the group's positions are contiguous: [first row's a, last row's b]
+      const int64_t lo = __shfl_sync(FULL, a, 0);
+      const int64_t hi = __shfl_sync(FULL, b, (int)min((int64_t)31, ic1 - g0));
+      const bool lng = act && b - a + 1 > kStageLong;
+      double sum = 0.0;
+      for (int64_t w0 = lo; w0 <= hi; w0 += kStageWin) {
+        const int wn = (int)min((int64_t)kStageWin, hi - w0 + 1);
+        stage_products(crd, vals, x, w0, wn, sp, pol);
+        __syncwarp();
+        const int64_t wl = w0 + wn - 1;
+        if (act && !lng && a <= wl && b >= w0) {  // short row: serial, stored order
+          const int qb = (int)(min(b, wl) - w0);
+          for (int q = (int)(max(a, w0) - w0); q <= qb; q++) sum += sp[q];
+        }
+        unsigned lm = __ballot_sync(FULL, lng && a <= wl && b >= w0);
+        while (lm) {  // long rows: the warp reduces the row's slice of the window
+          const int t = __ffs(lm) - 1;
+          lm &= lm - 1;
+          const int qa = (int)(max(__shfl_sync(FULL, a, t), w0) - w0);
+          const int qb = (int)(min(__shfl_sync(FULL, b, t), wl) - w0);
+          double part = 0.0;
+          for (int q = qa + lane; q <= qb; q += 32) part += sp[q];
+          part = warp_sum(part);
+          if (lane == t) sum += part;
+        }
+        __syncwarp();
+      }
+      if (act) {
+        const bool is_head = r == ic0 && head;
+        const bool ends_here = rend <= e;
+        if (is_head) {
+          head_row = id;
+          head_val = sum;
+          head_cont = ends_here ? 0 : 1;
+        } else if (!ends_here) {
+          tail_row = id;
+          tail_val = sum;
+        } else {
+          y[id] = sum;
+        }
+      }
+      // empty rows up to the next non-empty one (bounded by W_c at a chunk
+      // end): short gaps by their lane, long ones by the whole warp
+      int64_t glo = 1, ghi = 0;
+      if (act && rend <= e) {
+        glo = id + 1;
+        ghi = rend == e ? (nid < 0 ? ci.w_hi : min(nid - 1, ci.w_hi)) : nid - 1;
+      }
+      const bool long_gap = ghi - glo + 1 > 64;
+      if (!long_gap)
+        for (int64_t rr = glo; rr <= ghi; rr++) y[rr] = 0.0;
+      unsigned gaps = __ballot_sync(FULL, long_gap);
+      while (gaps) {
+        const int t = __ffs(gaps) - 1;
+        gaps &= gaps - 1;
+        zero_gap(y, 1, __shfl_sync(FULL, glo, t), __shfl_sync(FULL, ghi, t));
+      }
+    }
+    // records of the chunk's first (head) and last (tail) rows
+    head_row = __shfl_sync(FULL, head_row, 0);  // the head row is lane 0 of the first group
+    head_val = __shfl_sync(FULL, head_val, 0);
+    head_cont = __shfl_sync(FULL, head_cont, 0);
+    const int tl = (int)((ic1 - ic0) & 31);  // the tail row is lane (ic1 - ic0) % 32 of the last group
+    tail_row = __shfl_sync(FULL, tail_row, tl);
+    tail_val = __shfl_sync(FULL, tail_val, tl);
+    if (lane == 0) {
+      rec.row[2 * k] = head_row;
+      rec.row[2 * k + 1] = tail_row;
+      rec.cont[k] = head_cont;
+      rec.val[2 * k] = head_val;
+      rec.val[2 * k + 1] = tail_val;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // SpMM N == 32 over the compacted view: half a warp per position, 128-bit
 // register gathers UNR pairs deep, crd/vals of the next window prefetched,
 // row switches from the window mask (no dependent loads on the critical path).

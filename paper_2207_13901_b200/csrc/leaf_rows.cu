@@ -930,6 +930,17 @@ static bool spmv_rows_mode(int64_t nnz, int64_t m) {
   return m > 0 && nnz <= kRowsAvg * m;
 }
 
+// Staged-product SpMV / SpTTV leaf (k_spmv_stage), SPD_SPMV_STAGE=1; off by
+// default: R-MAT SpMV leaf 1.30 ms vs 1.00 ms for k_spmv_rows, C1 0.142 vs
+// 0.116 ms, C4 SpTTV 0.254 vs 0.190 ms (profiles/README.md).
+static bool spmv_stage_mode() {
+  static int v = [] {
+    const char* e = getenv("SPD_SPMV_STAGE");
+    return e ? atoi(e) : 0;
+  }();
+  return v != 0;
+}
+
 // Whether an op walks the compacted view (default) -- SPD_NZ=0 selects the
 // direct row-pointer walks (kept for comparison).
 static bool nz_enabled() {
@@ -1261,6 +1272,24 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
       if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, 0>);
       k_spmm32_nz<4, 4, 0><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
                                                        col.counters);
+    } else if (spmv_stage_mode()) {  // staged products, lane per row from shared memory
+      static int minb_env = [] {
+        const char* e = getenv("SPD_STAGE_MINB");
+        return e ? atoi(e) : 4;
+      }();
+      if (minb_env == 6) {
+        static int grid6 = 0;
+        if (!grid6) grid6 = occupancy_grid(ctx, k_spmv_stage<6>);
+        k_spmv_stage<6><<<grid6, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      } else if (minb_env == 3) {
+        static int grid3 = 0;
+        if (!grid3) grid3 = occupancy_grid(ctx, k_spmv_stage<3>);
+        k_spmv_stage<3><<<grid3, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      } else {
+        static int grid4 = 0;
+        if (!grid4) grid4 = occupancy_grid(ctx, k_spmv_stage<4>);
+        k_spmv_stage<4><<<grid4, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      }
     } else if (spmv_rows_mode(nnz, z.m)) {  // short rows: a lane per row
       static int grid = 0;
       // 6 CTAs/SM (40 registers, a few spills) wins on large matrices
