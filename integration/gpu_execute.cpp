@@ -115,18 +115,20 @@ std::string kernel_of(const Plan& plan) {
 // / A (a universe split), loop 1 the columns j of C / A (dense).  Every
 // (x, y) tuple runs spd_spmm on B's row colour x with the column slab y of C
 // (staged contiguous), its block scattered into A; worker ids follow
-// tuple_worker (sim.cpp:535-544, machine.cpp:88-92).
-ExecResult execute_batched_spmm(const Plan& plan, const TensorSet& tensors, const MachineGrid& machine) {
+// tuple_worker (sim.cpp:535-544, machine.cpp:88-92).  Batched SpMTTKRP is the
+// same shape: rows i over loop 0, the rank columns l of C, D and A over loop
+// 1, spd_spmttkrp on the slabs of both factors.
+ExecResult execute_batched(const Plan& plan, const TensorSet& tensors, const MachineGrid& machine,
+                           const std::string& kernel) {
   const PlanLoop& lx = plan.loops[0];
   const PlanLoop& ly = plan.loops[1];
   const auto& t = plan.stmt.terms[0];
   const std::string out_name = plan.stmt.lhs.tensor;
   const SparseTensor& Bt = tensors.at(t[0].tensor);
-  const SparseTensor& Ct = tensors.at(t[1].tensor);
   if (lx.position_space || ly.position_space || plan.combine)
-    throw ValidationError("unsupported on gpu: batched SpMM needs two universe loops and no combine");
+    throw ValidationError("unsupported on gpu: batched " + kernel + " needs two universe loops and no combine");
   const std::vector<int64_t>& od = plan.dims.at(out_name);
-  const int64_t n = od[0], N = od[1], K = Ct.dims()[0];
+  const int64_t n = od[0], N = od[1];
   Ctx ctx;
   DevTensor B;
   upload(ctx, Bt, B);
@@ -138,31 +140,41 @@ ExecResult execute_batched_spmm(const Plan& plan, const TensorSet& tensors, cons
     if (!same && !(cols[c].color.lo > cols[c].color.hi && want.empty()))
       throw std::logic_error("gpu partition differs from plan() colour bounds");
   }
-  const std::vector<double>& cv = Ct.vals().scalar_values();
   std::vector<double> out(static_cast<size_t>(n * N), 0.0);
   ExecResult r;
   r.stats.workers = machine.total_workers();
   r.stats.per_worker.resize(r.stats.workers);
   for (auto& w : r.stats.per_worker)
     for (const auto& nm : plan.stmt.tensor_names()) w.bytes_by_tensor[nm] = 0;
+  const int kinds[2] = {SPD_DENSE, SPD_DENSE}, order[2] = {0, 1};
+  // column slab [lo, lo + w) of a dense rows x N factor, uploaded contiguous
+  auto slab_of = [&](const SparseTensor& F, int64_t lo, int64_t w, DevTensor& dst) {
+    const int64_t rows = F.dims()[0];
+    const std::vector<double>& fv = F.vals().scalar_values();
+    std::vector<double> fy(static_cast<size_t>(rows * w));
+    for (int64_t k = 0; k < rows; k++)
+      for (int64_t j = 0; j < w; j++) fy[k * w + j] = fv[k * N + lo + j];
+    const int64_t dims[2] = {rows, w};
+    check(spd_tensor_upload(ctx.h, 2, dims, kinds, order, nullptr, nullptr, fy.data(), &dst.h));
+  };
   for (int64_t y = 0; y < ly.pieces; y++) {
     const CoordRange& slab = ly.color_bounds[y];
     const int64_t w = slab.empty() ? 0 : slab.hi - slab.lo + 1;
-    std::vector<double> cy(static_cast<size_t>(K * std::max<int64_t>(w, 1)));
-    for (int64_t k = 0; k < K; k++)
-      for (int64_t j = 0; j < w; j++) cy[k * w + j] = cv[k * N + slab.lo + j];
-    std::vector<int64_t> work(lx.pieces, 0);
+  std::vector<int64_t> work(lx.pieces, 0);
     if (w > 0) {
-      const int64_t dims[2] = {K, w};
-      const int kinds[2] = {SPD_DENSE, SPD_DENSE}, order[2] = {0, 1};
-      DevTensor Cy, Ay;
-      check(spd_tensor_upload(ctx.h, 2, dims, kinds, order, nullptr, nullptr, cy.data(), &Cy.h));
+      DevTensor Cy, Dy, Ay;
       const int64_t adims[2] = {n, w};
       std::vector<double> ay(static_cast<size_t>(n * w), 0.0);
       check(spd_tensor_upload(ctx.h, 2, adims, kinds, order, nullptr, nullptr, ay.data(), &Ay.h));
+      double* a_dev = const_cast<double*>(dense_vals_dev(Ay.h));
       spd_stats st{};
-      check(spd_spmm(ctx.h, B.h, dense_vals_dev(Cy.h), w, const_cast<double*>(dense_vals_dev(Ay.h)), 0,
-                     lx.pieces, &st));
+      slab_of(tensors.at(t[1].tensor), slab.lo, w, Cy);
+      if (kernel == "spmm") {
+        check(spd_spmm(ctx.h, B.h, dense_vals_dev(Cy.h), w, a_dev, 0, lx.pieces, &st));
+      } else {
+        slab_of(tensors.at(t[2].tensor), slab.lo, w, Dy);
+        check(spd_spmttkrp(ctx.h, B.h, dense_vals_dev(Cy.h), dense_vals_dev(Dy.h), w, a_dev, 0, lx.pieces, &st));
+      }
       check(spd_last_work(ctx.h, work.data(), lx.pieces));
       check(spd_tensor_download_vals(Ay.h, ay.data()));
       for (int64_t i = 0; i < n; i++)
@@ -187,9 +199,12 @@ ExecResult execute_batched_spmm(const Plan& plan, const TensorSet& tensors, cons
 }
 
 ExecResult execute_gpu(const Plan& plan, const TensorSet& tensors, const MachineGrid& machine) {
-  if (plan.loops.size() == 2 && kernel_of(plan) == "spmm") return execute_batched_spmm(plan, tensors, machine);
+  if (plan.loops.size() == 2) {
+    const std::string k = kernel_of(plan);
+    if (k == "spmm" || k == "spmttkrp") return execute_batched(plan, tensors, machine, k);
+  }
   if (plan.loops.size() != 1)
-    throw ValidationError("unsupported on gpu: one distributed loop, or the batched two-loop SpMM");
+    throw ValidationError("unsupported on gpu: one distributed loop, or the batched two-loop SpMM / SpMTTKRP");
   const PlanLoop& loop = plan.loops[0];
   const std::string kernel = kernel_of(plan);
   const auto& terms = plan.stmt.terms;

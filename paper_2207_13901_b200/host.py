@@ -824,6 +824,57 @@ def spmm_batched(ctx, B: DeviceTensor, Cd, n_cols, A, grid, rank=None, stats=Tru
     return Stats(Px * Py, work, imb, 0)
 
 
+def spmttkrp_batched(ctx, B: DeviceTensor, Cd, Dd, R, A, grid, rank=None, stats=True):
+    """SpMTTKRP A(i,l) = B(i,j,k) * C(j,l) * D(k,l) on a 2-D machine grid, the
+    batched form of spmm_batched: rows i of B/A divided over x (a universe
+    split of B's top level), the rank columns l of C, D and A divided over y
+    (divide_bounds on R).  Worker (x, y) computes A[rows_x, slab_y] from the
+    column slabs C[:, slab_y] and D[:, slab_y] only; no combine.  Same
+    schedule shape as test_planner.cpp:193-225 (divide both output modes,
+    distribute io over x and lo over y); the reference plans and executes it
+    through the same code (planner.cpp:142-359, sim.cpp:816-1010).
+
+    rank None: every tuple on this GPU, in worker order x*Py + y.  With a
+    communicator of Px*Py GPUs: this rank's tuple; Cd / Dd are then this
+    rank's slabs (J x w and K x w, contiguous) and A its I x w block buffer.
+    Stats: work[x*Py+y] = nnz(rows_x) * w_y (each leaf entry times the slab
+    width, the reference's per-coordinate count), combines 0."""
+    import torch
+
+    Px, Py = grid
+    n = B.dims[0]
+    slabs = divide_bounds(R, Py)
+    cols = partition_universe(ctx, B, Px)
+    if rank is not None:
+        x, y = divmod(rank, Py)
+        lo, hi = slabs[y]
+        w = max(hi - lo + 1, 0)
+        if w > 0:
+            spmttkrp(ctx, B, Cd, Dd, w, A, first=x, count=1, pieces=Px, stats=False)
+    else:
+        J = Cd.numel() // R if R else 0
+        Kd = Dd.numel() // R if R else 0
+        Cv, Dv, Av = Cd.view(J, R), Dd.view(Kd, R), A.view(n, R)
+        for y, (lo, hi) in enumerate(slabs):
+            w = hi - lo + 1
+            if w <= 0:
+                continue
+            Ay = torch.empty(n * w, dtype=torch.float64, device=A.device)
+            spmttkrp(ctx, B, Cv[:, lo:hi + 1].contiguous(), Dv[:, lo:hi + 1].contiguous(), w, Ay,
+                     pieces=Px, stats=False)
+            Av[:, lo:hi + 1] = Ay.view(n, w)
+    if not stats:
+        return None
+    nnz_x = [c.q[1] - c.q[0] + 1 if c.q[0] <= c.q[1] else 0 for c in cols]
+    work = [0] * (Px * Py)
+    for x in range(Px):
+        for y, (lo, hi) in enumerate(slabs):
+            work[x * Py + y] = nnz_x[x] * max(hi - lo + 1, 0)
+    total, mx = sum(work), max(work) if work else 0
+    imb = 1.0 if total == 0 else mx * len(work) / total
+    return Stats(Px * Py, work, imb, 0)
+
+
 def sddmm(ctx, B: DeviceTensor, Cd, Dd, K, dk, dj, Avals, first=0, count=None, pieces=None, stats=True):
     st = N.spd_stats()
     count = pieces - first if count is None else count

@@ -295,6 +295,44 @@ def main():
             failures += 0 if ok else 1
         Bd.close()
 
+    # Batched SpMTTKRP on the same 2-D grids: rows of B / A over x, rank
+    # columns of C, D, A over y; every GPU holds only its slabs of C and D.
+    BATCHED_MT = ("divide(i, io, ii, M.x); divide(l, lo, li, M.y); reorder(io, lo, ii, j, k, li); "
+                  "distribute(io, M.x); distribute(lo, M.y); communicate({B}, io); communicate({A, C, D}, lo)")
+    for Px in [d for d in range(1, world + 1) if world % d == 0]:
+        Py = world // Px
+        rng = np.random.default_rng(600 + Px)
+        I, J, Kd, R = 300, 120, 150, 32
+        B = K.random_sparse(rng, (I, J, Kd), "dss", 0.002, True)
+        Cm = K.dense(rng, (J, R), "dd", True)
+        Dm = K.dense(rng, (Kd, R), "dd", True)
+        Bd = H.DeviceTensor.upload(ctx, B)
+        x, y = divmod(rank, Py)
+        lo, hi = H.divide_bounds(R, Py)[y]
+        w = hi - lo + 1
+        Cs = torch.from_numpy(np.ascontiguousarray(Cm.vals.reshape(J, R)[:, lo:hi + 1])).to(dev)
+        Ds = torch.from_numpy(np.ascontiguousarray(Dm.vals.reshape(Kd, R)[:, lo:hi + 1])).to(dev)
+        Ab = torch.full((I * max(w, 1),), float("nan"), dtype=torch.float64, device=dev)
+        H.spmttkrp_batched(ctx, Bd, Cs, Ds, R, Ab, (Px, Py), rank=rank, stats=False)
+        cols_ = H.partition_universe(ctx, Bd, Px)
+        r0, r1 = cols_[x].top
+        block = Ab.view(I, max(w, 1))[r0:r1 + 1, :w].cpu().numpy() if r0 <= r1 else np.zeros((0, w))
+        blocks = [None] * world
+        dist.all_gather_object(blocks, (r0, r1, lo, hi, block))
+        if rank == 0:
+            got = np.full((I, R), np.nan)
+            for (a, b, c0, c1, blk) in blocks:
+                if a <= b and c0 <= c1:
+                    got[a:b + 1, c0:c1 + 1] = blk
+            run = ob.RefRun("A(i, l) = B(i, j, k) * C(j, l) * D(k, l)", BATCHED_MT, f"x={Px},y={Py}", "dd",
+                            K.ref_inputs("spmttkrp", {"B": B, "C": Cm, "D": Dm})).ok()
+            want = run.output()[1].reshape(I, R)
+            ok = np.array_equal(got, want)
+            print(f"[mgpu world={world}] batched spmttkrp grid x={Px},y={Py}: {'OK' if ok else 'MISMATCH'}",
+                  flush=True)
+            failures += 0 if ok else 1
+        Bd.close()
+
     # SpAdd3: every GPU assembles its row block, global pos offsets from the
     # all-gathered per-GPU nnz, pieces gathered on rank 0 with NCCL send/recv.
     for integers in (True, False):

@@ -531,3 +531,44 @@ def test_csf_upload_piece_single_gpu(ctx, fmt):
     bad.levels[2].crd[0] = Kd + 3
     with pytest.raises(SpdValidationError):
         H.DeviceTensor.upload_piece(ctx, bad, "nonzero")
+
+
+BATCHED_MTTKRP = ("divide(i, io, ii, M.x); divide(l, lo, li, M.y); reorder(io, lo, ii, j, k, li); "
+                  "distribute(io, M.x); distribute(lo, M.y); communicate({B}, io); communicate({A, C, D}, lo)")
+
+
+@pytest.mark.parametrize("grid,R", [((2, 3), 6), ((3, 2), 32), ((1, 4), 16), ((4, 1), 8), ((2, 2), 5)])
+def test_spmttkrp_batched_two_dimensional_grid(ctx, grid, R):
+    """Batched SpMTTKRP on a 2-D machine grid (rows over x, rank columns over
+    y) against the reference's own plan() + execute() with the same grid:
+    output, per-worker work, imbalance and combines."""
+    import torch
+
+    from paper_2207_13901_b200 import host as H
+
+    rng = np.random.default_rng(sum(grid) * 7 + R)
+    for integers in (True, False):
+        I, J, Kd = 40, 23, 31
+        B = K.random_sparse(rng, (I, J, Kd), "dss", 0.02, integers)
+        Cm = K.dense(rng, (J, R), "dd", integers)
+        Dm = K.dense(rng, (Kd, R), "dd", integers)
+        tensors = {"B": B, "C": Cm, "D": Dm}
+        run = ob.RefRun("A(i, l) = B(i, j, k) * C(j, l) * D(k, l)", BATCHED_MTTKRP, f"x={grid[0]},y={grid[1]}",
+                        "dd", K.ref_inputs("spmttkrp", tensors)).ok()
+        _, want = run.output()
+        st_ref = run.stats()
+        dev = H.DeviceTensor.upload(ctx, B)
+        try:
+            Cd = torch.from_numpy(Cm.vals.copy()).cuda()
+            Dd = torch.from_numpy(Dm.vals.copy()).cuda()
+            A = torch.full((I * R,), float("nan"), dtype=torch.float64, device="cuda")
+            st = H.spmttkrp_batched(ctx, dev, Cd, Dd, R, A, grid)
+            got = A.cpu().numpy()
+            if integers:
+                assert np.array_equal(got, want)
+            else:
+                assert np.all(np.abs(got - want) <= 1e-10 * np.maximum(np.abs(want), 1e-300))
+            assert st.workers == st_ref["workers"] and st.work == st_ref["work"]
+            assert st.combines == st_ref["combines"] and st.imbalance == st_ref["imbalance"]
+        finally:
+            dev.close()

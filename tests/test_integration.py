@@ -73,6 +73,25 @@ def test_batched_spmm_plan_with_gpu_execute(gpu_lib, grid):
     assert ws["work"] == gs["work"] and ws["combines"] == gs["combines"] and ws["imbalance"] == gs["imbalance"]
 
 
+BATCHED_MTTKRP = ("divide(i, io, ii, M.x); divide(l, lo, li, M.y); reorder(io, lo, ii, j, k, li); "
+                  "distribute(io, M.x); distribute(lo, M.y); communicate({B}, io); communicate({A, C, D}, lo)")
+
+
+@pytest.mark.parametrize("grid", ["x=2,y=2", "x=3,y=2", "x=1,y=4"])
+def test_batched_spmttkrp_plan_with_gpu_execute(gpu_lib, grid):
+    """The two-loop batched SpMTTKRP plan (rows over x, rank columns over y)
+    through the adapter: output, per-worker work, imbalance."""
+    spec = KERNELS["spmttkrp"]
+    rng = np.random.default_rng(9)
+    t = K.instance("spmttkrp", rng, integers=True, rank=12)
+    args = (spec["expr"], BATCHED_MTTKRP, grid, "dd", ref_inputs("spmttkrp", t))
+    want = ob.RefRun(*args, mode="seq").ok()
+    got = ob.RefRun(*args, mode="gpu", lib=gpu_lib).ok()
+    assert np.array_equal(want.output()[1], got.output()[1])
+    ws, gs = want.stats(), got.stats()
+    assert ws["work"] == gs["work"] and ws["combines"] == gs["combines"] and ws["imbalance"] == gs["imbalance"]
+
+
 @pytest.mark.parametrize("kernel", ["spttv", "spmttkrp"])
 def test_sss_plan_with_gpu_execute(gpu_lib, kernel):
     spec = KERNELS[kernel]
