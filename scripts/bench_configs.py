@@ -33,11 +33,14 @@ ap.add_argument("--configs", default="c1,c2,c3,c4,c5")
 ap.add_argument("--scale", type=int, default=24)
 ap.add_argument("--sddmm-scale", type=int, default=24)
 ap.add_argument("--no-check", action="store_true")
+ap.add_argument("--no-reference", action="store_true",
+                help="skip the reference's own plan() + execute() timings (C1, C4)")
 args = ap.parse_args()
 
 import torch  # noqa: E402
 
 import oracle_bind as ob  # noqa: E402  (checker + CPU baseline only)
+import spd_kernels as K  # noqa: E402
 from paper_2207_13901_b200 import host as H  # noqa: E402
 
 dev = torch.device("cuda", 0)
@@ -101,6 +104,24 @@ def report(name, workload, flops, bytes_, ms, check, cpu_s, extra=None):
     print(json.dumps(line), flush=True)
 
 
+def ref_timings(kernel, sched, out_fmt, tensors, flops, pieces_list, gpu_out):
+    """The reference's own CPU path (oracle/_ref: plan() + execute() in par
+    mode, SURVEY 8d "CPU timing beside the GPU"): one run per colour count P
+    (its thread pool is min(cores, P), sim.cpp:960-961), output compared with
+    the GPU's at 1e-10."""
+    if args.no_reference:
+        return None
+    spec = K.KERNELS[kernel]
+    rows = []
+    for P in pieces_list:
+        run = ob.RefRun(spec["expr"], sched, P, out_fmt, tensors, mode="par").ok()
+        ex = run.exec_seconds()
+        rows.append({"pieces": P, "threads": min(CORES, P), "plan_s": run.plan_seconds(), "exec_s": ex,
+                     "gflops": flops / ex / 1e9 if ex else None,
+                     "matches_gpu": rel_ok(gpu_out, run.output()[1])})
+    return {"kind": "reference", "cpu": bench.cpu_model(), "runs": rows}
+
+
 def rel_ok(got, want, exact=False):
     got = np.asarray(got).reshape(-1)
     want = np.asarray(want).reshape(-1)
@@ -149,8 +170,12 @@ if "c1" in configs:
     want, _, _ = ob.spmv(rp, crd, vals, x, ob.partition_universe([rp], n, 1))
     cpu = time.time() - t0
     ok = args.no_check or (rel_ok(y_d.cpu().numpy(), want) and rel_ok(yg.cpu().numpy(), want))
+    Bh = H.SparseTensor.from_rowptrs((n, n), H.parse_format("ds"), [rp], [crd], vals)
+    xh = H.SparseTensor.from_parts((n,), H.parse_format("d"), [H.Level("d", dom=(n,))], x)
+    ref = ref_timings("spmv", K.ROW, "d", {"B": (Bh, "ds"), "c": (xh, "d")}, 2.0 * nnz,
+                      sorted({1, 2, 4, 8, CORES}), y_d.cpu().numpy())
     report("C1", "SpMV uniform 1M x 1M, 10M samples (%d nnz), row split" % nnz, 2.0 * nnz,
-           8 * (n + 1) + 16 * nnz + 8 * n + 8 * n, ms, ok, cpu, {"ms_cuda_graph": ms_graph})
+           8 * (n + 1) + 16 * nnz + 8 * n + 8 * n, ms, ok, cpu, {"ms_cuda_graph": ms_graph, "cpu_reference": ref})
 
 rm = None
 if any(c in configs for c in ("c2", "c3", "c5")):
@@ -238,9 +263,12 @@ if "c4" in configs:
     want, _, _ = ob.spttv(rp1, crd1, rp2, crd2, vals, c, ob.partition_nonzero([rp1, rp2], nnz, 1))
     cpu = time.time() - t0
     ok = args.no_check or (rel_ok(Av.cpu().numpy(), want) and rel_ok(Avg.cpu().numpy(), want))
+    ch = H.SparseTensor.from_parts((Kd,), H.parse_format("d"), [H.Level("d", dom=(Kd,))], c)
+    ref = ref_timings("spttv", K.KERNELS["spttv"]["nonzero"], "ds", {"B": (t, "dss"), "c": (ch, "d")}, 2.0 * nnz,
+                      sorted({8, CORES}), Av.cpu().numpy())
     report("C4-SpTTV", "SpTTV, %dx%dx%d power-law dss, %d nnz, %d fibres, nonzero split" % (I, J, Kd, nnz, F),
            2.0 * nnz, 8 * (I + 1) + 8 * F + 8 * (F + 1) + 16 * nnz + 8 * Kd + 8 * F, ms, ok, cpu,
-           {"ms_cuda_graph": ms_graph})
+           {"ms_cuda_graph": ms_graph, "cpu_reference": ref})
     R = 32
     Cm = bench.dense_vals(J * R, 47)
     Dm = bench.dense_vals(Kd * R, 48)
@@ -264,9 +292,14 @@ if "c4" in configs:
     want, _, _ = ob.spmttkrp(rp1, crd1, rp2, crd2, vals, Cm, Dm, R, ob.partition_nonzero([rp1, rp2], nnz, 1))
     cpu = time.time() - t0
     ok = args.no_check or (rel_ok(A_d.cpu().numpy(), want) and rel_ok(A_g.cpu().numpy(), want))
+    Ch = H.SparseTensor.from_parts((J, R), H.parse_format("dd"), [H.Level("d", dom=(J, R))], Cm)
+    Dh = H.SparseTensor.from_parts((Kd, R), H.parse_format("dd"), [H.Level("d", dom=(Kd, R))], Dm)
+    ref = ref_timings("spmttkrp", K.KERNELS["spmttkrp"]["nonzero"], "dd",
+                      {"B": (t, "dss"), "C": (Ch, "dd"), "D": (Dh, "dd")}, 3.0 * nnz * R, [CORES],
+                      A_d.cpu().numpy())
     report("C4-SpMTTKRP", "SpMTTKRP R=32, same tensor, nonzero split", 3.0 * nnz * R,
            8 * (I + 1) + 8 * F + 8 * (F + 1) + 16 * nnz + 8 * (J + Kd + I) * R, ms, ok, cpu,
-           {"ms_cuda_graph": ms_graph})
+           {"ms_cuda_graph": ms_graph, "cpu_reference": ref})
 
 if "c5" in configs:
     n, rp, crd, vals = rm
