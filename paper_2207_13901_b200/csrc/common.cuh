@@ -183,6 +183,14 @@ struct spd_tensor {
   // column is 0x80000000 | slot, its row read from a per-call compact copy
   // of the hot rows (hot_ids[slot] = column); built for one dense-row size.
   int32_t* crd32p = nullptr;  // plain int32 copy of the leaf crd (SpMM HOT == 3)
+  // Compacted-column index (SpMV over a wide x): the referenced columns of
+  // the leaf level renumbered densely in ascending order -- crdc[q] = rank of
+  // crd[q] among them, cref[r] = the column of rank r, nref of them -- so a
+  // per-call gather xc[r] = x[cref[r]] packs every x entry the leaf reads
+  // into nref * 8 bytes that stay L2-resident.
+  int32_t* crdc = nullptr;
+  int32_t* cref = nullptr;
+  int64_t nref = -1;
   int32_t* crd32x = nullptr;
   int32_t* crd32x_alloc = nullptr;
   int32_t* hot_ids = nullptr;
@@ -212,7 +220,7 @@ struct spd_context {
   bool colors_host_valid = false;
 
   std::vector<int64_t> last_work;    // per colour
-  spd::DeviceBuffer scratch[7];  // [6]: compact hot-row copy
+  spd::DeviceBuffer scratch[8];  // [6]: compact hot-row copy, [7]: compacted x (SpMV)
   int64_t persist_bytes = -1;        // L2 persisting set-aside (-1: not set up)
   spd::DeviceBuffer counters;        // small int64 device counters
   int64_t* pinned_counters = nullptr;

@@ -602,6 +602,11 @@ static void restage_piece(spd_context* ctx, spd_tensor* t, const int64_t* const*
   t->crd32x_rowbytes = 0;
   dev_free(ctx, t->crd32p);
   t->crd32p = nullptr;
+  dev_free(ctx, t->crdc);
+  t->crdc = nullptr;
+  dev_free(ctx, t->cref);
+  t->cref = nullptr;
+  t->nref = -1;
   stage_piece(ctx, t, pos_pairs[1], crd ? crd[1] : nullptr, vals, t->piece_split, false);
 }
 
@@ -777,6 +782,11 @@ int spd_tensor_restage(spd_context* ctx, spd_tensor* t, const int64_t* const* po
     t->crd32x_rowbytes = 0;
     dev_free(ctx, t->crd32p);
     t->crd32p = nullptr;
+    dev_free(ctx, t->crdc);
+    t->crdc = nullptr;
+    dev_free(ctx, t->cref);
+    t->cref = nullptr;
+    t->nref = -1;
     dev_free(ctx, t->jleaf);
     t->jleaf = nullptr;
     dev_free(ctx, t->leaf_rowptr);
@@ -870,6 +880,8 @@ int spd_tensor_destroy(spd_tensor* t) {
     dev_free(ctx, t->crd32h_alloc);
     dev_free(ctx, t->crd32x_alloc);
     dev_free(ctx, t->crd32p);
+    dev_free(ctx, t->crdc);
+    dev_free(ctx, t->cref);
     dev_free(ctx, t->hot_ids);
     dev_free(ctx, t->stage_pairs);
     dev_free(ctx, t->stage_flags);

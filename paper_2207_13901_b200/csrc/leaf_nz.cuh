@@ -272,7 +272,32 @@ __global__ void __launch_bounds__(kBlock, 5) k_spmv_nz(WalkGeom g, NzView z, con
 // issues ~300 when rows are ~10 long.  Chunk / colour records as k_spmv_nz.
 constexpr int kRowsLong = 48;
 
-__device__ __forceinline__ double row_dot_serial(const int64_t* __restrict__ crd, const double* __restrict__ vals,
+__device__ __forceinline__ int64_t ld_crd_hint(const int64_t* p, uint64_t pol) { return ld_i64_hint(p, pol); }
+__device__ __forceinline__ int64_t ld_crd_hint(const int32_t* p, uint64_t pol) { return ld_i32_hint(p, pol); }
+
+// Compacted-column index build (once per pattern) and the per-call gather.
+__global__ void k_ref_flags(const int32_t* __restrict__ counts, int64_t ncols, int32_t* __restrict__ flags) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncols; c += (int64_t)gridDim.x * blockDim.x)
+    flags[c] = counts[c] > 0 ? 1 : 0;
+}
+__global__ void k_ref_list(const int32_t* __restrict__ flags, const int32_t* __restrict__ rank, int64_t ncols,
+                           int32_t* __restrict__ cref) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < ncols; c += (int64_t)gridDim.x * blockDim.x)
+    if (flags[c]) cref[rank[c]] = (int32_t)c;
+}
+__global__ void k_crd_rank(const int64_t* __restrict__ crd, int64_t n, const int32_t* __restrict__ rank,
+                           int32_t* __restrict__ out) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x)
+    out[q] = rank[crd[q]];
+}
+__global__ void k_gather_ref(const double* __restrict__ x, const int32_t* __restrict__ cref, int64_t nref,
+                             double* __restrict__ xc) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nref; r += (int64_t)gridDim.x * blockDim.x)
+    xc[r] = __ldg(x + cref[r]);
+}
+
+template <typename CI>
+__device__ __forceinline__ double row_dot_serial(const CI* __restrict__ crd, const double* __restrict__ vals,
                                                  const double* __restrict__ x, int64_t a, int64_t b) {
   // L1-allocating loads: a lane walks consecutive positions of its row, so
   // the 32-byte sectors it touches are reused from L1 by its next loads
@@ -299,8 +324,8 @@ __device__ __forceinline__ double row_dot_serial(const int64_t* __restrict__ crd
   return sum;
 }
 
-template <int MINB>
-__global__ void __launch_bounds__(kBlock, MINB) k_spmv_rows(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
+template <int MINB, typename CI = int64_t>
+__global__ void __launch_bounds__(kBlock, MINB) k_spmv_rows(WalkGeom g, NzView z, const CI* __restrict__ crd,
                                                       const double* __restrict__ vals,
                                                       const double* __restrict__ x, double* __restrict__ y,
                                                       ChunkRecs rec, const int64_t* __restrict__ counters) {
@@ -347,7 +372,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmv_rows(WalkGeom g, NzView z
         const int64_t aa = __shfl_sync(FULL, a, t), bb = __shfl_sync(FULL, b, t);
         double part = 0.0;
         for (int64_t q = aa + lane; q <= bb; q += 32)
-          part += ld_f64_hint(vals + q, pol) * __ldg(x + ld_i64_hint(crd + q, pol));
+          part += ld_f64_hint(vals + q, pol) * __ldg(x + ld_crd_hint(crd + q, pol));
         part = warp_sum(part);
         if (lane == t) sum = part;
       }

@@ -915,6 +915,73 @@ static int hot_enabled() {
   return v;
 }
 
+// Compacted-column SpMV (SPD_XC: 1 auto, 0 off, 2 always): when x is wider
+// than a quarter of L2, the leaf reads x through a dense renumbering of the
+// referenced columns (crdc / cref, built once per pattern, cached on the
+// tensor) and a per-call packed copy xc, so the x gathers hit an L2-resident
+// array and the crd stream is int32.  Same positions, same order, same x
+// values: the sums are unchanged.  Whole tensors with < 2^31 columns.
+static int xc_mode() {
+  static int v = [] {
+    const char* e = getenv("SPD_XC");
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
+static bool xc_wanted(spd_context* ctx, const spd_tensor* B, int64_t ncols) {
+  const int m = xc_mode();
+  if (m == 0 || B->piece || ncols >= (int64_t(1) << 31)) return false;
+  if (m == 2) return true;
+  int l2 = 0;
+  SPD_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
+  return ncols * 8 > l2 / 4;
+}
+
+static void xc_index(spd_context* ctx, spd_tensor* t, int64_t ncols) {
+  if (t->nref >= 0) return;
+  const spd_level_store& L = t->levels.back();
+  const int64_t nnz = L.positions;
+  cudaStream_t s = ctx->stream;
+  const unsigned gc = (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(ncols, 256), 1), ctx->num_sms * 16);
+  const unsigned gq = (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(nnz, 256), 1), ctx->num_sms * 16);
+  int32_t *counts = nullptr, *flags = nullptr, *rank = nullptr;
+  const size_t cb = sizeof(int32_t) * (ncols > 0 ? ncols : 1);
+  SPD_CUDA(cudaMallocAsync((void**)&counts, cb, s));
+  SPD_CUDA(cudaMallocAsync((void**)&flags, cb, s));
+  SPD_CUDA(cudaMallocAsync((void**)&rank, cb, s));
+  SPD_CUDA(cudaMemsetAsync(counts, 0, cb, s));
+  SPD_CUDA(cudaMallocAsync((void**)&t->crdc, sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
+  int64_t nref = 0;
+  if (nnz > 0 && ncols > 0) {
+    k_col_count<<<gq, 256, 0, s>>>(L.crd, nnz, counts);
+    SPD_CHECK_LAUNCH();
+    k_ref_flags<<<gc, 256, 0, s>>>(counts, ncols, flags);
+    SPD_CHECK_LAUNCH();
+    size_t bytes = 0;
+    SPD_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, flags, rank, ncols, s));
+    void* tmp = ctx->scratch[5].reserve(bytes);
+    SPD_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, flags, rank, ncols, s));
+    int32_t last[2] = {0, 0};
+    SPD_CUDA(cudaMemcpyAsync(&last[0], rank + ncols - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SPD_CUDA(cudaMemcpyAsync(&last[1], flags + ncols - 1, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SPD_CUDA(cudaStreamSynchronize(s));
+    nref = (int64_t)last[0] + last[1];
+    SPD_CUDA(cudaMallocAsync((void**)&t->cref, sizeof(int32_t) * (nref > 0 ? nref : 1), s));
+    k_ref_list<<<gc, 256, 0, s>>>(flags, rank, ncols, t->cref);
+    SPD_CHECK_LAUNCH();
+    k_crd_rank<<<gq, 256, 0, s>>>(L.crd, nnz, rank, t->crdc);
+    SPD_CHECK_LAUNCH();
+    ctx->launches += 4;
+  } else {
+    SPD_CUDA(cudaMallocAsync((void**)&t->cref, sizeof(int32_t), s));
+  }
+  cudaFreeAsync(counts, s);
+  cudaFreeAsync(flags, s);
+  cudaFreeAsync(rank, s);
+  t->nref = nref;
+}
+
 // SpMV / SpTTV leaf choice: the lane-per-row kernel when the non-empty rows
 // are not long on average (SPD_SPMV_ROWS: 1 always, 0 never, unset: average
 // <= kRowsAvg positions per non-empty row), else the window-scan walk.
@@ -1291,7 +1358,6 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
         k_spmv_stage<4><<<grid4, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
       }
     } else if (spmv_rows_mode(nnz, z.m)) {  // short rows: a lane per row
-      static int grid = 0;
       // 6 CTAs/SM (40 registers, a few spills) wins on large matrices
       // (R-MAT leaf 1.11 -> 1.045 ms), 4 on small ones (C1 / C4)
       static int minb_env = [] {
@@ -1299,7 +1365,28 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
         return e ? atoi(e) : 0;
       }();
       const int minb = minb_env ? minb_env : (nnz >= (int64_t(1) << 26) ? 6 : 4);
-      if (minb == 6) {
+      const int64_t ncols = B->dims[B->mode_order[B->groups.back()[0]]];
+      if (a.op == Op::SpMV && xc_wanted(ctx, B, ncols)) {  // compacted x, int32 crd
+        spd_tensor* Bm = const_cast<spd_tensor*>(B);
+        xc_index(ctx, Bm, ncols);
+        double* xc = (double*)ctx->scratch[7].reserve(sizeof(double) * (Bm->nref > 0 ? Bm->nref : 1));
+        if (Bm->nref > 0) {
+          k_gather_ref<<<(unsigned)std::min<int64_t>(ceil_div(Bm->nref, 256), ctx->num_sms * 16), 256, 0, s>>>(
+              a.x, Bm->cref, Bm->nref, xc);
+          SPD_CHECK_LAUNCH();
+          launches++;
+        }
+#define SPD_ROWS_XC(MB)                                                                                   \
+  do {                                                                                                    \
+    static int gr = 0;                                                                                    \
+    if (!gr) gr = occupancy_grid(ctx, k_spmv_rows<MB, int32_t>);                                         \
+    k_spmv_rows<MB, int32_t><<<gr, kBlock, 0, s>>>(g, z, Bm->crdc, B->vals, xc, a.out, rec, col.counters); \
+  } while (0)
+        if (minb == 6) SPD_ROWS_XC(6);
+        else if (minb == 8) SPD_ROWS_XC(8);
+        else SPD_ROWS_XC(4);
+#undef SPD_ROWS_XC
+      } else if (minb == 6) {
         static int grid6 = 0;
         if (!grid6) grid6 = occupancy_grid(ctx, k_spmv_rows<6>);
         k_spmv_rows<6><<<grid6, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
@@ -1308,6 +1395,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
         if (!grid8) grid8 = occupancy_grid(ctx, k_spmv_rows<8>);
         k_spmv_rows<8><<<grid8, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
       } else {
+        static int grid = 0;
         if (!grid) grid = occupancy_grid(ctx, k_spmv_rows<4>);
         k_spmv_rows<4><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
       }

@@ -572,3 +572,35 @@ def test_spmttkrp_batched_two_dimensional_grid(ctx, grid, R):
             assert st.combines == st_ref["combines"] and st.imbalance == st_ref["imbalance"]
         finally:
             dev.close()
+
+
+@pytest.mark.parametrize("schedule,pieces", [("row", 1), ("row", 3), ("nonzero", 1), ("nonzero", 4)])
+def test_spmv_wide_x_compacted_columns(ctx, schedule, pieces):
+    """x wider than a quarter of L2 (5M columns, 40 MB) takes the compacted-
+    column path (referenced columns renumbered, x packed per call, int32
+    crd): same sums as the reference, also after a restage of a new pattern
+    (the renumbering is rebuilt)."""
+    import torch
+
+    from paper_2207_13901_b200 import host as H
+
+    rng = np.random.default_rng(31 + pieces)
+    n, m, nnz = 2000, 5_000_000, 60000
+    c = K.dense(rng, (m,), "d")
+    x = torch.from_numpy(c.vals.copy()).cuda()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    B1, B2 = _same_nnz_matrix(rng, n, m, nnz), _same_nnz_matrix(rng, n, m, nnz)
+    dev = H.DeviceTensor.upload(ctx, B1)
+    try:
+        for Bt in (B1, B2):
+            if Bt is B2:
+                dev.restage(B2)
+            from paper_2207_13901_b200.execute import partition
+
+            partition(ctx, dev, schedule, pieces)
+            st = H.spmv(ctx, dev, x, out, pieces=pieces)
+            want = oracle_execute("spmv", {"B": Bt, "c": c}, schedule, pieces)
+            assert_close("spmv", out.cpu().numpy(), want["out"], False)
+            assert st.work == want["work"] and st.combines == want["combines"]
+    finally:
+        dev.close()

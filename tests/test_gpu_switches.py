@@ -26,6 +26,8 @@ VARIANTS = [
     {"SPD_DYN": "0"},  # static grid stride for the N=32 SpMM leaf
     {"SPD_SPMMV": "0"},  # lane-per-column SpMM / SpMTTKRP walks for N != 32
     {"SPD_ZCONC": "0"},  # zero-fill before the leaf
+    {"SPD_XC": "2"},  # compacted-column SpMV on every matrix
+    {"SPD_XC": "0"},  # never (the wide-x test then reads x directly)
 ]
 
 
@@ -34,6 +36,6 @@ def test_switch_variant_parity(env):
     full = dict(os.environ, **env)
     r = subprocess.run(
         [sys.executable, "-m", "pytest", os.path.join(HERE, "test_gpu_parity.py"), "-m", "gpu", "-x", "-q",
-         "-p", "no:cacheprovider", "-k", "restatement_random or long_hub or widths or long_empty"],
+         "-p", "no:cacheprovider", "-k", "restatement_random or long_hub or widths or long_empty or wide_x or restage"],
         env=full, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
