@@ -439,11 +439,12 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmv_rows(WalkGeom g, NzView z
 constexpr int kStageWin = 256;
 constexpr int kStageLong = 32;
 
+template <int WIN>
 __device__ __forceinline__ void stage_products(const int64_t* __restrict__ crd, const double* __restrict__ vals,
                                                const double* __restrict__ x, int64_t w0, int wn,
                                                double* __restrict__ sp, uint64_t pol) {
   const int lane = lane_id();
-  constexpr int PER = kStageWin / 32;
+  constexpr int PER = WIN / 32;
   int64_t k[PER];
   double v[PER];
 #pragma unroll
@@ -462,7 +463,7 @@ __device__ __forceinline__ void stage_products(const int64_t* __restrict__ crd, 
   }
 }
 
-template <int MINB>
+template <int MINB, int WIN = kStageWin>
 __global__ void __launch_bounds__(kBlock, MINB) k_spmv_stage(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
                                                       const double* __restrict__ vals,
                                                       const double* __restrict__ x, double* __restrict__ y,
@@ -470,7 +471,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmv_stage(WalkGeom g, NzView 
   const int lane = lane_id();
   const int64_t begin = counters[1], end = counters[2];
   const uint64_t pol = l2_policy_evict_first();
-  __shared__ double s_prod[kBlock / 32][kStageWin];
+  __shared__ double s_prod[kBlock / 32][WIN];
   double* sp = s_prod[threadIdx.x >> 5];
   for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
     const ChunkInfo ci = chunk_info(g, v, begin);
@@ -507,9 +508,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmv_stage(WalkGeom g, NzView 
       const int64_t hi = __shfl_sync(FULL, b, (int)min((int64_t)31, ic1 - g0));
       const bool lng = act && b - a + 1 > kStageLong;
       double sum = 0.0;
-      for (int64_t w0 = lo; w0 <= hi; w0 += kStageWin) {
-        const int wn = (int)min((int64_t)kStageWin, hi - w0 + 1);
-        stage_products(crd, vals, x, w0, wn, sp, pol);
+      for (int64_t w0 = lo; w0 <= hi; w0 += WIN) {
+        const int wn = (int)min((int64_t)WIN, hi - w0 + 1);
+        stage_products<WIN>(crd, vals, x, w0, wn, sp, pol);
         __syncwarp();
         const int64_t wl = w0 + wn - 1;
         if (act && !lng && a <= wl && b >= w0) {  // short row: serial, stored order

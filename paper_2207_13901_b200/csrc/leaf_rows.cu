@@ -1344,19 +1344,22 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
         const char* e = getenv("SPD_STAGE_MINB");
         return e ? atoi(e) : 4;
       }();
-      if (minb_env == 6) {
-        static int grid6 = 0;
-        if (!grid6) grid6 = occupancy_grid(ctx, k_spmv_stage<6>);
-        k_spmv_stage<6><<<grid6, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
-      } else if (minb_env == 3) {
-        static int grid3 = 0;
-        if (!grid3) grid3 = occupancy_grid(ctx, k_spmv_stage<3>);
-        k_spmv_stage<3><<<grid3, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+      static int win_env = [] {
+        const char* e = getenv("SPD_STAGE_WIN");
+        return e ? atoi(e) : 256;
+      }();
+#define SPD_STAGE(MB, WN)                                                                                \
+  do {                                                                                                   \
+    static int gr = 0;                                                                                   \
+    if (!gr) gr = occupancy_grid(ctx, k_spmv_stage<MB, WN>);                                            \
+    k_spmv_stage<MB, WN><<<gr, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters); \
+  } while (0)
+      if (win_env == 128) {
+        if (minb_env == 8) SPD_STAGE(8, 128); else if (minb_env == 6) SPD_STAGE(6, 128); else SPD_STAGE(4, 128);
       } else {
-        static int grid4 = 0;
-        if (!grid4) grid4 = occupancy_grid(ctx, k_spmv_stage<4>);
-        k_spmv_stage<4><<<grid4, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+        if (minb_env == 6) SPD_STAGE(6, 256); else if (minb_env == 3) SPD_STAGE(3, 256); else SPD_STAGE(4, 256);
       }
+#undef SPD_STAGE
     } else if (spmv_rows_mode(nnz, z.m)) {  // short rows: a lane per row
       // 6 CTAs/SM (40 registers, a few spills) wins on large matrices
       // (R-MAT leaf 1.11 -> 1.045 ms), 4 on small ones (C1 / C4)
