@@ -188,7 +188,8 @@ struct spd_tensor {
   // crd[q] among them, cref[r] = the column of rank r, nref of them -- so a
   // per-call gather xc[r] = x[cref[r]] packs every x entry the leaf reads
   // into nref * 8 bytes that stay L2-resident.
-  int32_t* crdc = nullptr;
+  int32_t* crdc = nullptr;        // indexed by global position (offset for pieces)
+  int32_t* crdc_alloc = nullptr;  // allocation behind crdc
   int32_t* cref = nullptr;
   int64_t nref = -1;
   int32_t* crd32x = nullptr;

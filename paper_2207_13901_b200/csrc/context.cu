@@ -602,8 +602,8 @@ static void restage_piece(spd_context* ctx, spd_tensor* t, const int64_t* const*
   t->crd32x_rowbytes = 0;
   dev_free(ctx, t->crd32p);
   t->crd32p = nullptr;
-  dev_free(ctx, t->crdc);
-  t->crdc = nullptr;
+  dev_free(ctx, t->crdc_alloc);
+  t->crdc_alloc = t->crdc = nullptr;
   dev_free(ctx, t->cref);
   t->cref = nullptr;
   t->nref = -1;
@@ -782,8 +782,8 @@ int spd_tensor_restage(spd_context* ctx, spd_tensor* t, const int64_t* const* po
     t->crd32x_rowbytes = 0;
     dev_free(ctx, t->crd32p);
     t->crd32p = nullptr;
-    dev_free(ctx, t->crdc);
-    t->crdc = nullptr;
+    dev_free(ctx, t->crdc_alloc);
+    t->crdc_alloc = t->crdc = nullptr;
     dev_free(ctx, t->cref);
     t->cref = nullptr;
     t->nref = -1;
@@ -880,7 +880,7 @@ int spd_tensor_destroy(spd_tensor* t) {
     dev_free(ctx, t->crd32h_alloc);
     dev_free(ctx, t->crd32x_alloc);
     dev_free(ctx, t->crd32p);
-    dev_free(ctx, t->crdc);
+    dev_free(ctx, t->crdc_alloc);
     dev_free(ctx, t->cref);
     dev_free(ctx, t->hot_ids);
     dev_free(ctx, t->stage_pairs);

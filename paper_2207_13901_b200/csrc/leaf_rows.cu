@@ -920,7 +920,8 @@ static int hot_enabled() {
 // referenced columns (crdc / cref, built once per pattern, cached on the
 // tensor) and a per-call packed copy xc, so the x gathers hit an L2-resident
 // array and the crd stream is int32.  Same positions, same order, same x
-// values: the sums are unchanged.  Whole tensors with < 2^31 columns.
+// values: the sums are unchanged.  < 2^31 columns; for a piece the index
+// covers the piece's positions (its referenced columns only).
 static int xc_mode() {
   static int v = [] {
     const char* e = getenv("SPD_XC");
@@ -931,7 +932,7 @@ static int xc_mode() {
 
 static bool xc_wanted(spd_context* ctx, const spd_tensor* B, int64_t ncols) {
   const int m = xc_mode();
-  if (m == 0 || B->piece || ncols >= (int64_t(1) << 31)) return false;
+  if (m == 0 || ncols >= (int64_t(1) << 31)) return false;
   if (m == 2) return true;
   int l2 = 0;
   SPD_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
@@ -941,7 +942,8 @@ static bool xc_wanted(spd_context* ctx, const spd_tensor* B, int64_t ncols) {
 static void xc_index(spd_context* ctx, spd_tensor* t, int64_t ncols) {
   if (t->nref >= 0) return;
   const spd_level_store& L = t->levels.back();
-  const int64_t nnz = L.positions;
+  const int64_t lo = t->piece ? t->piece_lo : 0;
+  const int64_t nnz = t->piece ? t->piece_hi - t->piece_lo + 1 : L.positions;
   cudaStream_t s = ctx->stream;
   const unsigned gc = (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(ncols, 256), 1), ctx->num_sms * 16);
   const unsigned gq = (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(nnz, 256), 1), ctx->num_sms * 16);
@@ -951,10 +953,11 @@ static void xc_index(spd_context* ctx, spd_tensor* t, int64_t ncols) {
   SPD_CUDA(cudaMallocAsync((void**)&flags, cb, s));
   SPD_CUDA(cudaMallocAsync((void**)&rank, cb, s));
   SPD_CUDA(cudaMemsetAsync(counts, 0, cb, s));
-  SPD_CUDA(cudaMallocAsync((void**)&t->crdc, sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
+  SPD_CUDA(cudaMallocAsync((void**)&t->crdc_alloc, sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
+  t->crdc = t->crdc_alloc - lo;  // indexed by global position
   int64_t nref = 0;
   if (nnz > 0 && ncols > 0) {
-    k_col_count<<<gq, 256, 0, s>>>(L.crd, nnz, counts);
+    k_col_count<<<gq, 256, 0, s>>>(L.crd + lo, nnz, counts);
     SPD_CHECK_LAUNCH();
     k_ref_flags<<<gc, 256, 0, s>>>(counts, ncols, flags);
     SPD_CHECK_LAUNCH();
@@ -970,7 +973,7 @@ static void xc_index(spd_context* ctx, spd_tensor* t, int64_t ncols) {
     SPD_CUDA(cudaMallocAsync((void**)&t->cref, sizeof(int32_t) * (nref > 0 ? nref : 1), s));
     k_ref_list<<<gc, 256, 0, s>>>(flags, rank, ncols, t->cref);
     SPD_CHECK_LAUNCH();
-    k_crd_rank<<<gq, 256, 0, s>>>(L.crd, nnz, rank, t->crdc);
+    k_crd_rank<<<gq, 256, 0, s>>>(L.crd + lo, nnz, rank, t->crdc_alloc);
     SPD_CHECK_LAUNCH();
     ctx->launches += 4;
   } else {
