@@ -116,6 +116,14 @@ def main():
                 first=rank, count=1, pieces=world)
         ga = [torch.zeros_like(A) for _ in range(world)]
         dist.all_gather(ga, A)
+        # SpMV on the piece (compacted-column index over the piece's positions
+        # when SPD_XC=2)
+        cv = K.dense(rng, (m,), "d", False)
+        yv = torch.zeros(n, dtype=torch.float64, device=dev)
+        (H.partition_universe(ctx, piece, world) if schedule == "row" else H.partition_nonzero(ctx, piece, 1, world))
+        H.spmv(ctx, piece, torch.from_numpy(cv.vals).to(dev), yv, first=rank, count=1, pieces=world)
+        gy = [torch.zeros_like(yv) for _ in range(world)]
+        dist.all_gather(gy, yv)
         spans = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in range(world)]
         dist.all_gather(spans, torch.tensor([lo, hi], dtype=torch.int64, device=dev))
         if rank == 0:
@@ -128,9 +136,13 @@ def main():
                 gs[a:b + 1] = ga[r].cpu().numpy()[a:b + 1]
             wsd = np.asarray(oracle_exec.oracle_execute("sddmm", {"B": B, "C": Cs, "D": Ds}, schedule, world)["out"])
             ok2 = np.all(np.abs(gs - wsd) <= 1e-10 * np.maximum(np.abs(wsd), 1e-300))
+            goty = assemble([x.cpu().numpy().reshape(n, 1) for x in gy], W, 1, n).reshape(-1)
+            wy = np.asarray(oracle_exec.oracle_execute("spmv", {"B": B, "c": cv}, schedule, world)["out"]).reshape(-1)
+            ok3 = np.all(np.abs(goty - wy) <= 1e-10 * np.maximum(np.abs(wy), 1e-300))
             print(f"[mgpu world={world}] placed {schedule}: spmm {'OK' if ok else 'MISMATCH'} sddmm "
-                  f"{'OK' if ok2 else 'MISMATCH'} piece=[{lo},{hi}] bytes_in={nbytes}", flush=True)
-            failures += (0 if ok else 1) + (0 if ok2 else 1)
+                  f"{'OK' if ok2 else 'MISMATCH'} spmv {'OK' if ok3 else 'MISMATCH'} piece=[{lo},{hi}] "
+                  f"bytes_in={nbytes}", flush=True)
+            failures += (0 if ok else 1) + (0 if ok2 else 1) + (0 if ok3 else 1)
         piece.close()
         if whole is not None:
             whole.close()
