@@ -334,7 +334,9 @@ int spd_last_work(spd_context* ctx, int64_t* work, int64_t pieces);
 /* CUDA graphs: capture the ops enqueued on `ctx` between begin and end
  * (e.g. spd_partition_* with colors_out NULL + a leaf op with stats NULL)
  * and replay them with one launch.  The context must own an explicit
- * stream.  Ops that need a host read-back fail the capture. */
+ * stream.  Ops that need a host read-back fail the capture, and so does the
+ * first use of a derived per-tensor index that sizes itself on the host
+ * (the compacted-column SpMV index): run the op once before capturing. */
 typedef struct spd_graph spd_graph;
 int spd_capture_begin(spd_context* ctx);
 int spd_capture_end(spd_context* ctx, spd_graph** out);
