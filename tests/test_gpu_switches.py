@@ -36,6 +36,6 @@ def test_switch_variant_parity(env):
     full = dict(os.environ, **env)
     r = subprocess.run(
         [sys.executable, "-m", "pytest", os.path.join(HERE, "test_gpu_parity.py"), "-m", "gpu", "-x", "-q",
-         "-p", "no:cacheprovider", "-k", "restatement_random or long_hub or widths or long_empty or wide_x or restage"],
+         "-p", "no:cacheprovider", "-k", "restatement_random or long_hub or widths or long_empty or wide_x or restage or degenerate or golden"],
         env=full, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
