@@ -1127,7 +1127,10 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   // Positions per chunk: ~256 KB of operand traffic per warp-chunk for the
   // column kernels, 2048 positions for the scalar ones.
   // (the lane-per-row SpMV kernel balances small problems better with 1024)
+  // SpTTV over CSF fibres (~1.5 positions per fibre on C4): 512-position
+  // chunks and 6 CTAs/SM (0.190 -> 0.160 ms, profiles/README.md)
   g.CH = (a.op == Op::SpMV || a.op == Op::SpTTV) ? (nnz < (int64_t(1) << 26) ? 1024 : 2048) : 1024;
+  if (a.op == Op::SpTTV && nnz < (int64_t(1) << 26)) g.CH = 512;
   {
     static int64_t ch_override = [] {
       const char* e = getenv("SPD_CH");
@@ -1370,7 +1373,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
         const char* e = getenv("SPD_SPMV_MINB");
         return e ? atoi(e) : 0;
       }();
-      const int minb = minb_env ? minb_env : (nnz >= (int64_t(1) << 26) ? 6 : 4);
+      const int minb = minb_env ? minb_env : (nnz >= (int64_t(1) << 26) || a.op == Op::SpTTV ? 6 : 4);
       const int64_t ncols = B->dims[B->mode_order[B->groups.back()[0]]];
       if (a.op == Op::SpMV && xc_wanted(ctx, B, ncols)) {  // compacted x, int32 crd
         spd_tensor* Bm = const_cast<spd_tensor*>(B);
