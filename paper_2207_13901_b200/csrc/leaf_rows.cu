@@ -1136,7 +1136,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
       const char* e = getenv("SPD_CH");
       return e ? atoll(e) : 0;
     }();
-    if (ch_override >= 32 && a.op == Op::SpMM) g.CH = ch_override;
+    if (ch_override >= 32 && (a.op == Op::SpMM || a.op == Op::SpMTTKRP)) g.CH = ch_override;
     static int64_t ch_spmv = [] {
       const char* e = getenv("SPD_CH_SPMV");
       return e ? atoll(e) : 0;
