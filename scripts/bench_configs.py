@@ -40,7 +40,7 @@ args = ap.parse_args()
 import torch  # noqa: E402
 
 import oracle_bind as ob  # noqa: E402  (checker + CPU baseline only)
-import spd_kernels as K  # noqa: E402
+import spd_kernels as SK  # noqa: E402
 from paper_2207_13901_b200 import host as H  # noqa: E402
 
 dev = torch.device("cuda", 0)
@@ -111,7 +111,7 @@ def ref_timings(kernel, sched, out_fmt, tensors, flops, pieces_list, gpu_out):
     the GPU's at 1e-10."""
     if args.no_reference:
         return None
-    spec = K.KERNELS[kernel]
+    spec = SK.KERNELS[kernel]
     rows = []
     for P in pieces_list:
         run = ob.RefRun(spec["expr"], sched, P, out_fmt, tensors, mode="par").ok()
@@ -172,7 +172,7 @@ if "c1" in configs:
     ok = args.no_check or (rel_ok(y_d.cpu().numpy(), want) and rel_ok(yg.cpu().numpy(), want))
     Bh = H.SparseTensor.from_rowptrs((n, n), H.parse_format("ds"), [rp], [crd], vals)
     xh = H.SparseTensor.from_parts((n,), H.parse_format("d"), [H.Level("d", dom=(n,))], x)
-    ref = ref_timings("spmv", K.ROW, "d", {"B": (Bh, "ds"), "c": (xh, "d")}, 2.0 * nnz,
+    ref = ref_timings("spmv", SK.ROW, "d", {"B": (Bh, "ds"), "c": (xh, "d")}, 2.0 * nnz,
                       sorted({1, 2, 4, 8, CORES}), y_d.cpu().numpy())
     report("C1", "SpMV uniform 1M x 1M, 10M samples (%d nnz), row split" % nnz, 2.0 * nnz,
            8 * (n + 1) + 16 * nnz + 8 * n + 8 * n, ms, ok, cpu, {"ms_cuda_graph": ms_graph, "cpu_reference": ref})
@@ -264,7 +264,7 @@ if "c4" in configs:
     cpu = time.time() - t0
     ok = args.no_check or (rel_ok(Av.cpu().numpy(), want) and rel_ok(Avg.cpu().numpy(), want))
     ch = H.SparseTensor.from_parts((Kd,), H.parse_format("d"), [H.Level("d", dom=(Kd,))], c)
-    ref = ref_timings("spttv", K.KERNELS["spttv"]["nonzero"], "ds", {"B": (t, "dss"), "c": (ch, "d")}, 2.0 * nnz,
+    ref = ref_timings("spttv", SK.KERNELS["spttv"]["nonzero"], "ds", {"B": (t, "dss"), "c": (ch, "d")}, 2.0 * nnz,
                       sorted({8, CORES}), Av.cpu().numpy())
     report("C4-SpTTV", "SpTTV, %dx%dx%d power-law dss, %d nnz, %d fibres, nonzero split" % (I, J, Kd, nnz, F),
            2.0 * nnz, 8 * (I + 1) + 8 * F + 8 * (F + 1) + 16 * nnz + 8 * Kd + 8 * F, ms, ok, cpu,
@@ -294,7 +294,7 @@ if "c4" in configs:
     ok = args.no_check or (rel_ok(A_d.cpu().numpy(), want) and rel_ok(A_g.cpu().numpy(), want))
     Ch = H.SparseTensor.from_parts((J, R), H.parse_format("dd"), [H.Level("d", dom=(J, R))], Cm)
     Dh = H.SparseTensor.from_parts((Kd, R), H.parse_format("dd"), [H.Level("d", dom=(Kd, R))], Dm)
-    ref = ref_timings("spmttkrp", K.KERNELS["spmttkrp"]["nonzero"], "dd",
+    ref = ref_timings("spmttkrp", SK.KERNELS["spmttkrp"]["nonzero"], "dd",
                       {"B": (t, "dss"), "C": (Ch, "dd"), "D": (Dh, "dd")}, 3.0 * nnz * R, [CORES],
                       A_d.cpu().numpy())
     report("C4-SpMTTKRP", "SpMTTKRP R=32, same tensor, nonzero split", 3.0 * nnz * R,
