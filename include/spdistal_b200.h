@@ -153,6 +153,17 @@ int spd_tensor_repartition(spd_context* ctx, const spd_tensor* piece, int need_s
  * compute partition on ctx. */
 int spd_ledger_bytes(spd_context* ctx, const spd_tensor* t, int need_split, int held_split,
                      int64_t pieces, int64_t* bytes_out);
+/* The ledger's primitive for arbitrary placements: missing_count of
+ * transfer_bytes (sim.cpp:76-84, 134-147) evaluated on the GPU for `npairs`
+ * pairs of sorted, duplicate-free int64 index sets in host memory --
+ * missing[p] = |{ i in needed[p] : i not in held[p] }|.  The integration
+ * adapter feeds it the needed sets of every (worker, tensor, region) of a
+ * plan and the Residency's held sets, so execute_gpu's bytes_by_tensor is
+ * the reference's ledger (replaces the accounting loop of execute,
+ * sim.cpp:868-887). */
+int spd_ledger_missing(spd_context* ctx, int64_t npairs, const int64_t* const* needed,
+                       const int64_t* n_needed, const int64_t* const* held, const int64_t* n_held,
+                       int64_t* missing);
 /* This GPU's piece of a CSR-like ("ds") matrix staged from host arrays: the
  * whole pos level (pairs, O(rows)) is uploaded, converted and checked, the
  * compute partition (split 1 = rows, 2 = nonzeros; spd_partition_universe /

@@ -5,7 +5,9 @@
 // reference library.  See INTEGRATION.md.
 //
 //   dspar::ExecResult dspar_gpu::execute_gpu(const Plan&, const TensorSet&,
-//                                            const MachineGrid&)
+//                                            const MachineGrid&, const Residency&)
+//
+// (execute()'s signature, sim.hpp:121-122, minus the ExecMode it replaces)
 //
 // * pattern-matches plan.stmt/formats against the six statements the backend
 //   implements and raises ValidationError("unsupported on gpu: ...") for
@@ -17,7 +19,9 @@
 //   plan.loops[0].position_space) and cross-checks the GPU colour bounds
 //   against plan.loops[0].color_bounds (a mismatch is a logic_error);
 // * runs the leaf + deterministic combine and rebuilds the output with
-//   SparseTensor::from_parts, so ExecResult / Stats are drop-in.
+//   SparseTensor::from_parts, so ExecResult / Stats are drop-in: per-worker
+//   work through tuple_worker, imbalance over every worker of the machine,
+//   and bytes_by_tensor from the Residency (the reference's ledger).
 #include <algorithm>
 #include <cstring>
 #include <map>
@@ -88,27 +92,165 @@ std::string kernel_of(const Plan& plan) {
     for (LevelKind x : f.kinds) k += x == LevelKind::Dense ? 'd' : 's';
     return k;
   };
+  // The kernels read every operand in mode order: a transposed storage order
+  // (CSC 'ds:1,0', column-major 'dd:1,0') is unsupported, except SDDMM's D,
+  // whose strides are passed explicitly, and SpAdd3, whose three operands and
+  // output only need to share one storage order (the union is per level).
+  auto ident = [&](const std::string& n) {
+    const auto& mo = plan.formats.at(n).mode_order;
+    for (size_t k = 0; k < mo.size(); k++)
+      if (mo[k] != static_cast<int>(k)) return false;
+    return true;
+  };
+  auto unsupported = [&](const std::string& why) { return ValidationError("unsupported on gpu: " + why + ": " + s); };
   const auto& terms = plan.stmt.terms;
   const auto& lhs = plan.stmt.lhs;
   if (terms.size() == 3 && lhs.vars.size() == 2) {
     for (const auto& t : terms)
-      if (t.size() != 1 || fmt(t[0].tensor) != "ds") throw ValidationError("unsupported on gpu: " + s);
+      if (t.size() != 1 || fmt(t[0].tensor) != "ds") throw unsupported("SpAdd3 needs three ds operands");
+    for (const auto& t : terms)
+      if (plan.formats.at(t[0].tensor).mode_order != plan.formats.at(lhs.tensor).mode_order)
+        throw unsupported("SpAdd3 operands and output must share one storage order");
     return "spadd3";
   }
-  if (terms.size() != 1) throw ValidationError("unsupported on gpu: " + s);
+  if (terms.size() != 1) throw unsupported("statement");
   const auto& t = terms[0];
+  std::string k;
   if (t.size() == 2 && lhs.vars.size() == 1 && fmt(t[0].tensor) == "ds" && fmt(t[1].tensor) == "d")
-    return "spmv";
-  if (t.size() == 2 && lhs.vars.size() == 2 && fmt(t[0].tensor) == "ds" && fmt(t[1].tensor) == "dd" &&
-      fmt(lhs.tensor) == "dd")
-    return "spmm";
-  if (t.size() == 3 && fmt(t[0].tensor) == "ds" && fmt(lhs.tensor) == "ds") return "sddmm";
-  const bool csf = fmt(t[0].tensor) == "dss" || fmt(t[0].tensor) == "sss";
-  if (t.size() == 2 && csf && fmt(t[1].tensor) == "d") return "spttv";
-  if (t.size() == 3 && csf && fmt(lhs.tensor) == "dd") return "spmttkrp";
-  throw ValidationError("unsupported on gpu: " + s);
+    k = "spmv";
+  else if (t.size() == 2 && lhs.vars.size() == 2 && fmt(t[0].tensor) == "ds" && fmt(t[1].tensor) == "dd" &&
+           fmt(lhs.tensor) == "dd")
+    k = "spmm";
+  else if (t.size() == 3 && fmt(t[0].tensor) == "ds" && fmt(lhs.tensor) == "ds")
+    k = "sddmm";
+  else {
+    const bool csf = fmt(t[0].tensor) == "dss" || fmt(t[0].tensor) == "sss";
+    if (t.size() == 2 && csf && fmt(t[1].tensor) == "d") k = "spttv";
+    else if (t.size() == 3 && csf && fmt(lhs.tensor) == "dd") k = "spmttkrp";
+    else throw unsupported("statement");
+  }
+  for (size_t a = 0; a < t.size(); a++)
+    if (!(k == "sddmm" && a == 2) && !ident(t[a].tensor)) throw unsupported("transposed storage of " + t[a].tensor);
+  if (!ident(lhs.tensor)) throw unsupported("transposed storage of " + lhs.tensor);
+  return k;
 }
 
+
+// One task per colour tuple (loop_tuples, sim.cpp:519-533), mapped to its
+// worker like tuple_worker (sim.cpp:535-544) and ordered by worker id as
+// execute() orders them (sim.cpp:843-847).
+struct Task {
+  std::vector<int64_t> colors;
+  int64_t wid = 0;
+};
+
+std::vector<Task> tasks_of(const Plan& plan, const MachineGrid& machine) {
+  std::vector<std::vector<int64_t>> tuples{{}};
+  for (const auto& loop : plan.loops) {
+    std::vector<std::vector<int64_t>> next;
+    for (const auto& t : tuples)
+      for (int64_t c = 0; c < loop.pieces; c++) {
+        auto e = t;
+        e.push_back(c);
+        next.push_back(std::move(e));
+      }
+    tuples = std::move(next);
+  }
+  std::vector<Task> tasks;
+  for (auto& colors : tuples) {
+    std::vector<int64_t> coords(machine.rank(), 0);
+    for (size_t k = 0; k < plan.loops.size(); k++) coords[machine.dim_index(plan.loops[k].machine_dim)] = colors[k];
+    tasks.push_back(Task{std::move(colors), machine.worker_id(coords)});
+  }
+  std::stable_sort(tasks.begin(), tasks.end(), [](const Task& a, const Task& b) { return a.wid < b.wid; });
+  return tasks;
+}
+
+// Stats of one execute (sim.cpp:824-829, 1000-1005): per-worker work written
+// task by task in worker order (a later task of the same worker overwrites,
+// as execute does), the communication ledger (bytes_by_tensor), imbalance over
+// every worker of the machine.  `task_work[k]` is the work of tasks[k].
+//
+// Ledger (sim.cpp:851-887): a tensor's needed sets at a task are the full
+// sets, or the intersection of its bundle colour sets over the loops up to
+// its communicate site (worker_needed_sets, sim.cpp:505-516); bytes are the
+// needed entries missing from the worker's Residency sets -- 16 B per pos
+// range, 8 B per crd, 8 B per val (sim.hpp:21-23, transfer_bytes :134-147).
+// The set construction is the reference's own bookkeeping (full_sets,
+// bundle_color_sets, intersect_sets from sim.hpp); the per-entry membership
+// counting runs on the GPU (spd_ledger_missing).
+Stats make_stats(spd_context* ctx, const Plan& plan, const TensorSet& tensors, const MachineGrid& machine,
+                 const Residency& residency, const std::vector<Task>& tasks, const std::vector<int64_t>& task_work) {
+  Stats st;
+  st.workers = machine.total_workers();
+  st.per_worker.resize(static_cast<size_t>(st.workers));
+  const auto names = plan.stmt.tensor_names();
+  for (auto& w : st.per_worker)
+    for (const auto& n : names) w.bytes_by_tensor[n] = 0;
+  std::map<std::string, int> site;
+  for (const auto& c : plan.root_communicates) site[c.tensor] = -1;
+  for (size_t k = 0; k < plan.loops.size(); k++)
+    for (const auto& c : plan.loops[k].communicates) site[c.tensor] = static_cast<int>(k);
+
+  // every (needed, held) set pair of every (task, tensor), weighted
+  std::vector<RegionIndexSets> keep_needed;
+  keep_needed.reserve(tasks.size() * names.size());
+  struct Pair {
+    const std::vector<int64_t>* need;
+    const std::vector<int64_t>* held;
+    int64_t weight;
+    size_t task;
+    std::string name;
+  };
+  std::vector<Pair> pairs;
+  for (size_t k = 0; k < tasks.size(); k++) {
+    for (const auto& name : names) {
+      auto rit = residency.tensors.find(name);
+      if (rit == residency.tensors.end()) continue;  // no declared placement: resident, 0 bytes
+      const SparseTensor& t = tensors.at(name);
+      RegionIndexSets needed = full_sets(t);
+      auto sit = site.find(name);
+      if (sit != site.end() && sit->second >= 0)
+        for (int l = 0; l <= sit->second; l++) {
+          auto b = plan.loops[l].bundle_of.find(name);
+          if (b == plan.loops[l].bundle_of.end()) continue;
+          needed = intersect_sets(needed, bundle_color_sets(plan.bundles[b->second], tasks[k].colors[l]));
+        }
+      keep_needed.push_back(std::move(needed));
+      const RegionIndexSets& nd = keep_needed.back();
+      const RegionIndexSets& held = rit->second.at(static_cast<size_t>(tasks[k].wid));
+      for (size_t l = 0; l < nd.levels.size(); l++) {
+        pairs.push_back({&nd.levels[l].pos, &held.levels[l].pos, kRangeBytes, k, name});
+        pairs.push_back({&nd.levels[l].crd, &held.levels[l].crd, kCoordBytes, k, name});
+      }
+      pairs.push_back({&nd.vals, &held.vals, kScalarBytes, k, name});
+    }
+  }
+  std::vector<int64_t> missing(pairs.size(), 0);
+  if (!pairs.empty()) {
+    std::vector<const int64_t*> np, hp;
+    std::vector<int64_t> nn, hn;
+    for (const auto& p : pairs) {
+      np.push_back(p.need->data());
+      nn.push_back(static_cast<int64_t>(p.need->size()));
+      hp.push_back(p.held->data());
+      hn.push_back(static_cast<int64_t>(p.held->size()));
+    }
+    check(spd_ledger_missing(ctx, static_cast<int64_t>(pairs.size()), np.data(), nn.data(), hp.data(), hn.data(),
+                             missing.data()));
+  }
+  std::vector<std::map<std::string, int64_t>> task_bytes(tasks.size());
+  for (size_t i = 0; i < pairs.size(); i++) task_bytes[pairs[i].task][pairs[i].name] += missing[i] * pairs[i].weight;
+  for (size_t k = 0; k < tasks.size(); k++) {
+    auto& w = st.per_worker[static_cast<size_t>(tasks[k].wid)];
+    w.work = task_work[k];
+    for (const auto& n : names) w.bytes_by_tensor[n] = task_bytes[k].count(n) ? task_bytes[k][n] : 0;
+  }
+  int64_t total = 0, mx = 0;
+  for (const auto& w : st.per_worker) total += w.work, mx = std::max(mx, w.work);
+  st.imbalance = total == 0 ? 1.0 : static_cast<double>(mx) * static_cast<double>(st.workers) / static_cast<double>(total);
+  return st;
+}
 }  // namespace
 
 // SpDISTAL-Batched SpMM: loop 0 divides the rows of B
@@ -119,7 +261,7 @@ std::string kernel_of(const Plan& plan) {
 // same shape: rows i over loop 0, the rank columns l of C, D and A over loop
 // 1, spd_spmttkrp on the slabs of both factors.
 ExecResult execute_batched(const Plan& plan, const TensorSet& tensors, const MachineGrid& machine,
-                           const std::string& kernel) {
+                           const Residency& residency, const std::string& kernel) {
   const PlanLoop& lx = plan.loops[0];
   const PlanLoop& ly = plan.loops[1];
   const auto& t = plan.stmt.terms[0];
@@ -142,25 +284,23 @@ ExecResult execute_batched(const Plan& plan, const TensorSet& tensors, const Mac
   }
   std::vector<double> out(static_cast<size_t>(n * N), 0.0);
   ExecResult r;
-  r.stats.workers = machine.total_workers();
-  r.stats.per_worker.resize(r.stats.workers);
-  for (auto& w : r.stats.per_worker)
-    for (const auto& nm : plan.stmt.tensor_names()) w.bytes_by_tensor[nm] = 0;
+  std::vector<std::vector<int64_t>> work_xy(static_cast<size_t>(ly.pieces),
+                                            std::vector<int64_t>(static_cast<size_t>(lx.pieces), 0));
   const int kinds[2] = {SPD_DENSE, SPD_DENSE}, order[2] = {0, 1};
   // column slab [lo, lo + w) of a dense rows x N factor, uploaded contiguous
+  // (one row copy per factor row)
   auto slab_of = [&](const SparseTensor& F, int64_t lo, int64_t w, DevTensor& dst) {
     const int64_t rows = F.dims()[0];
     const std::vector<double>& fv = F.vals().scalar_values();
     std::vector<double> fy(static_cast<size_t>(rows * w));
-    for (int64_t k = 0; k < rows; k++)
-      for (int64_t j = 0; j < w; j++) fy[k * w + j] = fv[k * N + lo + j];
+    for (int64_t k = 0; k < rows; k++) std::memcpy(fy.data() + k * w, fv.data() + k * N + lo, sizeof(double) * w);
     const int64_t dims[2] = {rows, w};
     check(spd_tensor_upload(ctx.h, 2, dims, kinds, order, nullptr, nullptr, fy.data(), &dst.h));
   };
   for (int64_t y = 0; y < ly.pieces; y++) {
     const CoordRange& slab = ly.color_bounds[y];
     const int64_t w = slab.empty() ? 0 : slab.hi - slab.lo + 1;
-  std::vector<int64_t> work(lx.pieces, 0);
+    std::vector<int64_t>& work = work_xy[static_cast<size_t>(y)];
     if (w > 0) {
       DevTensor Cy, Dy, Ay;
       const int64_t adims[2] = {n, w};
@@ -177,19 +317,13 @@ ExecResult execute_batched(const Plan& plan, const TensorSet& tensors, const Mac
       }
       check(spd_last_work(ctx.h, work.data(), lx.pieces));
       check(spd_tensor_download_vals(Ay.h, ay.data()));
-      for (int64_t i = 0; i < n; i++)
-        for (int64_t j = 0; j < w; j++) out[i * N + slab.lo + j] = ay[i * w + j];
-    }
-    for (int64_t x = 0; x < lx.pieces; x++) {
-      std::vector<int64_t> coords(machine.rank(), 0);
-      coords[machine.dim_index(lx.machine_dim)] = x;
-      coords[machine.dim_index(ly.machine_dim)] = y;
-      r.stats.per_worker[machine.worker_id(coords)].work = work[x];
+      for (int64_t i = 0; i < n; i++) std::memcpy(out.data() + i * N + slab.lo, ay.data() + i * w, sizeof(double) * w);
     }
   }
-  int64_t total = 0, mx = 0;
-  for (const auto& w : r.stats.per_worker) total += w.work, mx = std::max(mx, w.work);
-  r.stats.imbalance = total == 0 ? 1.0 : (double)mx * (double)r.stats.workers / (double)total;
+  const std::vector<Task> tasks = tasks_of(plan, machine);
+  std::vector<int64_t> task_work;
+  for (const auto& tk : tasks) task_work.push_back(work_xy[static_cast<size_t>(tk.colors[1])][static_cast<size_t>(tk.colors[0])]);
+  r.stats = make_stats(ctx.h, plan, tensors, machine, residency, tasks, task_work);
   r.stats.combines = 0;
   const SparseTensor& outstub = tensors.at(out_name);
   std::vector<LevelStorage> levels;
@@ -198,10 +332,11 @@ ExecResult execute_batched(const Plan& plan, const TensorSet& tensors, const Mac
   return r;
 }
 
-ExecResult execute_gpu(const Plan& plan, const TensorSet& tensors, const MachineGrid& machine) {
+ExecResult execute_gpu(const Plan& plan, const TensorSet& tensors, const MachineGrid& machine,
+                       const Residency& residency) {
   if (plan.loops.size() == 2) {
     const std::string k = kernel_of(plan);
-    if (k == "spmm" || k == "spmttkrp") return execute_batched(plan, tensors, machine, k);
+    if (k == "spmm" || k == "spmttkrp") return execute_batched(plan, tensors, machine, residency, k);
   }
   if (plan.loops.size() != 1)
     throw ValidationError("unsupported on gpu: one distributed loop, or the batched two-loop SpMM / SpMTTKRP");
@@ -288,15 +423,12 @@ ExecResult execute_gpu(const Plan& plan, const TensorSet& tensors, const Machine
   }
 
   ExecResult r{std::move(out), Stats{}};
-  r.stats.workers = machine.total_workers();
-  r.stats.per_worker.resize(r.stats.workers);
   std::vector<int64_t> work(loop.pieces);
   check(spd_last_work(ctx.h, work.data(), loop.pieces));
-  for (int64_t c = 0; c < loop.pieces; c++) {
-    r.stats.per_worker[c].work = work[c];
-    for (const auto& n : plan.stmt.tensor_names()) r.stats.per_worker[c].bytes_by_tensor[n] = 0;
-  }
-  r.stats.imbalance = st.imbalance;
+  const std::vector<Task> tasks = tasks_of(plan, machine);
+  std::vector<int64_t> task_work;
+  for (const auto& tk : tasks) task_work.push_back(work[static_cast<size_t>(tk.colors[0])]);
+  r.stats = make_stats(ctx.h, plan, tensors, machine, residency, tasks, task_work);
   r.stats.combines = st.combines;
   return r;
 }

@@ -33,7 +33,8 @@ using namespace dspar;
 #ifdef WITH_GPU_EXEC
 // integration/gpu_execute.cpp: the ExecMode::Gpu adapter under test.
 namespace dspar_gpu {
-ExecResult execute_gpu(const Plan& plan, const TensorSet& tensors, const MachineGrid& machine);
+ExecResult execute_gpu(const Plan& plan, const TensorSet& tensors, const MachineGrid& machine,
+                       const Residency& residency);
 }
 #endif
 
@@ -234,7 +235,7 @@ void* ref_run(const char* expr, const char* schedule, const char* grid, const ch
       double t1 = now();
 #ifdef WITH_GPU_EXEC
       if (std::string(mode) == "gpu")
-        r->result = dspar_gpu::execute_gpu(r->compute, r->tensors, r->machine);
+        r->result = dspar_gpu::execute_gpu(r->compute, r->tensors, r->machine, residency);
       else
 #endif
         r->result = execute(r->compute, r->tensors, r->machine, residency, parse_exec_mode(mode));

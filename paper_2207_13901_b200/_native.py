@@ -59,6 +59,7 @@ SIGNATURES = {
     "spd_deppart_by_bounds": (C.c_int, [vp, C.c_int, i64p, i64, i64p, vp, vp, i64, i64p, C.POINTER(C.c_int)]),
     "spd_tensor_restage": (C.c_int, [vp, vp, C.POINTER(i64p), C.POINTER(i64p), dblp]),
     "spd_ledger_bytes": (C.c_int, [vp, vp, C.c_int, C.c_int, i64, i64p]),
+    "spd_ledger_missing": (C.c_int, [vp, i64, C.POINTER(i64p), i64p, C.POINTER(i64p), i64p, i64p]),
     "spd_tensor_repartition": (C.c_int, [vp, vp, C.c_int, C.POINTER(vp), i64p]),
     "spd_tensor_upload_piece": (
         C.c_int,

@@ -148,8 +148,9 @@ struct spd_tensor {
     const int64_t* R = nullptr;
     int64_t* ptr = nullptr;
     int64_t* id = nullptr;
-    int64_t m = 0;
-    int64_t cap_ptr = 0, cap_id = 0;  // allocated entries (reused after a restage)
+    int64_t* m_dev = nullptr;  // count of non-empty rows, on the device
+    int64_t m = -1;            // host copy, -1 until read
+    int64_t cap_id = 0;        // allocated rows of id (ptr: cap_id + 1), reused after a restage
   } nz[3];
   // Staging buffers of spd_tensor_restage (pos pairs, row-start flags), kept
   // so a per-step re-upload allocates nothing.
@@ -157,6 +158,24 @@ struct spd_tensor {
   int64_t stage_pairs_cap = 0;
   unsigned char* stage_flags = nullptr;
   int64_t stage_flags_cap = 0;
+  // spd_tensor_restage validates before it swaps: the new row pointers, crd
+  // and vals land in these staging arrays, are checked on the device, and a
+  // commit kernel copies them over the live arrays only if every check
+  // passed -- a rejected restage leaves the tensor exactly as it was.  The
+  // verdict travels to the host without a synchronisation (pinned copy +
+  // event) and is reported by the next call on the tensor once the event has
+  // completed, or by spd_context_synchronize.
+  std::vector<int64_t*> stage_rowptr, stage_crd;  // per level
+  int64_t stage_leaf_cap = 0;                     // leaf crd / vals entries allocated
+  double* stage_vals = nullptr;
+  int* restage_err = nullptr;       // device flags of the last restage
+  int* restage_err_host = nullptr;  // pinned copy
+  cudaEvent_t restage_done = nullptr;
+  bool restage_pending = false;
+  bool restage_moved = false;  // the last restage moved a row-split piece's range
+  // A piece whose row-split range moved in a restage that was then rejected:
+  // its arrays no longer match its range, every later call refuses it.
+  bool poisoned = false;
   // Leaf crd as int32 with bit 31 = "hot column" (its dense row is among the
   // most referenced ones that fit in L2), for row-gathering kernels; built on
   // first use for a given dense-row size (crd32h_rowbytes).
@@ -175,14 +194,15 @@ struct spd_tensor {
   bool piece = false;
   int64_t piece_lo = 0, piece_hi = -1;
   int64_t piece_cap = 0;  // allocated positions of piece_crd / piece_vals
-  int piece_split = 0;  // 1 rows / 2 nonzeros: staged from host (spd_tensor_upload_piece); 0 placed
+  int piece_split = 0;  // 1 rows / 2 nonzeros: re-stageable from the host (upload_piece, place); 0 not (3-level pieces)
   int64_t* piece_crd = nullptr;
   double* piece_vals = nullptr;
   int32_t* crd32h_alloc = nullptr;  // allocation behind crd32h (offset for pieces)
-  // Hot-copy index (SpMM leaf, HOT == 2): leaf crd as int32 where a hot
-  // column is 0x80000000 | slot, its row read from a per-call compact copy
-  // of the hot rows (hot_ids[slot] = column); built for one dense-row size.
-  int32_t* crd32p = nullptr;  // plain int32 copy of the leaf crd (SpMM HOT == 3)
+  // int32 copy of the leaf crd (the N = 32 SpMM leaf), indexed by global
+  // position; crd32_alloc / crd32_cap the allocation behind it.
+  int32_t* crd32 = nullptr;
+  int32_t* crd32_alloc = nullptr;
+  int64_t crd32_cap = 0;
   // Compacted-column index (SpMV over a wide x): the referenced columns of
   // the leaf level renumbered densely in ascending order -- crdc[q] = rank of
   // crd[q] among them, cref[r] = the column of rank r, nref of them -- so a
@@ -192,10 +212,6 @@ struct spd_tensor {
   int32_t* crdc_alloc = nullptr;  // allocation behind crdc
   int32_t* cref = nullptr;
   int64_t nref = -1;
-  int32_t* crd32x = nullptr;
-  int32_t* crd32x_alloc = nullptr;
-  int32_t* hot_ids = nullptr;
-  int64_t hot_n = 0, crd32x_rowbytes = 0;
 };
 
 struct spd_context {
@@ -221,8 +237,8 @@ struct spd_context {
   bool colors_host_valid = false;
 
   std::vector<int64_t> last_work;    // per colour
-  spd::DeviceBuffer scratch[8];  // [6]: compact hot-row copy, [7]: compacted x (SpMV)
-  int64_t persist_bytes = -1;        // L2 persisting set-aside (-1: not set up)
+  std::vector<spd_tensor*> pending_restage;  // tensors whose last restage verdict is still on its way
+  spd::DeviceBuffer scratch[8];  // [7]: compacted x (SpMV)
   spd::DeviceBuffer counters;        // small int64 device counters
   int64_t* pinned_counters = nullptr;
 
@@ -280,8 +296,24 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// The leaf kernels read a tensor's levels in mode order (level 0 = output
+// row i, ...).  A transposed storage order (a CSC 'ds:1,0', a column-major
+// dense 'dd:1,0') is accepted by the reference (format_lang.hpp) but would be
+// read as the identity order here, so it is rejected like any other
+// unsupported format (advisor finding, round 1).
+inline void require_identity_order(const spd_tensor* t, const char* what) {
+  for (size_t k = 0; k < t->mode_order.size(); k++)
+    if (t->mode_order[k] != (int)k)
+      throw ValidationError(std::string("unsupported on gpu: ") + what +
+                            " must be stored in mode order (no transposed storage)");
+}
+
 // Host-side helpers implemented in context.cu.
 spd_context* checked(spd_context* ctx);
+// Reports the verdict of t's last spd_tensor_restage (ValidationError when it
+// was rejected) once it is known; `block` waits for it.  Also refuses a
+// poisoned piece.  Every call that uses a tensor starts with it.
+void settle_restage(const spd_tensor* t, bool block = false);
 void activate(spd_context* ctx);
 const std::vector<spd_color>& host_colors(spd_context* ctx);  // syncs if needed
 void require_partition(spd_context* ctx, const spd_tensor* t, int64_t first, int64_t count,

@@ -5,6 +5,7 @@
 // levels grouped like level_grouping (tensor.cpp:30-41), a compressed level
 // kept as an int64 row pointer (lossless versus the reference's inclusive
 // (lo,hi) pos pairs, tensor.cpp:258-281), crd int64 and vals fp64, all in HBM.
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -103,6 +104,48 @@ __global__ void k_rowptr_to_pairs(const int64_t* __restrict__ rowptr, int64_t np
     pairs[2 * p] = rowptr[p];
     pairs[2 * p + 1] = rowptr[p + 1] - 1;
   }
+}
+
+// Commit of a restage: copies the staged array over the live one only when
+// no validation flag was raised.
+__global__ void k_commit(const int* __restrict__ err, const int64_t* __restrict__ src, int64_t* __restrict__ dst,
+                         int64_t n) {
+  if (*err) return;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+static const char* restage_message(int err) {
+  if (err & 1) return "tensor: pos ranges must tile [0, nnz) with canonical empties";
+  if (err & 2) return "tensor: crd must be strictly increasing per range";
+  return "tensor: crd value out of dimension bounds";
+}
+
+void settle_restage(const spd_tensor* tc, bool block) {
+  spd_tensor* t = const_cast<spd_tensor*>(tc);
+  if (!t) return;
+  if (t->restage_pending) {
+    if (block) {
+      SPD_CUDA(cudaEventSynchronize(t->restage_done));
+    } else {
+      const cudaError_t q = cudaEventQuery(t->restage_done);
+      if (q == cudaErrorNotReady) return;
+      SPD_CUDA(q);
+    }
+    t->restage_pending = false;
+    auto& pend = t->ctx->pending_restage;
+    pend.erase(std::remove(pend.begin(), pend.end(), t), pend.end());
+    const int err = *t->restage_err_host;
+    if (err) {
+      if (t->restage_moved) t->poisoned = true;  // its range moved with the rejected pattern
+      throw ValidationError(std::string(restage_message(err)) +
+                            (t->poisoned ? " (spd_tensor_restage rejected it; the row-split piece is unusable, "
+                                           "destroy it)"
+                                         : " (spd_tensor_restage rejected it; the tensor keeps its previous "
+                                           "contents)"));
+    }
+  }
+  if (t->poisoned) throw ValidationError("tensor: a rejected restage left this piece unusable");
 }
 
 static int grid_for(spd_context* ctx, int64_t n, int block = 256) {
@@ -451,6 +494,17 @@ int spd_context_synchronize(spd_context* ctx) {
     checked(ctx);
     activate(ctx);
     SPD_CUDA(cudaStreamSynchronize(ctx->stream));
+    // report the verdicts of restages issued on this context (the first
+    // rejection raises; every pending verdict is consumed)
+    std::string first;
+    while (!ctx->pending_restage.empty()) {
+      try {
+        settle_restage(ctx->pending_restage.front(), true);
+      } catch (const ValidationError& e) {
+        if (first.empty()) first = e.what();
+      }
+    }
+    if (!first.empty()) throw ValidationError(first);
   });
 }
 
@@ -508,62 +562,97 @@ int spd_tensor_upload(spd_context* ctx, int order, const int64_t* dims, const in
 
 namespace spd {
 
+// This GPU's colour of a piece, read off the host pos pairs (no device
+// round trip): divide_bounds (planner.cpp:10-20) over the positions for a
+// nonzero split, or over the rows for a row split -- then the positions of
+// that row block.  The pairs are not validated yet; only the two entries read
+// here are range-checked (the device checks the rest).
+static spd_range host_piece_range(const int64_t* pairs, int64_t nrows, int64_t nnz, int split, int world,
+                                  int rank) {
+  auto divide = [&](int64_t n) {
+    const int64_t block = n / world;
+    spd_range r{rank * block, rank < world - 1 ? rank * block + block - 1 : n - 1};
+    if (r.lo > r.hi) r = spd_range{0, -1};
+    return r;
+  };
+  if (split == 2) return divide(nnz);
+  const spd_range rows = divide(nrows);
+  if (rows.lo > rows.hi) return spd_range{0, -1};
+  spd_range q{pairs[2 * rows.lo], pairs[2 * rows.hi + 1]};
+  if (q.lo < 0 || q.hi >= nnz || q.lo > q.hi + 1)
+    throw ValidationError("tensor: pos ranges must tile [0, nnz) with canonical empties");
+  if (q.lo > q.hi) q = spd_range{0, -1};
+  return q;
+}
+
 // Per-GPU piece of a CSR matrix staged from host arrays (spd_tensor_upload_
 // piece / spd_tensor_restage of a piece): the whole pos level (O(rows), the
-// partition step needs it) converted and checked on the GPU, then the compute
-// partition of `split` over the communicator's GPUs, then only this GPU's
-// colour of crd / vals copied from the host arrays (indexed by global
-// position) and checked.  `fresh`: allocate; else re-stage into t, whose
-// position range must come out unchanged.
+// partition step needs it) converted and checked on the GPU, and only this
+// GPU's colour of crd / vals (split 1 = rows, 2 = nonzeros over the
+// communicator's GPUs) copied from the host arrays (indexed by global
+// position) and checked.  `fresh`: an upload -- allocate, write in place and
+// synchronise (the handle is returned validated).  Else a restage: stage,
+// validate and commit on the device like spd_tensor_restage, no host
+// synchronisation.
 static void stage_piece(spd_context* ctx, spd_tensor* t, const int64_t* pairs, const int64_t* crd,
                         const double* vals, int split, bool fresh) {
   cudaStream_t s = ctx->stream;
   spd_level_store& L = t->levels[1];
   const int64_t nrows = L.parent_positions, nnz = L.positions;
-  int* err_d = (int*)ctx->counters.reserve(sizeof(int64_t) * 16) + 2;
+  if (nrows > 0 && !pairs) throw ValidationError("compressed level 1 needs pos");
+  const spd_range mine = host_piece_range(pairs, nrows, nnz, split, ctx->world, ctx->rank);
+  const int64_t cnt = std::max<int64_t>(mine.hi - mine.lo + 1, 0);
+  if (cnt > 0 && !crd) throw ValidationError("compressed level 1 needs crd");
+  if (cnt > 0 && !vals) throw ValidationError("tensor: vals length does not match leaf count");
+  int* err_d = nullptr;
+  int64_t *rp = L.rowptr, *cd = nullptr;
+  double* vd = nullptr;
+  if (fresh) {
+    err_d = (int*)ctx->counters.reserve(sizeof(int64_t) * 16) + 2;
+    t->piece_cap = std::max<int64_t>(cnt, 1);
+    t->piece_crd = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * t->piece_cap);
+    t->piece_vals = (double*)dev_alloc(ctx, sizeof(double) * t->piece_cap);
+    cd = t->piece_crd;
+    vd = t->piece_vals;
+  } else {
+    if (!t->restage_err) {
+      t->restage_err = (int*)dev_alloc(ctx, sizeof(int));
+      SPD_CUDA(cudaMallocHost((void**)&t->restage_err_host, sizeof(int)));
+      SPD_CUDA(cudaEventCreateWithFlags(&t->restage_done, cudaEventDisableTiming));
+    }
+    err_d = t->restage_err;
+    if (t->stage_rowptr.size() != 2) {
+      t->stage_rowptr.assign(2, nullptr);
+      t->stage_crd.assign(2, nullptr);
+      t->stage_rowptr[1] = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (nrows + 1));
+    }
+    if (t->stage_leaf_cap < cnt) {
+      dev_free(ctx, t->stage_crd[1]);
+      dev_free(ctx, t->stage_vals);
+      t->stage_leaf_cap = std::max<int64_t>(cnt, 1);
+      t->stage_crd[1] = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * t->stage_leaf_cap);
+      t->stage_vals = (double*)dev_alloc(ctx, sizeof(double) * t->stage_leaf_cap);
+    }
+    rp = t->stage_rowptr[1];
+    cd = t->stage_crd[1];
+    vd = t->stage_vals;
+  }
   SPD_CUDA(cudaMemsetAsync(err_d, 0, sizeof(int), s));
   if (nrows > 0) {
-    if (!pairs) throw ValidationError("compressed level 1 needs pos");
     if (t->stage_pairs_cap < 2 * nrows) {
       dev_free(ctx, t->stage_pairs);
       t->stage_pairs = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * 2 * nrows);
       t->stage_pairs_cap = 2 * nrows;
     }
     SPD_CUDA(cudaMemcpyAsync(t->stage_pairs, pairs, sizeof(int64_t) * 2 * nrows, cudaMemcpyHostToDevice, s));
-    k_pairs_to_rowptr<<<grid_for(ctx, nrows), 256, 0, s>>>(t->stage_pairs, nrows, nnz, L.rowptr, err_d);
+    k_pairs_to_rowptr<<<grid_for(ctx, nrows), 256, 0, s>>>(t->stage_pairs, nrows, nnz, rp, err_d);
     SPD_CHECK_LAUNCH();
   } else {
-    SPD_CUDA(cudaMemsetAsync(L.rowptr, 0, sizeof(int64_t), s));
+    SPD_CUDA(cudaMemsetAsync(rp, 0, sizeof(int64_t), s));
   }
-  const int rc = split == 1 ? spd_partition_universe(ctx, t, ctx->world, nullptr)
-                            : spd_partition_nonzero(ctx, t, 1, ctx->world, nullptr);
-  if (rc != SPD_OK) throw ValidationError(spd_last_error());
-  const spd_range mine = host_colors(ctx)[ctx->rank].q;  // syncs
-  int err_h = 0;
-  SPD_CUDA(cudaMemcpy(&err_h, err_d, sizeof(int), cudaMemcpyDeviceToHost));
-  if (err_h & 1) throw ValidationError("tensor: pos ranges must tile [0, nnz) with canonical empties");
-  const int64_t cnt = std::max<int64_t>(mine.hi - mine.lo + 1, 0);
-  // a row split's ranges follow the new row pointer: reuse the piece
-  // buffers when they are large enough
-  if (fresh || cnt > t->piece_cap) {
-    dev_free(ctx, t->piece_crd);
-    dev_free(ctx, t->piece_vals);
-    t->piece_cap = std::max<int64_t>(cnt, 1);
-    t->piece_crd = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * t->piece_cap);
-    t->piece_vals = (double*)dev_alloc(ctx, sizeof(double) * t->piece_cap);
-  }
-  t->piece_split = split;
-  t->piece_lo = mine.lo;
-  t->piece_hi = mine.hi;
-  L.crd = t->piece_crd - mine.lo;  // indexed by global position
-  t->vals = t->piece_vals - mine.lo;
-  if (t->crd32h_alloc) dev_free(ctx, t->crd32h_alloc), t->crd32h_alloc = nullptr;  // sized by the old piece
-  if (t->crd32x_alloc) dev_free(ctx, t->crd32x_alloc), t->crd32x_alloc = nullptr;
   if (cnt > 0) {
-    if (!crd) throw ValidationError("compressed level 1 needs crd");
-    if (!vals) throw ValidationError("tensor: vals length does not match leaf count");
-    SPD_CUDA(cudaMemcpyAsync(t->piece_crd, crd + mine.lo, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice, s));
-    SPD_CUDA(cudaMemcpyAsync(t->piece_vals, vals + mine.lo, sizeof(double) * cnt, cudaMemcpyHostToDevice, s));
+    SPD_CUDA(cudaMemcpyAsync(cd, crd + mine.lo, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice, s));
+    SPD_CUDA(cudaMemcpyAsync(vd, vals + mine.lo, sizeof(double) * cnt, cudaMemcpyHostToDevice, s));
     const int64_t need = std::max<int64_t>(cnt, nrows);  // also the nz_view flags buffer
     if (t->stage_flags_cap < need) {
       dev_free(ctx, t->stage_flags);
@@ -572,42 +661,78 @@ static void stage_piece(spd_context* ctx, spd_tensor* t, const int64_t* pairs, c
     }
     unsigned char* start = t->stage_flags - mine.lo;  // indexed by global position
     SPD_CUDA(cudaMemsetAsync(t->stage_flags, 0, cnt, s));
-    k_mark_starts<<<grid_for(ctx, nrows), 256, 0, s>>>(L.rowptr, nrows, start, mine.lo, mine.hi);
+    k_mark_starts<<<grid_for(ctx, nrows), 256, 0, s>>>(rp, nrows, start, mine.lo, mine.hi);
     SPD_CHECK_LAUNCH();
     const int64_t dim = t->dims[t->mode_order[1]];
-    k_check_crd<<<grid_for(ctx, cnt), 256, 0, s>>>(L.crd, mine.lo, mine.hi, dim, start, mine.lo > 0 ? 1 : 0,
+    k_check_crd<<<grid_for(ctx, cnt), 256, 0, s>>>(cd - mine.lo, mine.lo, mine.hi, dim, start, mine.lo > 0 ? 1 : 0,
                                                    mine.lo > 0 ? crd[mine.lo - 1] : 0, err_d);
     SPD_CHECK_LAUNCH();
   }
-  SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters + 12, err_d, sizeof(int), cudaMemcpyDeviceToHost, s));
-  SPD_CUDA(cudaStreamSynchronize(s));
-  std::memcpy(&err_h, ctx->pinned_counters + 12, sizeof(int));
-  if (err_h & 2) throw ValidationError("tensor: crd must be strictly increasing per range");
-  if (err_h & 4) throw ValidationError("tensor: crd value out of dimension bounds");
+  const bool moved = !fresh && (mine.lo != t->piece_lo || mine.hi != t->piece_hi);
+  t->piece_split = split;
+  if (fresh) {
+    t->piece_lo = mine.lo;
+    t->piece_hi = mine.hi;
+    L.crd = t->piece_crd - mine.lo;  // indexed by global position
+    t->vals = t->piece_vals - mine.lo;
+    int err_h = 0;
+    SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters + 12, err_d, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SPD_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(&err_h, ctx->pinned_counters + 12, sizeof(int));
+    if (err_h) throw ValidationError(restage_message(err_h));
+    return;
+  }
+  // restage: a row split's range follows the new pattern; grow the live piece
+  // arrays when it does not fit (a rejection then poisons the piece)
+  if (cnt > t->piece_cap) {
+    dev_free(ctx, t->piece_crd);
+    dev_free(ctx, t->piece_vals);
+    t->piece_cap = cnt;
+    t->piece_crd = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * t->piece_cap);
+    t->piece_vals = (double*)dev_alloc(ctx, sizeof(double) * t->piece_cap);
+    if (t->crd32_alloc) dev_free(ctx, t->crd32_alloc), t->crd32_alloc = nullptr, t->crd32_cap = 0;
+  }
+  t->piece_lo = mine.lo;
+  t->piece_hi = mine.hi;
+  L.crd = t->piece_crd - mine.lo;
+  t->vals = t->piece_vals - mine.lo;
+  t->restage_moved = moved;
+  k_commit<<<grid_for(ctx, nrows + 1), 256, 0, s>>>(err_d, rp, L.rowptr, nrows + 1);
+  SPD_CHECK_LAUNCH();
+  if (cnt > 0) {
+    k_commit<<<grid_for(ctx, cnt), 256, 0, s>>>(err_d, cd, t->piece_crd, cnt);
+    SPD_CHECK_LAUNCH();
+    k_commit<<<grid_for(ctx, cnt), 256, 0, s>>>(err_d, reinterpret_cast<const int64_t*>(vd),
+                                                reinterpret_cast<int64_t*>(t->piece_vals), cnt);
+    SPD_CHECK_LAUNCH();
+  }
+  SPD_CUDA(cudaMemcpyAsync(t->restage_err_host, err_d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  SPD_CUDA(cudaEventRecord(t->restage_done, s));
+  t->restage_pending = true;
+  ctx->pending_restage.push_back(t);
 }
 
 static void restage_piece(spd_context* ctx, spd_tensor* t, const int64_t* const* pos_pairs,
                           const int64_t* const* crd, const double* vals) {
   if (t->piece_split != 1 && t->piece_split != 2)
-    throw ValidationError("restage: a placed piece (spd_tensor_place) cannot be re-staged from the host");
+    throw ValidationError("restage: a placed piece (spd_tensor_place) or a 3-level piece cannot be re-staged "
+                          "from the host");
   const int64_t nrows = t->levels[1].parent_positions, nnz = t->levels[1].positions;
   const int64_t got = nrows == 0 ? 0 : (pos_pairs && pos_pairs[1] ? pos_pairs[1][2 * (nrows - 1) + 1] + 1 : -1);
   if (got != nnz)
     throw ValidationError("restage: level 1 holds " + std::to_string(nnz) + " positions, the new pos " +
                           std::to_string(got));
+  stage_piece(ctx, t, pos_pairs[1], crd ? crd[1] : nullptr, vals, t->piece_split, false);
   for (auto& z : t->nz) z.R = nullptr;
   t->crd32h = nullptr;
   t->crd32h_rowbytes = 0;
-  t->crd32x = nullptr;
-  t->crd32x_rowbytes = 0;
-  dev_free(ctx, t->crd32p);
-  t->crd32p = nullptr;
+  t->crd32 = nullptr;
   dev_free(ctx, t->crdc_alloc);
   t->crdc_alloc = t->crdc = nullptr;
   dev_free(ctx, t->cref);
   t->cref = nullptr;
   t->nref = -1;
-  stage_piece(ctx, t, pos_pairs[1], crd ? crd[1] : nullptr, vals, t->piece_split, false);
+  if (ctx->split_tensor == t) ctx->split = SplitKind::None, ctx->split_tensor = nullptr;
 }
 
 // 3-level trees (dss / sss, the CSF of SpTTV / SpMTTKRP): the upper levels
@@ -720,19 +845,18 @@ int spd_tensor_restage(spd_context* ctx, spd_tensor* t, const int64_t* const* po
     checked(ctx);
     if (!t) throw ValidationError("null tensor");
     if (t->ctx != ctx) throw ValidationError("restage: tensor belongs to another context");
+    activate(ctx);
+    settle_restage(t, true);  // the previous restage's verdict (its staging buffers are reused)
     if (t->piece) {
       restage_piece(ctx, t, pos_pairs, crd, vals);
       return;
     }
     if (!t->owns) throw ValidationError("restage: needs a tensor uploaded by spd_tensor_upload*");
     HostTrace ht("restage");
-    activate(ctx);
     cudaStream_t s = ctx->stream;
-    int* err_d = (int*)ctx->counters.reserve(sizeof(int64_t) * 16) + 2;  // [8..] belong to nz_view
-    int err_h = 0;
-    SPD_CUDA(cudaMemsetAsync(err_d, 0, sizeof(int), s));
+    // geometry checks on the host (nothing is queued before they pass)
     for (size_t l = 0; l < t->levels.size(); l++) {
-      spd_level_store& L = t->levels[l];
+      const spd_level_store& L = t->levels[l];
       if (L.kind != SPD_COMPRESSED) continue;
       const int64_t parent = L.parent_positions, nnz = L.positions;
       if (parent > 0 && (!pos_pairs || !pos_pairs[l]))
@@ -743,6 +867,33 @@ int spd_tensor_restage(spd_context* ctx, spd_tensor* t, const int64_t* const* po
                                             std::to_string(got));
       if (nnz > 0 && (!crd || !crd[l]))
         throw ValidationError("compressed level " + std::to_string(l) + " needs crd");
+    }
+    if (t->nvals > 0 && !vals) throw ValidationError("tensor: vals length does not match leaf count");
+    // staging arrays (allocated on the first restage, reused after)
+    const size_t nl = t->levels.size();
+    if (t->stage_rowptr.size() != nl) {
+      t->stage_rowptr.assign(nl, nullptr);
+      t->stage_crd.assign(nl, nullptr);
+      for (size_t l = 0; l < nl; l++) {
+        const spd_level_store& L = t->levels[l];
+        if (L.kind != SPD_COMPRESSED) continue;
+        t->stage_rowptr[l] = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (L.parent_positions + 1));
+        t->stage_crd[l] = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * std::max<int64_t>(L.positions, 1));
+      }
+      t->stage_vals = (double*)dev_alloc(ctx, sizeof(double) * std::max<int64_t>(t->nvals, 1));
+    }
+    if (!t->restage_err) {
+      t->restage_err = (int*)dev_alloc(ctx, sizeof(int));
+      SPD_CUDA(cudaMallocHost((void**)&t->restage_err_host, sizeof(int)));
+      SPD_CUDA(cudaEventCreateWithFlags(&t->restage_done, cudaEventDisableTiming));
+    }
+    int* err_d = t->restage_err;
+    SPD_CUDA(cudaMemsetAsync(err_d, 0, sizeof(int), s));
+    for (size_t l = 0; l < nl; l++) {
+      spd_level_store& L = t->levels[l];
+      if (L.kind != SPD_COMPRESSED) continue;
+      const int64_t parent = L.parent_positions, nnz = L.positions;
+      int64_t* rp = t->stage_rowptr[l];
       if (parent > 0) {
         if (t->stage_pairs_cap < 2 * parent) {
           dev_free(ctx, t->stage_pairs);
@@ -751,11 +902,13 @@ int spd_tensor_restage(spd_context* ctx, spd_tensor* t, const int64_t* const* po
         }
         SPD_CUDA(cudaMemcpyAsync(t->stage_pairs, pos_pairs[l], sizeof(int64_t) * 2 * parent,
                                  cudaMemcpyHostToDevice, s));
-        k_pairs_to_rowptr<<<grid_for(ctx, parent), 256, 0, s>>>(t->stage_pairs, parent, nnz, L.rowptr, err_d);
+        k_pairs_to_rowptr<<<grid_for(ctx, parent), 256, 0, s>>>(t->stage_pairs, parent, nnz, rp, err_d);
         SPD_CHECK_LAUNCH();
+      } else {
+        SPD_CUDA(cudaMemsetAsync(rp, 0, sizeof(int64_t), s));
       }
       if (nnz > 0) {
-        SPD_CUDA(cudaMemcpyAsync(L.crd, crd[l], sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
+        SPD_CUDA(cudaMemcpyAsync(t->stage_crd[l], crd[l], sizeof(int64_t) * nnz, cudaMemcpyHostToDevice, s));
         const int64_t need = std::max<int64_t>(nnz, parent);  // also the nz_view flags buffer
         if (t->stage_flags_cap < need) {
           dev_free(ctx, t->stage_flags);
@@ -763,25 +916,43 @@ int spd_tensor_restage(spd_context* ctx, spd_tensor* t, const int64_t* const* po
           t->stage_flags_cap = need;
         }
         SPD_CUDA(cudaMemsetAsync(t->stage_flags, 0, nnz, s));
-        k_mark_starts<<<grid_for(ctx, parent), 256, 0, s>>>(L.rowptr, parent, t->stage_flags, 0, nnz - 1);
+        k_mark_starts<<<grid_for(ctx, parent), 256, 0, s>>>(rp, parent, t->stage_flags, 0, nnz - 1);
         SPD_CHECK_LAUNCH();
         const int64_t dim = t->dims[t->mode_order[t->groups[l][0]]];
-        k_check_crd<<<grid_for(ctx, nnz), 256, 0, s>>>(L.crd, 0, nnz - 1, dim, t->stage_flags, 0, 0, err_d);
+        k_check_crd<<<grid_for(ctx, nnz), 256, 0, s>>>(t->stage_crd[l], 0, nnz - 1, dim, t->stage_flags, 0, 0,
+                                                       err_d);
+        SPD_CHECK_LAUNCH();
+      }
+    }
+    if (t->nvals > 0)
+      SPD_CUDA(cudaMemcpyAsync(t->stage_vals, vals, sizeof(double) * t->nvals, cudaMemcpyHostToDevice, s));
+    // commit (skipped on the device when a check failed)
+    for (size_t l = 0; l < nl; l++) {
+      spd_level_store& L = t->levels[l];
+      if (L.kind != SPD_COMPRESSED) continue;
+      k_commit<<<grid_for(ctx, L.parent_positions + 1), 256, 0, s>>>(err_d, t->stage_rowptr[l], L.rowptr,
+                                                                     L.parent_positions + 1);
+      SPD_CHECK_LAUNCH();
+      if (L.positions > 0) {
+        k_commit<<<grid_for(ctx, L.positions), 256, 0, s>>>(err_d, t->stage_crd[l], L.crd, L.positions);
         SPD_CHECK_LAUNCH();
       }
     }
     if (t->nvals > 0) {
-      if (!vals) throw ValidationError("tensor: vals length does not match leaf count");
-      SPD_CUDA(cudaMemcpyAsync(t->vals, vals, sizeof(double) * t->nvals, cudaMemcpyHostToDevice, s));
+      k_commit<<<grid_for(ctx, t->nvals), 256, 0, s>>>(err_d, reinterpret_cast<const int64_t*>(t->stage_vals),
+                                                       reinterpret_cast<int64_t*>(t->vals), t->nvals);
+      SPD_CHECK_LAUNCH();
     }
+    SPD_CUDA(cudaMemcpyAsync(t->restage_err_host, err_d, sizeof(int), cudaMemcpyDeviceToHost, s));
+    SPD_CUDA(cudaEventRecord(t->restage_done, s));
+    t->restage_pending = true;
+    ctx->pending_restage.push_back(t);
     // derived indices are functions of the old pattern: invalidate, keep buffers
+    // (rebuilding them over an unchanged pattern after a rejection is harmless)
     for (auto& z : t->nz) z.R = nullptr;
     t->crd32h = nullptr;
     t->crd32h_rowbytes = 0;
-    t->crd32x = nullptr;
-    t->crd32x_rowbytes = 0;
-    dev_free(ctx, t->crd32p);
-    t->crd32p = nullptr;
+    t->crd32 = nullptr;
     dev_free(ctx, t->crdc_alloc);
     t->crdc_alloc = t->crdc = nullptr;
     dev_free(ctx, t->cref);
@@ -793,13 +964,6 @@ int spd_tensor_restage(spd_context* ctx, spd_tensor* t, const int64_t* const* po
     t->leaf_rowptr = nullptr;
     if (ctx->split_tensor == t) ctx->split = SplitKind::None, ctx->split_tensor = nullptr;
     ht.mark("queued");
-    SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters + 12, err_d, sizeof(int), cudaMemcpyDeviceToHost, s));
-    SPD_CUDA(cudaStreamSynchronize(s));
-    std::memcpy(&err_h, ctx->pinned_counters + 12, sizeof(int));
-    ht.mark("synced");
-    if (err_h & 1) throw ValidationError("tensor: pos ranges must tile [0, nnz) with canonical empties");
-    if (err_h & 2) throw ValidationError("tensor: crd must be strictly increasing per range");
-    if (err_h & 4) throw ValidationError("tensor: crd value out of dimension bounds");
   });
 }
 
@@ -861,6 +1025,17 @@ int spd_tensor_destroy(spd_tensor* t) {
       ctx->split = SplitKind::None;
       ctx->split_tensor = nullptr;
     }
+    if (t->restage_pending) {  // the verdict is dropped with the tensor
+      cudaEventSynchronize(t->restage_done);
+      auto& pend = ctx->pending_restage;
+      pend.erase(std::remove(pend.begin(), pend.end(), t), pend.end());
+    }
+    for (int64_t* p : t->stage_rowptr) dev_free(ctx, p);
+    for (int64_t* p : t->stage_crd) dev_free(ctx, p);
+    dev_free(ctx, t->stage_vals);
+    dev_free(ctx, t->restage_err);
+    if (t->restage_err_host) cudaFreeHost(t->restage_err_host);
+    if (t->restage_done) cudaEventDestroy(t->restage_done);
     if (t->piece) {
       for (size_t l = 0; l + 1 < t->levels.size(); l++) {
         dev_free(ctx, t->levels[l].rowptr);
@@ -878,17 +1053,16 @@ int spd_tensor_destroy(spd_tensor* t) {
     }
     dev_free(ctx, t->leaf_rowptr);
     dev_free(ctx, t->crd32h_alloc);
-    dev_free(ctx, t->crd32x_alloc);
-    dev_free(ctx, t->crd32p);
+    dev_free(ctx, t->crd32_alloc);
     dev_free(ctx, t->crdc_alloc);
     dev_free(ctx, t->cref);
-    dev_free(ctx, t->hot_ids);
     dev_free(ctx, t->stage_pairs);
     dev_free(ctx, t->stage_flags);
     dev_free(ctx, t->jleaf);
     for (auto& z : t->nz) {
       dev_free(ctx, z.ptr);
       dev_free(ctx, z.id);
+      dev_free(ctx, z.m_dev);
     }
     delete t;
     ht.mark("freed");
@@ -944,6 +1118,8 @@ int spd_tensor_download_level(const spd_tensor* t, int level, int64_t* pos_pairs
       throw ValidationError("a placed piece holds only its colour's positions: download the whole tensor");
     spd_context* ctx = t->ctx;
     activate(ctx);
+    settle_restage(t, true);
+    activate(ctx);
     if (pos_pairs && L.parent_positions > 0) {
       int64_t* tmp = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * 2 * L.parent_positions);
       k_rowptr_to_pairs<<<grid_for(ctx, L.parent_positions), 256, 0, ctx->stream>>>(
@@ -967,6 +1143,8 @@ int spd_tensor_download_rowptr(const spd_tensor* t, int level, int64_t* rowptr) 
     if (L.kind != SPD_COMPRESSED) throw ValidationError("level is dense: nothing stored");
     spd_context* ctx = t->ctx;
     activate(ctx);
+    settle_restage(t, true);
+    activate(ctx);
     SPD_CUDA(cudaMemcpyAsync(rowptr, L.rowptr, sizeof(int64_t) * (L.parent_positions + 1),
                              cudaMemcpyDeviceToHost, ctx->stream));
     SPD_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -978,6 +1156,8 @@ int spd_tensor_download_vals(const spd_tensor* t, double* vals) {
     if (!t) throw ValidationError("null tensor");
     if (t->piece) throw ValidationError("a placed piece holds only its colour's positions");
     spd_context* ctx = t->ctx;
+    activate(ctx);
+    settle_restage(t, true);
     activate(ctx);
     if (t->nvals > 0)
       SPD_CUDA(cudaMemcpyAsync(vals, t->vals, sizeof(double) * t->nvals, cudaMemcpyDeviceToHost,
@@ -994,6 +1174,8 @@ int spd_tensor_download_vals_range(const spd_tensor* t, int64_t first, int64_t c
     if (t->piece && count > 0 && (first < t->piece_lo || first + count - 1 > t->piece_hi))
       throw ValidationError("range outside the placed piece");
     spd_context* ctx = t->ctx;
+    activate(ctx);
+    settle_restage(t, true);
     activate(ctx);
     if (count > 0)
       SPD_CUDA(cudaMemcpyAsync(vals, t->vals + first, sizeof(double) * count,

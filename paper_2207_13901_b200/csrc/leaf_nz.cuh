@@ -24,8 +24,14 @@ namespace spd {
 struct NzView {
   const int64_t* __restrict__ ptr;  // m + 1 starts
   const int64_t* __restrict__ id;   // m row ids
-  int64_t m;
+  int64_t m;                        // count, or -1: read it from *m_dev
+  const int64_t* __restrict__ m_dev;  // device-side count (built without a host sync)
 };
+
+// The compacted-row count as the kernel sees it (kernels start with
+// `z.m = nz_count(z)`): the build leaves it on the device, so no host
+// synchronisation sits between building the view and using it.
+__device__ __forceinline__ int64_t nz_count(const NzView& z) { return z.m >= 0 ? z.m : __ldg(z.m_dev); }
 
 // Register-resident window of 64 compacted rows [cb, cb + 64).
 struct NzCursor {
@@ -55,7 +61,7 @@ __device__ __forceinline__ int64_t nz_get(int64_t v0, int64_t v1, int idx) {
   return idx < 32 ? a : b;
 }
 
-__device__ __noinline__ void nz_slide(const NzView& z, NzCursor& c) {
+__device__ __forceinline__ void nz_slide(const NzView& z, NzCursor& c) {
   while (c.ic - c.cb >= 32) {  // slide the register window; the new block is far ahead
     c.cb += 32;
     c.P0 = c.P1;
@@ -154,6 +160,7 @@ __global__ void __launch_bounds__(kBlock, 5) k_spmv_nz(WalkGeom g, NzView z, con
                                                     const double* __restrict__ x, double* __restrict__ y,
                                                     ChunkRecs rec, const int64_t* __restrict__ counters) {
   const int lane = lane_id();
+  z.m = nz_count(z);
   const int64_t begin = counters[1], end = counters[2];
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -330,6 +337,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmv_rows(WalkGeom g, NzView z
                                                       const double* __restrict__ x, double* __restrict__ y,
                                                       ChunkRecs rec, const int64_t* __restrict__ counters) {
   const int lane = lane_id();
+  z.m = nz_count(z);
   const int64_t begin = counters[1], end = counters[2];
   const uint64_t pol = l2_policy_evict_first();
   for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
@@ -425,230 +433,98 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmv_rows(WalkGeom g, NzView z
 }
 
 // ---------------------------------------------------------------------------
-// SpMV / SpTTV, staged (CSR-stream style): a group of 32 compacted rows is a
-// contiguous position range; the warp computes its products B(p) * x(crd(p))
-// window by window with lane-per-position loads -- crd / vals coalesced and
-// streamed, 8 independent x gathers per lane in flight -- into a per-warp
-// shared-memory window, then each lane sums its own row's products from
-// shared memory in stored-position order (rows longer than kStageLong: the
-// whole warp, lane-strided + butterfly).  Against k_spmv_rows this replaces
-// per-lane uncoalesced crd / vals loads (32 lines per instruction) and the
-// crd -> x dependence chain per lane with coalesced loads and more memory
-// parallelism.  Short rows add the rounded products in stored order, as the
-// reference does (sim.cpp:328-350).
-constexpr int kStageWin = 256;
-constexpr int kStageLong = 32;
+// SpMM N == 32 over the compacted view (the C2 leaf).  Half a warp per stored
+// position: lane l gathers columns 2(l%16), 2(l%16)+1 of C(k,:) with one
+// 128-bit load, so a warp instruction covers two positions.  Per 32-position
+// window the warp loads the window's int32 columns and values (one per lane,
+// the next window prefetched) and the row-start mask.  Per group of 2*UNR
+// positions it issues UNR gathers unconditionally (positions past the chunk
+// end read column 0 and are never added) and, when no row starts in a full
+// group, 2*UNR FMAs -- no per-position row logic.  A group holding row starts
+// walks only its starts: the products before each start are added under a
+// predicate, the finished row is flushed (the halves' partials summed with one
+// xor-shuffle) and the next row's id is read from the register cursor.  The
+// cursor keeps row starts relative to the chunk and row ids as 32-bit values
+// (rows < 2^31), so the walk fits 64 registers (32 warps / SM) without spills.
+// The previous leaf issued ~16 warp instructions per position, mostly 64-bit
+// address arithmetic and per-position row tests
+// (profiles/r02_spmm_leaf_base_ncu.txt); this one issues ~5.
+struct NzCur32 {
+  int64_t cb;  // block base (compacted row index)
+  int off;     // current compacted row - cb, in [0, 32) between windows
+  int P0, P1;  // starts of rows cb + lane, cb + 32 + lane, relative to the chunk start (clamped)
+  int I0, I1;  // ids of the same rows
+};
 
-template <int WIN>
-__device__ __forceinline__ void stage_products(const int64_t* __restrict__ crd, const double* __restrict__ vals,
-                                               const double* __restrict__ x, int64_t w0, int wn,
-                                               double* __restrict__ sp, uint64_t pol) {
-  const int lane = lane_id();
-  constexpr int PER = WIN / 32;
-  int64_t k[PER];
-  double v[PER];
-#pragma unroll
-  for (int i = 0; i < PER; i++) {
-    const int o = i * 32 + lane;
-    k[i] = o < wn ? ld_i64_hint(crd + w0 + o, pol) : 0;
-    v[i] = o < wn ? ld_f64_hint(vals + w0 + o, pol) : 0.0;
-  }
-  double xv[PER];
-#pragma unroll
-  for (int i = 0; i < PER; i++) xv[i] = i * 32 + lane < wn ? __ldg(x + k[i]) : 0.0;
-#pragma unroll
-  for (int i = 0; i < PER; i++) {
-    const double pr = __dmul_rn(v[i], xv[i]);
-    if (i * 32 + lane < wn) sp[i * 32 + lane] = pr;
-  }
+__device__ __forceinline__ void nz32_load(const NzView& z, int64_t j0, int64_t s, int& P, int& I) {
+  const int64_t j = j0 + lane_id();
+  const int64_t p = j <= z.m ? ld64(z.ptr + j) - s : (int64_t)INT32_MAX;
+  P = (int)max(min(p, (int64_t)INT32_MAX), (int64_t)-1);
+  I = j < z.m ? (int)ld64(z.id + j) : -1;
 }
 
-template <int MINB, int WIN = kStageWin>
-__global__ void __launch_bounds__(kBlock, MINB) k_spmv_stage(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
+__device__ __forceinline__ int shfl_pair(int v0, int v1, int idx) {
+  const int a = __shfl_sync(FULL, v0, idx & 31), b = __shfl_sync(FULL, v1, idx & 31);
+  return idx < 32 ? a : b;
+}
+
+template <int UNR, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z, const int32_t* __restrict__ crd32,
                                                       const double* __restrict__ vals,
-                                                      const double* __restrict__ x, double* __restrict__ y,
+                                                      const double* __restrict__ C, double* __restrict__ A,
                                                       ChunkRecs rec, const int64_t* __restrict__ counters) {
-  const int lane = lane_id();
-  const int64_t begin = counters[1], end = counters[2];
-  const uint64_t pol = l2_policy_evict_first();
-  __shared__ double s_prod[kBlock / 32][WIN];
-  double* sp = s_prod[threadIdx.x >> 5];
-  for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
-    const ChunkInfo ci = chunk_info(g, v, begin);
-    if (ci.q_lo > ci.q_hi) {
-      zero_gap(y, 1, ci.w_lo, ci.w_hi);
-      if (lane == 0) rec.row[2 * ci.local] = -1, rec.row[2 * ci.local + 1] = -1, rec.cont[ci.local] = 0;
-      continue;
-    }
-    const int64_t k = ci.local, s = ci.s, e = ci.e;
-    const int64_t ic0 = warp_owner(z.ptr, z.m, s);  // the last row is found by the walk itself
-    const bool head = ld64(z.ptr + ic0) < s;
-    int64_t ic1 = z.m - 1;
-    if (s == ci.q_lo && !head) zero_gap(y, 1, ci.w_lo, ld64(z.id + ic0) - 1);
-    int64_t head_row = -1, tail_row = -1;
-    int head_cont = 0;
-    double head_val = 0.0, tail_val = 0.0;
-    for (int64_t g0 = ic0; g0 <= ic1; g0 += 32) {
-      const int64_t r = g0 + lane;
-      const int64_t pa = r < z.m ? ld64(z.ptr + r) : INT64_MAX;
-      // rows of this group that start inside the chunk (or the head row)
-      const unsigned in = __ballot_sync(FULL, r == ic0 || pa <= e);
-      if (in != FULL) ic1 = g0 + 31 - __clz(in);  // the chunk's last row is in this group
-      const bool act = r <= ic1;
-      int64_t a = 0, b = -1, id = -1, nid = -1, rend = -1;
-      if (act) {
-        rend = ld64(z.ptr + r + 1) - 1;
-        a = max(pa, s);
-        b = min(rend, e);
-        id = ld64(z.id + r);
-        nid = r + 1 < z.m ? ld64(z.id + r + 1) : -1;
-      }
-      // the group's positions are contiguous: [first row's a, last row's b]
-      const int64_t lo = __shfl_sync(FULL, a, 0);
-      const int64_t hi = __shfl_sync(FULL, b, (int)min((int64_t)31, ic1 - g0));
-      const bool lng = act && b - a + 1 > kStageLong;
-      double sum = 0.0;
-      for (int64_t w0 = lo; w0 <= hi; w0 += WIN) {
-        const int wn = (int)min((int64_t)WIN, hi - w0 + 1);
-        stage_products<WIN>(crd, vals, x, w0, wn, sp, pol);
-        __syncwarp();
-        const int64_t wl = w0 + wn - 1;
-        if (act && !lng && a <= wl && b >= w0) {  // short row: serial, stored order
-          const int qb = (int)(min(b, wl) - w0);
-          for (int q = (int)(max(a, w0) - w0); q <= qb; q++) sum += sp[q];
-        }
-        unsigned lm = __ballot_sync(FULL, lng && a <= wl && b >= w0);
-        while (lm) {  // long rows: the warp reduces the row's slice of the window
-          const int t = __ffs(lm) - 1;
-          lm &= lm - 1;
-          const int qa = (int)(max(__shfl_sync(FULL, a, t), w0) - w0);
-          const int qb = (int)(min(__shfl_sync(FULL, b, t), wl) - w0);
-          double part = 0.0;
-          for (int q = qa + lane; q <= qb; q += 32) part += sp[q];
-          part = warp_sum(part);
-          if (lane == t) sum += part;
-        }
-        __syncwarp();
-      }
-      if (act) {
-        const bool is_head = r == ic0 && head;
-        const bool ends_here = rend <= e;
-        if (is_head) {
-          head_row = id;
-          head_val = sum;
-          head_cont = ends_here ? 0 : 1;
-        } else if (!ends_here) {
-          tail_row = id;
-          tail_val = sum;
-        } else {
-          y[id] = sum;
-        }
-      }
-      // empty rows up to the next non-empty one (bounded by W_c at a chunk
-      // end): short gaps by their lane, long ones by the whole warp
-      int64_t glo = 1, ghi = 0;
-      if (act && rend <= e) {
-        glo = id + 1;
-        ghi = rend == e ? (nid < 0 ? ci.w_hi : min(nid - 1, ci.w_hi)) : nid - 1;
-      }
-      const bool long_gap = ghi - glo + 1 > 64;
-      if (!long_gap)
-        for (int64_t rr = glo; rr <= ghi; rr++) y[rr] = 0.0;
-      unsigned gaps = __ballot_sync(FULL, long_gap);
-      while (gaps) {
-        const int t = __ffs(gaps) - 1;
-        gaps &= gaps - 1;
-        zero_gap(y, 1, __shfl_sync(FULL, glo, t), __shfl_sync(FULL, ghi, t));
-      }
-    }
-    // records of the chunk's first (head) and last (tail) rows
-    head_row = __shfl_sync(FULL, head_row, 0);  // the head row is lane 0 of the first group
-    head_val = __shfl_sync(FULL, head_val, 0);
-    head_cont = __shfl_sync(FULL, head_cont, 0);
-    const int tl = (int)((ic1 - ic0) & 31);  // the tail row is lane (ic1 - ic0) % 32 of the last group
-    tail_row = __shfl_sync(FULL, tail_row, tl);
-    tail_val = __shfl_sync(FULL, tail_val, tl);
-    if (lane == 0) {
-      rec.row[2 * k] = head_row;
-      rec.row[2 * k + 1] = tail_row;
-      rec.cont[k] = head_cont;
-      rec.val[2 * k] = head_val;
-      rec.val[2 * k + 1] = tail_val;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// SpMM N == 32 over the compacted view: half a warp per position, 128-bit
-// register gathers UNR pairs deep, crd/vals of the next window prefetched,
-// row switches from the window mask (no dependent loads on the critical path).
-// HOT selects the column index and the C-row load:
-//   0  int64 crd, every C row gathered with L2 evict_last;
-//   1  int32 crd with the hot-column bit (crd32h), hot rows evict_last, cold
-//      rows evict_first (two predicated uniform-policy loads);
-//   2  int32 crd with hot-copy slots (crd32x): a hot column reads its row from
-//      Chot, the per-call compact copy of the hot rows that the launch's L2
-//      access-policy window marks persisting; one plain load per position;
-//   3  plain int32 crd (crd32p), every C row evict_last (mode 0 with half
-//      the index bytes).
-template <int UNR, int MINB, int HOT, bool DYN = false>
-__global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
-                                                      const int32_t* __restrict__ crd32h,
-                                                      const double* __restrict__ vals,
-                                                      const double* __restrict__ C,
-                                                      double* __restrict__ A, ChunkRecs rec,
-                                                      const int64_t* __restrict__ counters,
-                                                      const double* __restrict__ Chot = nullptr) {
+  static_assert(2 * UNR < 32 && 32 % (2 * UNR) == 0, "groups tile the 32-position window");
+  constexpr unsigned kGroupMask = (1u << (2 * UNR)) - 1u;
   const int lane = lane_id();
   const int half = lane >> 4, hl = lane & 15;
+  z.m = nz_count(z);
   const int64_t begin = counters[1], end = counters[2];
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t pol_keep = l2_policy_evict_last();
-  const uint64_t pol_stream = l2_policy_evict_first();
   const double* Cl = C + 2 * hl;
-  const double* Hl = Chot + 2 * hl;
-  // DYN: chunks handed out by an atomic ticket (counters[3]) instead of a
-  // static grid stride, so warps that drew cheap chunks take more.
-  const int64_t tmax = end - begin;
-  for (int64_t t = DYN ? chunk_ticket(counters) : gw; t < tmax; t = DYN ? chunk_ticket(counters) : t + nw) {
-    const int64_t v = begin + t;
-    const ChunkInfo ci = chunk_info(g, v, begin);
+  const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
+  for (int64_t t = chunk_ticket(counters); t < end - begin; t = chunk_ticket(counters)) {
+    const ChunkInfo ci = chunk_info(g, begin + t, begin);
     if (ci.q_lo > ci.q_hi) {
       if (lane == 0) rec.row[2 * ci.local] = -1, rec.row[2 * ci.local + 1] = -1, rec.cont[ci.local] = 0;
       continue;
     }
-    const int64_t k = ci.local, s = ci.s, e = ci.e;
-    NzCursor c;
-    nz_start(z, c, s);
-    bool head = __shfl_sync(FULL, c.P0, 0) < s;
-    int64_t head_row = -1;
-    int head_cont = 0;
+    const int64_t s = ci.s;
+    const int ne = (int)(ci.e - s);  // last offset of the chunk
+    const int32_t* cp = crd32 + s;
+    const double* vp = vals + s;
+    NzCur32 c;
+    c.cb = warp_owner(z.ptr, z.m, s);  // compacted row holding position s
+    c.off = 0;
+    nz32_load(z, c.cb, s, c.P0, c.I0);
+    nz32_load(z, c.cb + 32, s, c.P1, c.I1);
+    bool head = __shfl_sync(FULL, c.P0, 0) < 0;  // the chunk's first row began before it
+    int cur = __shfl_sync(FULL, c.I0, 0);        // id of the current row
+    int head_row = -1;
     double2 acc = make_double2(0.0, 0.0);
-    // prefetched crd/vals of the next window
     int kn = 0;
     double vn = 0.0;
-    if (lane <= e - s) {
-      kn = HOT ? ld_i32_hint(crd32h + s + lane, pol_stream) : (int)ld_i64_hint(crd + s + lane, pol_stream);
-      vn = ld_f64_hint(vals + s + lane, pol_stream);
+    if (lane <= ne) {
+      kn = ld_i32_hint(cp + lane, pol_stream);
+      vn = ld_f64_hint(vp + lane, pol_stream);
     }
-    for (int64_t base = s; base <= e; base += 32) {
-      const int last_off = (int)min((int64_t)31, e - base);
-      const int cnt = last_off + 1;
+    for (int b0 = 0; b0 <= ne; b0 += 32) {
+      const int cnt = min(32, ne - b0 + 1);
       const int my_k = kn;
       const double my_v = vn;
-      if (base + 32 + lane <= e) {
-        kn = HOT ? ld_i32_hint(crd32h + base + 32 + lane, pol_stream)
-                 : (int)ld_i64_hint(crd + base + 32 + lane, pol_stream);
-        vn = ld_f64_hint(vals + base + 32 + lane, pol_stream);
+      kn = 0;
+      vn = 0.0;
+      if (b0 + 32 + lane <= ne) {
+        kn = ld_i32_hint(cp + b0 + 32 + lane, pol_stream);
+        vn = ld_f64_hint(vp + b0 + 32 + lane, pol_stream);
       }
-      const unsigned bm = nz_window_mask(c, base, base + last_off);
-      // Fixed-trip groups of 2*UNR positions: positions past `cnt` carry
-      // crd 0 / val 0 (their loads are predicated off), so the fast path is
-      // branch-free; one mask test per group selects the row-switch path.
+      // row starts after the current row inside [b0, b0 + cnt)
+      const int last = b0 + cnt - 1;
+      unsigned bm = __reduce_or_sync(
+          FULL, (lane > c.off && c.P0 >= b0 && c.P0 <= last) ? 1u << (c.P0 - b0) : 0u);
+      if (__shfl_sync(FULL, c.P0, 31) <= last)
+        bm |= __reduce_or_sync(FULL, (c.P1 >= b0 && c.P1 <= last) ? 1u << (c.P1 - b0) : 0u);
+      int j = c.off + 1;  // cursor slot of the next row to start
 #pragma unroll 1
-      for (int u = 0; u < 32; u += 2 * UNR) {
-        if (u >= cnt) break;
+      for (int u = 0; u < cnt; u += 2 * UNR) {
         double2 cv[UNR];
         double bv[UNR];
 #pragma unroll
@@ -656,75 +532,78 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
           const int p = u + 2 * i + half;
           const int kk = __shfl_sync(FULL, my_k, p);
           bv[i] = __shfl_sync(FULL, my_v, p);
-          const double* src = Cl + (int64_t)(kk & 0x7fffffff) * 32;
-          if (HOT == 2) {
-            const double* hsrc = (kk < 0 ? Hl : Cl) + (int64_t)(kk & 0x7fffffff) * 32;
-            cv[i] = p < cnt ? __ldg(reinterpret_cast<const double2*>(hsrc)) : make_double2(0.0, 0.0);
-          } else if (HOT == 1) {  // two uniform-policy loads instead of a per-lane policy
-            cv[i] = make_double2(0.0, 0.0);
-            if (p < cnt && kk < 0) cv[i] = ld_f64x2_hint(src, pol_keep);
-            if (p < cnt && kk >= 0) cv[i] = ld_f64x2_hint(src, pol_stream);
-          } else {
-            cv[i] = p < cnt ? ld_f64x2_hint(src, pol_keep) : make_double2(0.0, 0.0);
-          }
+          cv[i] = ld_f64x2_hint(Cl + (int64_t)kk * 32, pol_keep);
         }
-        const unsigned gm = (bm >> u) & ((1u << (2 * UNR)) - 1u);
-        if (gm == 0u) {
+        unsigned gm = (bm >> u) & kGroupMask;
+        if (gm == 0u && u + 2 * UNR <= cnt) {
 #pragma unroll
           for (int i = 0; i < UNR; i++) {
             acc.x = fma(bv[i], cv[i].x, acc.x);
             acc.y = fma(bv[i], cv[i].y, acc.y);
           }
-        } else {
+          continue;
+        }
+        // segments [lo, hi) of the group between row starts (and the chunk end)
+        const int lim = min(2 * UNR, cnt - u);
+        int lo = 0;
+        for (;;) {
+          const int hi = gm ? __ffs(gm) - 1 : lim;
 #pragma unroll
           for (int i = 0; i < UNR; i++) {
-            const unsigned two = (gm >> (2 * i)) & 3u;
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-              if ((two >> h) & 1u) {  // a new row starts at position u + 2i + h
-                double2 o;
-                o.x = acc.x + __shfl_xor_sync(FULL, acc.x, 16);
-                o.y = acc.y + __shfl_xor_sync(FULL, acc.y, 16);
-                const int64_t id = nz_get(c.I0, c.I1, (int)(c.ic - c.cb));
-                if (head) {
-                  if (lane < 16) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
-                  head_row = id;
-                  head_cont = 0;
-                  head = false;
-                } else if (lane < 16) {
-                  st_f64x2_hint(A + id * 32 + 2 * lane, o, pol_stream);
-                }
-                acc = make_double2(0.0, 0.0);
-                nz_advance(z, c, 1);
-              }
-              if (half == h) {
-                acc.x = fma(bv[i], cv[i].x, acc.x);
-                acc.y = fma(bv[i], cv[i].y, acc.y);
-              }
+            const int o = 2 * i + half;
+            if (o >= lo && o < hi) {
+              acc.x = fma(bv[i], cv[i].x, acc.x);
+              acc.y = fma(bv[i], cv[i].y, acc.y);
             }
           }
+          if (!gm) break;
+          // row `cur` ends before offset hi: flush it
+          double2 o;
+          o.x = acc.x + __shfl_xor_sync(FULL, acc.x, 16);
+          o.y = acc.y + __shfl_xor_sync(FULL, acc.y, 16);
+          if (head) {
+            if (lane < 16) reinterpret_cast<double2*>(rec.val + 2 * ci.local * 32)[lane] = o;
+            head_row = cur;
+            head = false;
+          } else if (lane < 16) {
+            st_f64x2_hint(A + (int64_t)cur * 32 + 2 * lane, o, pol_stream);
+          }
+          acc = make_double2(0.0, 0.0);
+          cur = shfl_pair(c.I0, c.I1, j);
+          j++;
+          lo = hi;
+          gm &= gm - 1u;
         }
       }
+      c.off = j - 1;
+      if (c.off >= 32) {  // slide the register window; the new block is far ahead
+        c.cb += 32;
+        c.off -= 32;
+        c.P0 = c.P1;
+        c.I0 = c.I1;
+        nz32_load(z, c.cb + 32, s, c.P1, c.I1);
+      }
     }
+    // chunk end: the current row ends exactly at the chunk end, or continues past it
     double2 o;
     o.x = acc.x + __shfl_xor_sync(FULL, acc.x, 16);
     o.y = acc.y + __shfl_xor_sync(FULL, acc.y, 16);
-    const int64_t next = nz_get(c.P0, c.P1, (int)(c.ic - c.cb) + 1);
-    const int64_t id = nz_get(c.I0, c.I1, (int)(c.ic - c.cb));
-    int64_t tail_row = -1;
-    if (next == e + 1) {
+    const int next = shfl_pair(c.P0, c.P1, c.off + 1);
+    const int64_t k = ci.local;
+    int tail_row = -1, head_cont = 0;
+    if (next == ne + 1) {
       if (head) {
         if (lane < 16) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
-        head_row = id, head_cont = 0;
+        head_row = cur;
       } else if (lane < 16) {
-        st_f64x2_hint(A + id * 32 + 2 * lane, o, pol_stream);
+        st_f64x2_hint(A + (int64_t)cur * 32 + 2 * lane, o, pol_stream);
       }
     } else if (head) {
       if (lane < 16) reinterpret_cast<double2*>(rec.val + 2 * k * 32)[lane] = o;
-      head_row = id, head_cont = 1;
+      head_row = cur, head_cont = 1;
     } else {
       if (lane < 16) reinterpret_cast<double2*>(rec.val + (2 * k + 1) * 32)[lane] = o;
-      tail_row = id;
+      tail_row = cur;
     }
     if (lane == 0) {
       rec.row[2 * k] = head_row;
@@ -761,6 +640,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm_nzv(WalkGeom g, NzView z,
   constexpr int GP = PPI * UNR;                // positions per group
   static_assert(GP <= 32, "a group must fit one 32-position window");
   const int lane = lane_id();
+  z.m = nz_count(z);
   const int sub = lane / LP, sl = lane % LP;
   const int64_t begin = counters[1], end = counters[2];
   const uint64_t pol_keep = l2_policy_evict_last();
@@ -936,6 +816,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_mttkrp32_nz(WalkGeom g, NzView
                                                       double* __restrict__ A, ChunkRecs rec,
                                                       const int64_t* __restrict__ counters) {
   const int lane = lane_id();
+  z.m = nz_count(z);
   const int half = lane >> 4, hl = lane & 15;
   const int64_t begin = counters[1], end = counters[2];
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
@@ -1110,50 +991,9 @@ __global__ void k_crd32h(const int64_t* __restrict__ crd, int64_t nnz, const int
   }
 }
 
-__global__ void k_iota32(int32_t* __restrict__ a, int64_t n) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    a[i] = (int32_t)i;
-}
-
 __global__ void k_crd_to_i32(const int64_t* __restrict__ crd, int64_t n, int32_t* __restrict__ out) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = (int32_t)crd[i];
-}
-
-// Hot-copy index: the first H entries of the columns sorted by descending
-// reference count get slots 0..H-1 (slot_of[col]); columns referenced once
-// are never worth a slot.
-__global__ void k_hot_slots(const int32_t* __restrict__ counts_desc, const int32_t* __restrict__ ids_desc,
-                            int64_t H, int32_t* __restrict__ slot_of, int32_t* __restrict__ hot_ids,
-                            int64_t* __restrict__ n_hot) {
-  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < H; r += (int64_t)gridDim.x * blockDim.x) {
-    const bool hot = counts_desc[r] >= 2;
-    if (hot) slot_of[ids_desc[r]] = (int32_t)r, hot_ids[r] = ids_desc[r];
-    if (hot && (r == H - 1 || counts_desc[r + 1] < 2)) *n_hot = r + 1;
-  }
-}
-
-// crd32x[q] = 0x80000000 | slot for a hot column, else the column.
-__global__ void k_crd32x(const int64_t* __restrict__ crd, int64_t nnz, const int32_t* __restrict__ slot_of,
-                         int32_t* __restrict__ out) {
-  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < nnz; q += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t col = ld64(crd + q);
-    const int32_t sl = slot_of[col];
-    out[q] = sl >= 0 ? (int32_t)(0x80000000u | (uint32_t)sl) : (int32_t)col;
-  }
-}
-
-// Chot[slot] = C[hot_ids[slot]] for W-wide rows (W even): a half-warp per row,
-// 128-bit loads and stores.
-__global__ void k_hot_gather(const double* __restrict__ C, const int32_t* __restrict__ hot_ids, int64_t H,
-                             int64_t W, double* __restrict__ Chot) {
-  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  const int64_t vec = W / 2;
-  for (int64_t i = t; i < H * vec; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = i / vec, l = i - r * vec;
-    const double2 v = __ldg(reinterpret_cast<const double2*>(C + (int64_t)hot_ids[r] * W) + l);
-    reinterpret_cast<double2*>(Chot + r * W)[l] = v;
-  }
 }
 
 }  // namespace spd
@@ -1187,6 +1027,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sddmm_nz(WalkGeom g, NzView z,
   static_assert(KT == 1 || KT == 2 || KT == 4 || KT == 8, "K must be 32, 64, 128 or 256");
   constexpr int NV = KT >= 2 ? KT / 2 : 1;
   const int lane = lane_id();
+  z.m = nz_count(z);
   const int64_t begin = counters[1], end = counters[2];
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;

@@ -669,65 +669,72 @@ static int occupancy_grid(spd_context* ctx, K kernel) {
 }
 
 // Compacted non-empty-row view of row pointer R of tensor t (cached on t).
-static NzView nz_view(spd_context* ctx, spd_tensor* t, const int64_t* R, int64_t nrows) {
+// Built without a host synchronisation: the row-id and start arrays are sized
+// by the row count (an upper bound of the non-empty rows) and the count stays
+// on the device (NzView::m_dev, read by the kernels); `need_host_m` also
+// copies it to the host (the SpMV leaf choice depends on it).
+static NzView nz_view(spd_context* ctx, spd_tensor* t, const int64_t* R, int64_t nrows, bool need_host_m = false) {
+  cudaStream_t s = ctx->stream;
+  auto host_m = [&](spd_tensor::NzCache& e) {
+    if (need_host_m && e.m < 0) {
+      SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters + 8, e.m_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+      SPD_CUDA(cudaStreamSynchronize(s));
+      e.m = ctx->pinned_counters[8];
+    }
+  };
   for (auto& e : t->nz)
-    if (e.R == R) return NzView{e.ptr, e.id, e.m};
+    if (e.R == R) {
+      host_m(e);
+      return NzView{e.ptr, e.id, e.m, e.m_dev};
+    }
   spd_tensor::NzCache* slot = nullptr;
   for (auto& e : t->nz)
     if (!e.R && (!slot || e.cap_id > slot->cap_id)) slot = &e;  // prefer reusable buffers
   if (!slot) {
     slot = &t->nz[0];
-    cudaFreeAsync(slot->ptr, ctx->stream);
-    cudaFreeAsync(slot->id, ctx->stream);
-    slot->ptr = slot->id = nullptr;
-    slot->cap_ptr = slot->cap_id = 0;
+    slot->R = nullptr;
   }
-  cudaStream_t s = ctx->stream;
   unsigned char* flags = nullptr;
-  int64_t* m_dev = nullptr;
   const int64_t nid = nrows > 0 ? nrows : 1;
   if (t->stage_flags_cap >= nid) {
     flags = t->stage_flags;  // a restaged tensor's staging buffer, idle here
   } else {
     SPD_CUDA(cudaMallocAsync((void**)&flags, nid, s));
   }
-  m_dev = (int64_t*)ctx->counters.reserve(sizeof(int64_t) * 16) + 8;
+  if (!slot->m_dev) SPD_CUDA(cudaMallocAsync((void**)&slot->m_dev, sizeof(int64_t), s));
   if (slot->cap_id < nid) {
     if (slot->id) cudaFreeAsync(slot->id, s);
+    if (slot->ptr) cudaFreeAsync(slot->ptr, s);
     SPD_CUDA(cudaMallocAsync((void**)&slot->id, sizeof(int64_t) * nid, s));
+    SPD_CUDA(cudaMallocAsync((void**)&slot->ptr, sizeof(int64_t) * (nid + 1), s));
     slot->cap_id = nid;
   }
-  SPD_CUDA(cudaMemsetAsync(m_dev, 0, sizeof(int64_t), s));
+  SPD_CUDA(cudaMemsetAsync(slot->m_dev, 0, sizeof(int64_t), s));
   if (nrows > 0) {
     k_nz_flags<<<(unsigned)std::min<int64_t>(ceil_div(nrows, 256), ctx->num_sms * 16), 256, 0, s>>>(R, nrows, flags);
     SPD_CHECK_LAUNCH();
     cub::CountingInputIterator<int64_t> it(0);
     size_t bytes = 0;
-    SPD_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, slot->id, m_dev, nrows, s));
+    SPD_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, slot->id, slot->m_dev, nrows, s));
     void* tmp = ctx->scratch[5].reserve(bytes);
-    SPD_CUDA(cub::DeviceSelect::Flagged(tmp, bytes, it, flags, slot->id, m_dev, nrows, s));
+    SPD_CUDA(cub::DeviceSelect::Flagged(tmp, bytes, it, flags, slot->id, slot->m_dev, nrows, s));
   }
-  SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters + 8, m_dev, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  SPD_CUDA(cudaStreamSynchronize(s));
-  slot->m = ctx->pinned_counters[8];
-  if (slot->cap_ptr < slot->m + 1) {
-    if (slot->ptr) cudaFreeAsync(slot->ptr, s);
-    SPD_CUDA(cudaMallocAsync((void**)&slot->ptr, sizeof(int64_t) * (slot->m + 1), s));
-    slot->cap_ptr = slot->m + 1;
-  }
-  k_nz_ptr<<<(unsigned)std::min<int64_t>(ceil_div(slot->m + 1, 256), ctx->num_sms * 16), 256, 0, s>>>(
-      R, nrows, slot->id, m_dev, slot->ptr);
+  k_nz_ptr<<<(unsigned)std::min<int64_t>(ceil_div(nid + 1, 256), ctx->num_sms * 16), 256, 0, s>>>(
+      R, nrows, slot->id, slot->m_dev, slot->ptr);
   SPD_CHECK_LAUNCH();
   if (flags != t->stage_flags) cudaFreeAsync(flags, s);
   slot->R = R;
+  slot->m = -1;
   ctx->launches += 3;
-  return NzView{slot->ptr, slot->id, slot->m};
+  host_m(*slot);
+  return NzView{slot->ptr, slot->id, slot->m, slot->m_dev};
 }
 
 // Non-empty rows of row pointer R (of t) inside each span [lo, hi]: two
 // binary searches over the compacted view's sorted row ids.
-__global__ void k_nonempty_in_spans(const int64_t* __restrict__ ids, int64_t m, const int64_t* __restrict__ spans,
-                                    int64_t nspans, int64_t* __restrict__ out) {
+__global__ void k_nonempty_in_spans(const int64_t* __restrict__ ids, const int64_t* __restrict__ m_dev,
+                                    const int64_t* __restrict__ spans, int64_t nspans, int64_t* __restrict__ out) {
+  const int64_t m = *m_dev;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nspans; j += (int64_t)gridDim.x * blockDim.x) {
     const int64_t lo = spans[2 * j], hi = spans[2 * j + 1];
     if (lo > hi) {
@@ -757,7 +764,7 @@ std::vector<int64_t> nonempty_in_spans(spd_context* ctx, spd_tensor* t, const in
   cudaStream_t s = ctx->stream;
   int64_t* d = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * 3 * ns);
   SPD_CUDA(cudaMemcpyAsync(d, spans.data(), sizeof(int64_t) * 2 * ns, cudaMemcpyHostToDevice, s));
-  k_nonempty_in_spans<<<(unsigned)std::min<int64_t>(ceil_div(ns, 256), 1024), 256, 0, s>>>(z.id, z.m, d, ns,
+  k_nonempty_in_spans<<<(unsigned)std::min<int64_t>(ceil_div(ns, 256), 1024), 256, 0, s>>>(z.id, z.m_dev, d, ns,
                                                                                              d + 2 * ns);
   SPD_CHECK_LAUNCH();
   SPD_CUDA(cudaMemcpyAsync(out.data(), d + 2 * ns, sizeof(int64_t) * ns, cudaMemcpyDeviceToHost, s));
@@ -808,111 +815,6 @@ static const int32_t* hot_crd(spd_context* ctx, spd_tensor* t, int64_t rowbytes)
   cudaFreeAsync(sorted, s);
   t->crd32h_rowbytes = rowbytes;
   return t->crd32h;
-}
-
-// Hot-copy index for dense rows of `rowbytes` (cached on t): the most
-// referenced columns (count >= 2) whose rows fit in SPD_HOT_FRAC of L2 get
-// slots in a compact per-call copy of C; crd32x addresses slot or column.
-static void hot_copy_index(spd_context* ctx, spd_tensor* t, int64_t rowbytes) {
-  if (t->crd32x && t->crd32x_rowbytes == rowbytes) return;
-  const spd_level_store& L = t->levels.back();
-  const int64_t lo = t->piece ? t->piece_lo : 0;
-  const int64_t nnz = t->piece ? t->piece_hi - t->piece_lo + 1 : L.positions;
-  const int64_t ncols = t->dims[t->mode_order[t->groups.back()[0]]];
-  cudaStream_t s = ctx->stream;
-  int l2 = 0;
-  SPD_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device));
-  static double frac = [] {
-    const char* e = getenv("SPD_HOT_FRAC");
-    return e ? atof(e) : 0.6;
-  }();
-  const int64_t k = std::min<int64_t>(ncols, std::max<int64_t>(1, (int64_t)(frac * l2) / rowbytes));
-  const int64_t nc = ncols > 0 ? ncols : 1;
-  int32_t *counts = nullptr, *counts_desc = nullptr, *ids = nullptr, *ids_desc = nullptr, *slot_of = nullptr;
-  int64_t* n_hot = nullptr;
-  SPD_CUDA(cudaMallocAsync((void**)&counts, sizeof(int32_t) * nc, s));
-  SPD_CUDA(cudaMallocAsync((void**)&counts_desc, sizeof(int32_t) * nc, s));
-  SPD_CUDA(cudaMallocAsync((void**)&ids, sizeof(int32_t) * nc, s));
-  SPD_CUDA(cudaMallocAsync((void**)&ids_desc, sizeof(int32_t) * nc, s));
-  SPD_CUDA(cudaMallocAsync((void**)&slot_of, sizeof(int32_t) * nc, s));
-  SPD_CUDA(cudaMallocAsync((void**)&n_hot, sizeof(int64_t), s));
-  SPD_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * nc, s));
-  SPD_CUDA(cudaMemsetAsync(slot_of, 0xff, sizeof(int32_t) * nc, s));
-  SPD_CUDA(cudaMemsetAsync(n_hot, 0, sizeof(int64_t), s));
-  if (!t->crd32x_alloc)
-    SPD_CUDA(cudaMallocAsync((void**)&t->crd32x_alloc, sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
-  t->crd32x = t->crd32x_alloc - lo;  // indexed by global position
-  if (t->hot_ids) cudaFreeAsync(t->hot_ids, s);
-  SPD_CUDA(cudaMallocAsync((void**)&t->hot_ids, sizeof(int32_t) * k, s));
-  const unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(nnz, 256), 1), ctx->num_sms * 16);
-  if (nnz > 0 && ncols > 0) {
-    k_col_count<<<grid, 256, 0, s>>>(L.crd + lo, nnz, counts);
-    SPD_CHECK_LAUNCH();
-    k_iota32<<<(unsigned)std::min<int64_t>(ceil_div(ncols, 256), ctx->num_sms * 16), 256, 0, s>>>(ids, ncols);
-    SPD_CHECK_LAUNCH();
-    size_t bytes = 0;
-    SPD_CUDA(cub::DeviceRadixSort::SortPairsDescending(nullptr, bytes, counts, counts_desc, ids, ids_desc, ncols, 0,
-                                                       32, s));
-    void* tmp = ctx->scratch[5].reserve(bytes);
-    SPD_CUDA(cub::DeviceRadixSort::SortPairsDescending(tmp, bytes, counts, counts_desc, ids, ids_desc, ncols, 0, 32,
-                                                       s));
-    k_hot_slots<<<(unsigned)std::min<int64_t>(ceil_div(k, 256), ctx->num_sms * 16), 256, 0, s>>>(
-        counts_desc, ids_desc, k, slot_of, t->hot_ids, n_hot);
-    SPD_CHECK_LAUNCH();
-    k_crd32x<<<grid, 256, 0, s>>>(L.crd + lo, nnz, slot_of, t->crd32x_alloc);
-    SPD_CHECK_LAUNCH();
-    ctx->launches += 5;
-  }
-  SPD_CUDA(cudaMemcpyAsync(ctx->pinned_counters + 9, n_hot, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  SPD_CUDA(cudaStreamSynchronize(s));
-  t->hot_n = ctx->pinned_counters[9];
-  for (void* p : {(void*)counts, (void*)counts_desc, (void*)ids, (void*)ids_desc, (void*)slot_of, (void*)n_hot})
-    cudaFreeAsync(p, s);
-  t->crd32x_rowbytes = rowbytes;
-}
-
-// L2 set-aside for persisting accesses (once per context): the hot-copy
-// window of the SpMM leaf.  0 when the device offers none.
-static int64_t persist_setaside(spd_context* ctx, int64_t want) {
-  if (ctx->persist_bytes >= 0) return ctx->persist_bytes;
-  int maxp = 0;
-  SPD_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, ctx->device));
-  const size_t b = (size_t)std::min<int64_t>(want, maxp);
-  if (b > 0 && cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, b) == cudaSuccess) {
-    size_t got = 0;
-    cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
-    ctx->persist_bytes = (int64_t)got;
-  } else {
-    cudaGetLastError();
-    ctx->persist_bytes = 0;
-  }
-  return ctx->persist_bytes;
-}
-
-static bool dyn_enabled() {
-  static int v = [] {
-    const char* e = getenv("SPD_DYN");
-    return e ? atoi(e) : 1;
-  }();
-  return v != 0;
-}
-
-// The compacted-row SpMM for N in {8, 16, 64, 128} (k_spmm_nzv);
-// SPD_SPMMV=0 selects the lane-per-column walks instead.
-static bool spmmv_enabled() {
-  static int v = [] {
-    const char* e = getenv("SPD_SPMMV");
-    return e ? atoi(e) : 1;
-  }();
-  return v != 0;
-}
-
-static int hot_enabled() {
-  static int v = [] {
-    const char* e = getenv("SPD_HOT");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
 }
 
 // Compacted-column SpMV (SPD_XC: 1 auto, 0 off, 2 always): when x is wider
@@ -1000,32 +902,11 @@ static bool spmv_rows_mode(int64_t nnz, int64_t m) {
   return m > 0 && nnz <= kRowsAvg * m;
 }
 
-// Staged-product SpMV / SpTTV leaf (k_spmv_stage), SPD_SPMV_STAGE=1; off by
-// default: R-MAT SpMV leaf 1.30 ms vs 1.00 ms for k_spmv_rows, C1 0.142 vs
-// 0.116 ms, C4 SpTTV 0.254 vs 0.190 ms (profiles/README.md).
-static bool spmv_stage_mode() {
-  static int v = [] {
-    const char* e = getenv("SPD_SPMV_STAGE");
-    return e ? atoi(e) : 0;
-  }();
-  return v != 0;
-}
-
-// Whether an op walks the compacted view (default) -- SPD_NZ=0 selects the
-// direct row-pointer walks (kept for comparison).
-static bool nz_enabled() {
-  static int v = [] {
-    const char* e = getenv("SPD_NZ");
-    return e ? atoi(e) : 1;
-  }();
-  return v != 0;
-}
-
 // SDDMM over the compacted view (called by sddmm.cu): K = 128, D j-major.
 bool sddmm_nz_launch(spd_context* ctx, const spd_tensor* B, const WalkGeom& g, const double* C,
                      const double* D, int64_t K, int64_t dk, int64_t dj, double* Avals,
                      const int64_t* counters) {
-  if (!nz_enabled() || (K != 32 && K != 64 && K != 128 && K != 256) || dk != 1 || dj != K ||
+  if ((K != 32 && K != 64 && K != 128 && K != 256) || dk != 1 || dj != K ||
       B->dims[1] >= (int64_t(1) << 31))
     return false;
   NzView z = nz_view(ctx, const_cast<spd_tensor*>(B), g.R, g.nrows);
@@ -1059,12 +940,37 @@ bool sddmm_nz_launch(spd_context* ctx, const spd_tensor* B, const WalkGeom& g, c
   return true;
 }
 
+// int32 copy of the leaf crd (cached on t, rebuilt after a restage): the
+// N = 32 SpMM leaf streams 4-byte columns and forms addresses with one
+// 32x32->64-bit multiply-add.  Indexed by global position (offset for a piece).
+static const int32_t* crd32_index(spd_context* ctx, spd_tensor* t) {
+  if (t->crd32) return t->crd32;
+  const spd_level_store& L = t->levels.back();
+  const int64_t lo = t->piece ? t->piece_lo : 0;
+  const int64_t nnz = t->piece ? t->piece_hi - t->piece_lo + 1 : L.positions;
+  cudaStream_t s = ctx->stream;
+  if (!t->crd32_alloc || t->crd32_cap < nnz) {
+    if (t->crd32_alloc) cudaFreeAsync(t->crd32_alloc, s);
+    SPD_CUDA(cudaMallocAsync((void**)&t->crd32_alloc, sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
+    t->crd32_cap = nnz;
+  }
+  if (nnz > 0) {
+    k_crd_to_i32<<<(unsigned)std::min<int64_t>(ceil_div(nnz, 256), ctx->num_sms * 16), 256, 0, s>>>(L.crd + lo, nnz,
+                                                                                                   t->crd32_alloc);
+    SPD_CHECK_LAUNCH();
+    ctx->launches++;
+  }
+  t->crd32 = t->crd32_alloc - lo;
+  return t->crd32;
+}
+
 static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_t count,
                         spd_stats* stats) {
   HostTrace ht("rowwalk");
   checked(ctx);
   const spd_tensor* B = a.B;
   if (!B) throw ValidationError("null tensor");
+  settle_restage(B);
   require_partition(ctx, B, first, count, true);
   activate(ctx);
   const int nl = (int)B->levels.size();
@@ -1080,6 +986,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
              B->levels[0].dom.size() != 1) {
     throw ValidationError("unsupported on gpu: this kernel needs a ds (CSR-like) matrix");
   }
+  require_identity_order(B, csf ? "the CSF operand" : "the sparse operand");
   if (ctx->split == SplitKind::NonZero && ctx->split_level != nl - 1)
     throw ValidationError("unsupported on gpu: nonzero split must be on the leaf level");
   if (a.W < 0 || a.W > 128) throw ValidationError("unsupported on gpu: inner extent must be in [0, 128]");
@@ -1143,9 +1050,9 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
     }();
     if (ch_spmv >= 32 && (a.op == Op::SpMV || a.op == Op::SpTTV)) g.CH = ch_spmv;
   }
-  const bool spmm32 = a.op == Op::SpMM && a.W == 32 && B->dims[1] < (int64_t(1) << 31);
+  const bool spmm32 = a.op == Op::SpMM && a.W == 32 && B->dims[1] < (int64_t(1) << 31) && g.nrows < (int64_t(1) << 31);
   const bool spmmv = a.op == Op::SpMM && (a.W == 8 || a.W == 16 || a.W == 64 || a.W == 128) &&
-                     B->dims[1] < (int64_t(1) << 31) && spmmv_enabled();
+                     B->dims[1] < (int64_t(1) << 31);
   const int64_t W = a.W > 0 ? a.W : 1;
   const int64_t max_chunks = nnz / g.CH + 2 * P + 2;
 
@@ -1177,13 +1084,14 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   const bool mttkrp32 = a.op == Op::SpMTTKRP && a.W == 32 && B->dims[1] < (int64_t(1) << 31) &&
                         B->dims[2] < (int64_t(1) << 31);
   const bool mttkrpv = a.op == Op::SpMTTKRP && (a.W == 8 || a.W == 16 || a.W == 64 || a.W == 128) &&
-                       B->dims[1] < (int64_t(1) << 31) && B->dims[2] < (int64_t(1) << 31) && spmmv_enabled();
-  const bool use_nz = nz_enabled() && (a.op == Op::SpMV || a.op == Op::SpTTV || mttkrp32 || mttkrpv ||
-                                       spmm32 || spmmv);
-  NzView z{nullptr, nullptr, 0};
+                       B->dims[1] < (int64_t(1) << 31) && B->dims[2] < (int64_t(1) << 31);
+  // the compacted-row walks cover SpMV / SpTTV and the widths with a
+  // specialised leaf; other widths use the lane-per-column walks
+  const bool use_nz = a.op == Op::SpMV || a.op == Op::SpTTV || mttkrp32 || mttkrpv || spmm32 || spmmv;
+  NzView z{nullptr, nullptr, 0, nullptr};
   bool zero_joined = false;
   if (use_nz) {
-    z = nz_view(ctx, const_cast<spd_tensor*>(B), g.R, g.nrows);
+    z = nz_view(ctx, const_cast<spd_tensor*>(B), g.R, g.nrows, a.op == Op::SpMV || a.op == Op::SpTTV);
     ht.mark("nz_view");
     // SpMV/SpTTV walks zero the empty rows between consecutive non-empty
     // rows themselves (8 bytes each); the W-wide outputs use this pass.
@@ -1266,106 +1174,11 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
         SPD_SPMMV(128, 2, 4)
 #undef SPD_SPMMV
       }
-    } else if (a.op == Op::SpMM && hot_enabled() == 3 && !B->piece) {  // int32 crd, no hot set
-      spd_tensor* Bm = const_cast<spd_tensor*>(B);
-      if (!Bm->crd32p) {
-        SPD_CUDA(cudaMallocAsync((void**)&Bm->crd32p, sizeof(int32_t) * (nnz > 0 ? nnz : 1), s));
-        k_crd_to_i32<<<(unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(nnz, 256), 1), ctx->num_sms * 16), 256,
-                       0, s>>>(leaf.crd, nnz, Bm->crd32p);
-        SPD_CHECK_LAUNCH();
-      }
+    } else if (a.op == Op::SpMM) {  // N == 32 (C2): the lean compacted-row leaf
+      const int32_t* c32 = crd32_index(ctx, const_cast<spd_tensor*>(B));
       static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, 3, true>);
-      k_spmm32_nz<4, 4, 3, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, Bm->crd32p, B->vals, a.x, a.out, rec,
-                                                         col.counters);
-    } else if (a.op == Op::SpMM && hot_enabled() == 2) {
-      // hot-copy leaf: gather the hot rows of C into a compact buffer that
-      // an L2 access-policy window keeps persisting across the leaf
-      spd_tensor* Bm = const_cast<spd_tensor*>(B);
-      hot_copy_index(ctx, Bm, 256);
-      const int64_t H = Bm->hot_n;
-      double* Chot = (double*)ctx->scratch[6].reserve(sizeof(double) * 32 * (H > 0 ? H : 1));
-      const int64_t win = H * 256;
-      static const bool persist = [] {
-        const char* e = getenv("SPD_PERSIST");
-        return e ? atoi(e) != 0 : true;
-      }();
-      const int64_t setaside = persist ? persist_setaside(ctx, win) : 0;
-      cudaLaunchAttribute attr[1];
-      int nattr = 0;
-      if (setaside > 0 && win > 0) {
-        int maxwin = 0;
-        SPD_CUDA(cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, ctx->device));
-        attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
-        attr[0].val.accessPolicyWindow.base_ptr = Chot;
-        attr[0].val.accessPolicyWindow.num_bytes = (size_t)std::min<int64_t>(win, maxwin);
-        attr[0].val.accessPolicyWindow.hitRatio =
-            (float)std::min(1.0, (double)setaside / (double)attr[0].val.accessPolicyWindow.num_bytes);
-        attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-        attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-        nattr = 1;
-      }
-      if (H > 0) {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3((unsigned)std::min<int64_t>(ceil_div(H * 16, 256), ctx->num_sms * 8));
-        cfg.blockDim = dim3(256);
-        cfg.stream = s;
-        cfg.attrs = attr;
-        cfg.numAttrs = nattr;
-        SPD_CUDA(cudaLaunchKernelEx(&cfg, k_hot_gather, (const double*)a.x, (const int32_t*)Bm->hot_ids, H,
-                                    (int64_t)32, Chot));
-        launches++;
-      }
-      static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, 2, true>);
-      cudaLaunchConfig_t cfg{};
-      cfg.gridDim = dim3(grid);
-      cfg.blockDim = dim3(kBlock);
-      cfg.stream = s;
-      cfg.attrs = attr;
-      cfg.numAttrs = nattr;
-      SPD_CUDA(cudaLaunchKernelEx(&cfg, k_spmm32_nz<4, 4, 2, true>, g, z, (const int64_t*)leaf.crd,
-                                  (const int32_t*)Bm->crd32x, (const double*)B->vals, (const double*)a.x, a.out,
-                                  rec, (const int64_t*)col.counters, (const double*)Chot));
-    } else if (a.op == Op::SpMM && hot_enabled()) {
-      const int32_t* h = hot_crd(ctx, const_cast<spd_tensor*>(B), 256);
-      static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, 1, true>);
-      k_spmm32_nz<4, 4, 1, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, h, B->vals, a.x, a.out, rec,
-                                                            col.counters);
-    } else if (a.op == Op::SpMM && dyn_enabled()) {
-      // production SpMM leaf: chunks by atomic ticket (27% faster than the
-      // static grid stride on the R-MAT step, profiles/README.md)
-      static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, 0, true>);
-      k_spmm32_nz<4, 4, 0, true><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
-                                                             col.counters);
-    } else if (a.op == Op::SpMM) {  // static grid stride (SPD_DYN=0, comparison only)
-      static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4, 0>);
-      k_spmm32_nz<4, 4, 0><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, nullptr, B->vals, a.x, a.out, rec,
-                                                       col.counters);
-    } else if (spmv_stage_mode()) {  // staged products, lane per row from shared memory
-      static int minb_env = [] {
-        const char* e = getenv("SPD_STAGE_MINB");
-        return e ? atoi(e) : 4;
-      }();
-      static int win_env = [] {
-        const char* e = getenv("SPD_STAGE_WIN");
-        return e ? atoi(e) : 256;
-      }();
-#define SPD_STAGE(MB, WN)                                                                                \
-  do {                                                                                                   \
-    static int gr = 0;                                                                                   \
-    if (!gr) gr = occupancy_grid(ctx, k_spmv_stage<MB, WN>);                                            \
-    k_spmv_stage<MB, WN><<<gr, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters); \
-  } while (0)
-      if (win_env == 128) {
-        if (minb_env == 8) SPD_STAGE(8, 128); else if (minb_env == 6) SPD_STAGE(6, 128); else SPD_STAGE(4, 128);
-      } else {
-        if (minb_env == 6) SPD_STAGE(6, 256); else if (minb_env == 3) SPD_STAGE(3, 256); else SPD_STAGE(4, 256);
-      }
-#undef SPD_STAGE
+      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4>);
+      k_spmm32_nz<4, 4><<<grid, kBlock, 0, s>>>(g, z, c32, B->vals, a.x, a.out, rec, col.counters);
     } else if (spmv_rows_mode(nnz, z.m)) {  // short rows: a lane per row
       // 6 CTAs/SM (40 registers, a few spills) wins on large matrices
       // (R-MAT leaf 1.11 -> 1.045 ms), 4 on small ones (C1 / C4)

@@ -172,6 +172,7 @@ static void run_partition(spd_context* ctx, const spd_tensor* t, int level, int6
   if (pieces < 1) throw ValidationError("pieces must be positive");
   if (t->levels.empty()) throw ValidationError("cannot partition a rank-0 tensor");
   activate(ctx);
+  settle_restage(t);
   TreeView v = make_view(t);
   ctx->colors_dev.reserve(sizeof(DevColor) * pieces);
   DevColor* cols = (DevColor*)ctx->colors_dev.ptr;

@@ -13,6 +13,7 @@
 // run on it unchanged for that colour.  The bytes each GPU received are
 // returned (the placement's cost, reported apart from compute).
 #include <algorithm>
+#include <string>
 
 #include "common.cuh"
 
@@ -35,27 +36,35 @@ void run_place(spd_context* ctx, int root, const spd_tensor* whole, int split, s
   activate(ctx);
   cudaStream_t s = ctx->stream;
   const bool is_root = ctx->rank == root;
-  // header: order, dims (2), kinds, mode order, nnz
+  // header: order, dims (2), mode order, nnz, rows, root status.  The root's
+  // input checks travel in the header, so every rank fails together instead
+  // of the others waiting in a collective the root never joins.
   int64_t hdr[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  std::string root_error;
   if (is_root) {
-    if (!whole) throw ValidationError("the root must pass the whole tensor");
-    if (whole->piece) throw ValidationError("cannot place a piece");
-    if (whole->levels.size() != 2 || whole->levels[0].kind != SPD_DENSE ||
-        whole->levels[1].kind != SPD_COMPRESSED)
-      throw ValidationError("unsupported on gpu: placement of ds (CSR-like) matrices");
-    hdr[0] = whole->order;
-    hdr[1] = whole->dims[0];
-    hdr[2] = whole->dims[1];
-    hdr[3] = whole->mode_order[0];
-    hdr[4] = whole->mode_order[1];
-    hdr[5] = whole->levels[1].positions;
-    hdr[6] = whole->levels[1].parent_positions;
+    if (!whole) root_error = "the root must pass the whole tensor";
+    else if (whole->piece) root_error = "cannot place a piece";
+    else if (whole->levels.size() != 2 || whole->levels[0].kind != SPD_DENSE ||
+             whole->levels[1].kind != SPD_COMPRESSED)
+      root_error = "unsupported on gpu: placement of ds (CSR-like) matrices";
+    if (root_error.empty()) {
+      hdr[0] = whole->order;
+      hdr[1] = whole->dims[0];
+      hdr[2] = whole->dims[1];
+      hdr[3] = whole->mode_order[0];
+      hdr[4] = whole->mode_order[1];
+      hdr[5] = whole->levels[1].positions;
+      hdr[6] = whole->levels[1].parent_positions;
+    } else {
+      hdr[7] = 1;
+    }
   }
   int64_t* dh = (int64_t*)ctx->counters.reserve(sizeof(hdr));
   SPD_CUDA(cudaMemcpyAsync(dh, hdr, sizeof(hdr), cudaMemcpyHostToDevice, s));
   SPD_NCCL(ncclBroadcast(dh, dh, 8, ncclInt64, root, ctx->comm, s));
   SPD_CUDA(cudaMemcpyAsync(hdr, dh, sizeof(hdr), cudaMemcpyDeviceToHost, s));
   SPD_CUDA(cudaStreamSynchronize(s));
+  if (hdr[7]) throw ValidationError(is_root ? root_error : "spd_tensor_place: the root rejected its input");
   const int64_t dims[2] = {hdr[1], hdr[2]};
   const int kinds[2] = {SPD_DENSE, SPD_COMPRESSED};
   const int mo[2] = {(int)hdr[3], (int)hdr[4]};
@@ -87,8 +96,9 @@ void run_place(spd_context* ctx, int root, const spd_tensor* whole, int split, s
     t->piece_lo = mine.lo;
     t->piece_hi = mine.hi;
     const int64_t cnt = std::max<int64_t>(mine.hi - mine.lo + 1, 0);
-    t->piece_crd = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * std::max<int64_t>(cnt, 1));
-    t->piece_vals = (double*)dev_alloc(ctx, sizeof(double) * std::max<int64_t>(cnt, 1));
+    t->piece_cap = std::max<int64_t>(cnt, 1);  // a placed piece can be re-staged from the host later
+    t->piece_crd = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * t->piece_cap);
+    t->piece_vals = (double*)dev_alloc(ctx, sizeof(double) * t->piece_cap);
     L.crd = t->piece_crd - mine.lo;  // indexed by global position
     t->vals = t->piece_vals - mine.lo;
     SPD_NCCL(ncclGroupStart());
@@ -294,6 +304,81 @@ void run_ledger(spd_context* ctx, const spd_tensor* t, int need_split, int held_
   }
 }
 
+// missing_count (sim.cpp:76-84) for many (needed, held) pairs of sorted,
+// duplicate-free index sets at once: one thread per needed entry, a binary
+// search in its pair's held set, warp-aggregated counts per pair.
+__global__ void k_missing(const int64_t* __restrict__ need, const int64_t* __restrict__ need_off,
+                          const int64_t* __restrict__ held, const int64_t* __restrict__ held_off,
+                          const int32_t* __restrict__ pair_of, int64_t total,
+                          unsigned long long* __restrict__ missing) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t p = pair_of[i];
+    const int64_t v = need[i];
+    int64_t lo = held_off[p], hi = held_off[p + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (held[mid] < v) lo = mid + 1; else hi = mid;
+    }
+    const bool miss = lo == held_off[p + 1] || held[lo] != v;
+    if (miss) atomicAdd(missing + p, 1ull);
+  }
+}
+
+__global__ void k_pair_of(const int64_t* __restrict__ need_off, int64_t npairs, int32_t* __restrict__ pair_of) {
+  for (int64_t p = blockIdx.x; p < npairs; p += gridDim.x)
+    for (int64_t i = need_off[p] + threadIdx.x; i < need_off[p + 1]; i += blockDim.x) pair_of[i] = (int32_t)p;
+}
+
+void run_ledger_missing(spd_context* ctx, int64_t npairs, const int64_t* const* needed, const int64_t* n_needed,
+                        const int64_t* const* held, const int64_t* n_held, int64_t* missing) {
+  checked(ctx);
+  if (npairs < 0) throw ValidationError("npairs must be non-negative");
+  if (npairs == 0) return;
+  if (!needed || !n_needed || !held || !n_held || !missing) throw ValidationError("null argument");
+  if (npairs >= (int64_t(1) << 31)) throw ValidationError("too many set pairs");
+  activate(ctx);
+  cudaStream_t s = ctx->stream;
+  std::vector<int64_t> noff(npairs + 1, 0), hoff(npairs + 1, 0);
+  for (int64_t p = 0; p < npairs; p++) {
+    if (n_needed[p] < 0 || n_held[p] < 0) throw ValidationError("negative set size");
+    if ((n_needed[p] > 0 && !needed[p]) || (n_held[p] > 0 && !held[p])) throw ValidationError("null set");
+    noff[p + 1] = noff[p] + n_needed[p];
+    hoff[p + 1] = hoff[p] + n_held[p];
+  }
+  const int64_t tn = noff[npairs], th = hoff[npairs];
+  const size_t bytes = sizeof(int64_t) * (tn + th + 2 * (npairs + 1)) + sizeof(int32_t) * (tn + 1) +
+                       sizeof(unsigned long long) * npairs + 64;
+  char* buf = (char*)dev_alloc(ctx, bytes);
+  int64_t* d_need = (int64_t*)buf;
+  int64_t* d_held = d_need + tn;
+  int64_t* d_noff = d_held + th;
+  int64_t* d_hoff = d_noff + npairs + 1;
+  unsigned long long* d_miss = (unsigned long long*)(d_hoff + npairs + 1);
+  int32_t* d_pair = (int32_t*)(d_miss + npairs);
+  for (int64_t p = 0; p < npairs; p++) {
+    if (n_needed[p] > 0)
+      SPD_CUDA(cudaMemcpyAsync(d_need + noff[p], needed[p], sizeof(int64_t) * n_needed[p], cudaMemcpyHostToDevice, s));
+    if (n_held[p] > 0)
+      SPD_CUDA(cudaMemcpyAsync(d_held + hoff[p], held[p], sizeof(int64_t) * n_held[p], cudaMemcpyHostToDevice, s));
+  }
+  SPD_CUDA(cudaMemcpyAsync(d_noff, noff.data(), sizeof(int64_t) * (npairs + 1), cudaMemcpyHostToDevice, s));
+  SPD_CUDA(cudaMemcpyAsync(d_hoff, hoff.data(), sizeof(int64_t) * (npairs + 1), cudaMemcpyHostToDevice, s));
+  SPD_CUDA(cudaMemsetAsync(d_miss, 0, sizeof(unsigned long long) * npairs, s));
+  if (tn > 0) {
+    k_pair_of<<<(unsigned)std::min<int64_t>(npairs, 65535), 256, 0, s>>>(d_noff, npairs, d_pair);
+    SPD_CHECK_LAUNCH();
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(tn, 256), (int64_t)ctx->num_sms * 16);
+    k_missing<<<grid, 256, 0, s>>>(d_need, d_noff, d_held, d_hoff, d_pair, tn, d_miss);
+    SPD_CHECK_LAUNCH();
+    ctx->launches += 2;
+  }
+  std::vector<unsigned long long> out(npairs);
+  SPD_CUDA(cudaMemcpyAsync(out.data(), d_miss, sizeof(unsigned long long) * npairs, cudaMemcpyDeviceToHost, s));
+  SPD_CUDA(cudaStreamSynchronize(s));
+  dev_free(ctx, buf);
+  for (int64_t p = 0; p < npairs; p++) missing[p] = (int64_t)out[p];
+}
+
 }  // namespace
 
 }  // namespace spd
@@ -308,6 +393,12 @@ extern "C" int spd_tensor_repartition(spd_context* ctx, const spd_tensor* piece,
 extern "C" int spd_ledger_bytes(spd_context* ctx, const spd_tensor* t, int need_split, int held_split,
                                 int64_t pieces, int64_t* bytes_out) {
   return guarded([&] { run_ledger(ctx, t, need_split, held_split, pieces, bytes_out); });
+}
+
+extern "C" int spd_ledger_missing(spd_context* ctx, int64_t npairs, const int64_t* const* needed,
+                                  const int64_t* n_needed, const int64_t* const* held, const int64_t* n_held,
+                                  int64_t* missing) {
+  return guarded([&] { run_ledger_missing(ctx, npairs, needed, n_needed, held, n_held, missing); });
 }
 
 extern "C" int spd_tensor_place(spd_context* ctx, int root, const spd_tensor* whole, int split,

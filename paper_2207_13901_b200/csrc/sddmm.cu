@@ -110,11 +110,13 @@ static void run_sddmm(spd_context* ctx, const spd_tensor* B, const double* C, co
                       int64_t count, spd_stats* stats) {
   checked(ctx);
   if (!B) throw ValidationError("null tensor");
+  settle_restage(B);
   require_partition(ctx, B, first, count);
   activate(ctx);
   if (B->levels.size() != 2 || B->levels[0].kind != SPD_DENSE ||
       B->levels[1].kind != SPD_COMPRESSED)
     throw ValidationError("unsupported on gpu: SDDMM needs a ds (CSR-like) matrix");
+  require_identity_order(B, "the sparse operand");
   if (ctx->split == SplitKind::NonZero && ctx->split_level != 1)
     throw ValidationError("unsupported on gpu: nonzero split must be on the leaf level");
   if (K < 0 || K > 256) throw ValidationError("unsupported on gpu: K must be in [0, 256]");

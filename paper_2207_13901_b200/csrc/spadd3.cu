@@ -392,6 +392,7 @@ static void run_spadd3(spd_context* ctx, const spd_tensor* B, const spd_tensor* 
                        spd_stats* stats) {
   checked(ctx);
   if (!B || !C || !D || !A_out) throw ValidationError("null argument");
+  for (const spd_tensor* X : {B, C, D}) settle_restage(X);
   require_partition(ctx, B, first, count);
   activate(ctx);
   if (ctx->split != SplitKind::Universe)

@@ -355,9 +355,13 @@ class DeviceTensor:
                                         vals.ctypes.data_as(N.dblp), C.byref(h)))
         return DeviceTensor(ctx, h, t.dims, t.format)
 
-    def restage(self, t: SparseTensor):
+    def restage(self, t: SparseTensor, wait: bool = True):
         """spd_tensor_restage: new contents of the same geometry from host
-        arrays, into this tensor's device buffers (validated like upload)."""
+        arrays, into this tensor's device buffers.  The device validates the
+        staged pattern and commits it only if it is valid; the verdict is
+        reported by the next call on the tensor, or here when `wait` (the
+        default) synchronises the context -- a rejected restage leaves the
+        tensor's previous contents in place."""
         nl = len(t.levels)
         keep = []
         pos = (N.i64p * nl)()
@@ -371,6 +375,8 @@ class DeviceTensor:
                 crd[l] = c.ctypes.data_as(N.i64p)
         vals = np.ascontiguousarray(t.vals, dtype=np.float64)
         check(N.lib().spd_tensor_restage(self.ctx.h, self.h, pos, crd, vals.ctypes.data_as(N.dblp)))
+        if wait:
+            check(N.lib().spd_context_synchronize(self.ctx.h))
         return self
 
     @staticmethod

@@ -249,6 +249,23 @@ def test_restage_reuses_buffers_and_matches(ctx, kernel):
         bad.levels[1].crd = bad.levels[1].crd[::-1].copy()
         with pytest.raises(SpdValidationError):
             dev.restage(bad)
+        # validate-before-swap: the rejected pattern never reached the live
+        # arrays -- the tensor still holds B1 (advisor finding, round 1)
+        got = dev.download()
+        assert np.array_equal(got.levels[1].crd, B1.levels[1].crd) and np.array_equal(got.vals, B1.vals)
+        H.partition_nonzero(ctx, dev, 1, 3)
+        if kernel == "spmv":
+            H.spmv(ctx, dev, x, out, pieces=3)
+        else:
+            H.spmm(ctx, dev, x, N, out, pieces=3)
+        want = oracle_execute(kernel, {"B": B1, ("c" if kernel == "spmv" else "C"): c}, "nonzero", 3)
+        assert np.array_equal(out.cpu().numpy().reshape(-1), np.asarray(want["out"]).reshape(-1))
+        # without waiting, the verdict arrives with the next call on the tensor
+        dev.restage(bad, wait=False)
+        with pytest.raises(SpdValidationError):
+            ctx.synchronize()
+        got = dev.download()
+        assert np.array_equal(got.levels[1].crd, B1.levels[1].crd)
     finally:
         dev.close()
 

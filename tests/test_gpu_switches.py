@@ -1,5 +1,5 @@
-"""Every non-default leaf variant kept behind a switch
-passes the same parity checks as the default path.
+"""Every leaf choice that an automatic rule or a tuning knob can flip
+ passes the same parity checks as the default path.
 
 The switches are read once per process, so each variant runs the random-
 instance and hub-row parity tests of test_gpu_parity.py in a subprocess
@@ -16,16 +16,10 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 VARIANTS = [
-    {"SPD_HOT": "1"},  # per-access evict_last / evict_first C-row loads
-    {"SPD_HOT": "2"},  # hot-row copy under a persisting window
-    {"SPD_HOT": "3"},  # plain int32 crd
-    {"SPD_SPMV_STAGE": "1"},  # staged-product SpMV / SpTTV
-    {"SPD_SPMV_ROWS": "0"},  # window-scan SpMV instead of lane per row
-    {"SPD_SPMV_ROWS": "1"},
-    {"SPD_NZ": "0"},  # direct row-pointer walks
-    {"SPD_DYN": "0"},  # static grid stride for the N=32 SpMM leaf
-    {"SPD_SPMMV": "0"},  # lane-per-column SpMM / SpMTTKRP walks for N != 32
-    {"SPD_ZCONC": "0"},  # zero-fill before the leaf
+    {"SPD_SPMV_ROWS": "0"},  # window-scan SpMV (the long-row leaf) on every matrix
+    {"SPD_SPMV_ROWS": "1"},  # lane-per-row SpMV on every matrix
+    {"SPD_ZCONC": "0"},  # zero-fill before the leaf instead of concurrent with it
+    {"SPD_CH": "64"},  # tiny SpMM / SpMTTKRP chunks: every row crosses chunk records
     {"SPD_XC": "2"},  # compacted-column SpMV on every matrix
     {"SPD_XC": "0"},  # never (the wide-x test then reads x directly)
 ]

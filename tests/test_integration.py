@@ -106,3 +106,92 @@ def test_sss_plan_with_gpu_execute(gpu_lib, kernel):
         got = ob.RefRun(spec["expr"], spec["nonzero"], pieces, out_fmt, inputs, mode="gpu", lib=gpu_lib).ok()
         assert np.array_equal(want.output()[1], got.output()[1])
         assert want.stats()["work"] == got.stats()["work"]
+
+
+def _stats_json(run):
+    import json
+
+    return json.loads(run.L.ref_stats_json(run.h).decode())
+
+
+# Explicit placements (tensor distribution notation): row blocks,
+# nonzero blocks and replication, so the ledger charges real bytes.
+EXPLICIT_TDN = {
+    "spmv": {"B": "B(x, y) onto M(x)", "c": "c(x) onto M(x)", "a": "a(x) onto M(x)"},
+    "spmm": {"B": "B(x, y) fuse(x, y -> f) onto M(~f)", "C": "C(x, y) onto M(x)", "A": "A(x, y) onto M(x)"},
+    "sddmm": {"B": "B(x, y) onto M(x)", "C": "C(x, y) onto M(z)", "D": "D(x, y) onto M(x)", "A": "A(x, y) onto M(x)"},
+    "spttv": {"B": "B(x, y, z) onto M(x)", "c": "c(x) onto M(x)", "A": "A(x, y) onto M(x)"},
+    "spmttkrp": {"B": "B(x, y, z) onto M(x)", "C": "C(x, y) onto M(x)", "D": "D(x, y) onto M(z)",
+                 "A": "A(x, y) onto M(x)"},
+    "spadd3": {"B": "B(x, y) onto M(x)", "C": "C(x, y) fuse(x, y -> f) onto M(~f)", "D": "D(x, y) onto M(z)",
+               "A": "A(x, y) onto M(x)"},
+}
+
+
+@pytest.mark.parametrize("kernel", list(KERNELS))
+@pytest.mark.parametrize("schedule", ["row", "nonzero"])
+@pytest.mark.parametrize("tdns", ["default", "explicit"])
+def test_residency_ledger_matches_reference(gpu_lib, kernel, schedule, tdns):
+    """execute_gpu(plan, tensors, machine, residency): with the TDN placements
+    lowered into a Residency (cli.cpp:152-160), the whole Stats JSON --
+    per-worker bytes_by_tensor (the ledger, sim.cpp:868-887), work, imbalance,
+    combines -- equals the reference's execute in par mode."""
+    if schedule == "nonzero" and KERNELS[kernel]["nonzero"] is None:
+        pytest.skip("position split rejected for union statements")
+    spec = KERNELS[kernel]
+    sched = ROW if schedule == "row" else spec["nonzero"]
+    rng = np.random.default_rng(1234)
+    out = OUTPUT[kernel]
+    for pieces in (1, 3, 4):
+        t = K.instance(kernel, rng, integers=True)
+        inputs = ref_inputs(kernel, t)
+        out_tdn = None
+        if tdns == "explicit":
+            inputs = {nm: (x[0], x[1], EXPLICIT_TDN[kernel][nm]) for nm, x in inputs.items()}
+            out_tdn = EXPLICIT_TDN[kernel][out]
+        args = (spec["expr"], sched, pieces, spec["formats"][out], inputs)
+        want = ob.RefRun(*args, mode="par", use_placements=True, out_tdn=out_tdn).ok()
+        got = ob.RefRun(*args, mode="gpu", use_placements=True, out_tdn=out_tdn, lib=gpu_lib).ok()
+        ws, gs = _stats_json(want), _stats_json(got)
+        assert gs == ws, (kernel, schedule, tdns, pieces)
+        if pieces > 1 and tdns == "explicit":
+            assert any(b for w in ws["per_worker"] for b in w["bytes_by_tensor"].values())
+
+
+@pytest.mark.parametrize("kernel", ["spmv", "spmm", "spttv"])
+def test_worker_mapping_on_a_2d_machine(gpu_lib, kernel):
+    """A one-loop schedule on a 2-D grid (x=2,y=2, distribute over M.x): the
+    colours map to workers through tuple_worker (sim.cpp:535-544) and the
+    imbalance is over all four workers (sim.cpp:1000-1005)."""
+    spec = KERNELS[kernel]
+    rng = np.random.default_rng(3)
+    t = K.instance(kernel, rng, integers=True)
+    args = (spec["expr"], ROW, "x=2,y=2", spec["formats"][OUTPUT[kernel]], ref_inputs(kernel, t))
+    want = ob.RefRun(*args, mode="par", use_placements=True).ok()
+    got = ob.RefRun(*args, mode="gpu", use_placements=True, lib=gpu_lib).ok()
+    assert _stats_json(got) == _stats_json(want)
+    assert np.array_equal(want.output()[1], got.output()[1])
+
+
+@pytest.mark.parametrize("case", ["csc_B", "colmajor_C", "colmajor_out"])
+def test_transposed_storage_is_rejected(gpu_lib, case):
+    """A CSC B ('ds:1,0') or a column-major dense operand / output is valid
+    for the reference but would be read in the wrong order by the leaf
+    kernels: the adapter rejects it as unsupported (no wrong results)."""
+    from paper_2207_13901_b200.host import SparseTensor, parse_format
+
+    rng = np.random.default_rng(11)
+    n, k, N = 6, 5, 3
+    fmtB = "ds:1,0" if case == "csc_B" else "ds"
+    fmtC = "dd:1,0" if case == "colmajor_C" else "dd"
+    fmtA = "dd:1,0" if case == "colmajor_out" else "dd"
+    B = K.random_sparse(rng, (n, k), fmtB, 0.4)
+    C = K.dense(rng, (k, N), fmtC)
+    sched = "divide(i, io, ii, M.x); distribute(io, M.x)"
+    if case == "csc_B":
+        sched = "reorder(k, i, j); fuse(k, i, f); divide(f, fo, fi, B.pos, M.x); distribute(fo, M.x)"
+    run = ob.RefRun("A(i, j) = B(i, k) * C(k, j)", sched, 2, fmtA, {"B": (B, fmtB), "C": (C, fmtC)},
+                    mode="gpu", lib=gpu_lib)
+    if run.status == 2 and "unsupported on gpu" not in run.error:
+        pytest.skip(f"the reference itself rejects this schedule: {run.error}")
+    assert run.status == 2 and "unsupported on gpu" in run.error, run.error
