@@ -44,9 +44,15 @@ def parse():
     ap.add_argument("--scale", type=int, default=24)
     ap.add_argument("--edge-factor", type=int, default=10)
     ap.add_argument("--cols", type=int, default=32, help="N, columns of C")
-    ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--e2e-steps", type=int, default=None, help="steps of the e2e leg (default: --steps)")
     ap.add_argument("--ref-scale", type=int, default=17, help="R-MAT scale of the CPU reference sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--configs", default="c1,spmv,c3,c4,c5",
+                    help="the other BASELINE configs measured in the same run (empty: headline only)")
+    ap.add_argument("--sddmm-ref-scale", type=int, default=13,
+                    help="R-MAT scale of the CPU reference samples of C3 / C5 (dense per-task accumulators)")
+    ap.add_argument("--no-traffic", action="store_true",
+                    help="skip the ncu DRAM-traffic measurement of the headline leaf (N=1)")
     ap.add_argument("--seed", type=int, default=42)
     ap.add_argument("--trace", action="store_true",
                     help="after the timed run, print per-phase device times of the SpMM step (stderr)")
@@ -376,18 +382,6 @@ def main():
             print(f"[trace rank {r}] " + " ".join(f"{k}={x * 1e3:.1f}us" for k, x in zip(names, v.cpu().numpy())),
                   file=sys.stderr, flush=True)
 
-    # Secondary: SpMV on the same R-MAT (the metric names SpMV and SpMM).
-    x_d = torch.from_numpy(dense_vals(n, args.seed + 2)).to(dev) if rank == 0 else torch.empty(n, dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.broadcast(x_d, 0)
-    y_d = torch.empty(n, dtype=torch.float64, device=dev)
-
-    def step_spmv():
-        H.partition_nonzero(ctx, Bstep, 1, pieces, host=False)
-        H.spmv(ctx, Bstep, x_d, y_d, first=first, count=count, pieces=pieces, stats=False)
-
-    ms_v, leaf_v, _, _ = measure(step_spmv, args.steps, args.warmup, False)
-    spmv_bytes = 8 * (n + 1) + 16 * nnz + 8 * n + 8 * n
     flops = 2.0 * nnz * N
     value = flops / (ms * 1e-3) / 1e9
 
@@ -404,20 +398,69 @@ def main():
     alg_bytes_total = spmm_bytes(n, nnz, n, N)
     per_launch = alg_bytes_total * share if world > 1 else alg_bytes_total
     achieved = per_launch / (leaf_avg * 1e-3) / 1e9 if leaf_avg > 0 else None
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "spmm_leaf_traffic.json")
-    if os.path.exists(tpath):
-        try:
-            tj = json.load(open(tpath))
-            if tj.get("scale") == args.scale and tj.get("gpus") == world:
-                traffic = tj.get("dram_bytes_per_launch")
-        except (OSError, ValueError):
-            traffic = None
-
     # ---- e2e through the C-ABI with host buffers ----
     e2e = None
+    if args.e2e_steps is None:
+        args.e2e_steps = args.steps
     if args.e2e_steps > 0:
         e2e = run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, C_d, N)
+
+    # ---- the other BASELINE configs, same run ----
+    configs = {}
+    cfg = [c for c in args.configs.split(",") if c]
+    if cfg:
+        sys.path.insert(0, os.path.join(ROOT, "scripts"))
+        import bench_cfg as BC
+        from paper_2207_13901_b200 import _native as NN
+        del A_d, C_d
+        torch.cuda.empty_cache()
+        env = BC.Env(ctx, torch, dev, rank, world, args, peak, host_cores(), cpu_model())
+        host_B = (rp, crd, vals) if rank == 0 else None
+
+        def spadd3_inputs(scale=None):
+            """B and its copies with columns shifted +1 / +2."""
+            if rank != 0 and scale is None:
+                return None
+            sc = args.scale if scale is None else scale
+            outs = [host_B if scale is None else rmat_csr(sc, args.edge_factor, args.seed)[1:]]
+            nn = 1 << sc
+            for shift in (1, 2):
+                rps = np.empty(nn + 1, np.int64)
+                e = args.edge_factor * nn
+                cs = np.empty(e, np.int64)
+                vs = np.empty(e)
+                nz = NN.synth().syn_rmat_csr(sc, e, A_RMAT, B_RMAT, C_RMAT, args.seed, 0, 0, shift,
+                                             rps.ctypes.data_as(NN.i64p), cs.ctypes.data_as(NN.i64p),
+                                             vs.ctypes.data_as(NN.dblp))
+                outs.append((rps, cs[:nz], vs[:nz]))
+            return outs
+
+        rm = {"n": n, "scale": args.scale, "rp_d": rp_d, "crd_d": crd_d, "vals_d": vals_d, "Bstep": Bstep,
+              "host": host_B, "dense": lambda count, seed: dense_vals(count, seed),
+              "gen": lambda sc: rmat_csr(sc, args.edge_factor, args.seed), "spadd3_inputs": spadd3_inputs}
+        for name in cfg:
+            t0 = time.time()
+            try:
+                if name == "c1":
+                    configs["C1"] = BC.config_c1(env, H, NN.synth())
+                elif name == "spmv":
+                    configs["SpMV-RMAT"] = BC.config_spmv_rmat(env, H, rm, args.seed + 2)
+                elif name == "c3":
+                    configs["C3"] = BC.config_c3(env, H, rm)
+                elif name == "c4":
+                    configs.update(BC.config_c4(env, H, NN.synth()))
+                elif name == "c5":
+                    configs["C5"] = BC.config_c5(env, H, rm)
+            except Exception as ex:  # a failed leg is reported, the headline line still prints
+                configs[name] = {"error": f"{type(ex).__name__}: {ex}"}
+            torch.cuda.empty_cache()
+            if rank == 0:
+                print(f"[bench] config {name}: {time.time() - t0:.1f} s", file=sys.stderr, flush=True)
+
+    # ---- DRAM traffic of the headline leaf: one ncu pass in a child process ----
+    traffic = None
+    if rank == 0 and world == 1 and not args.no_traffic:
+        traffic = measure_traffic(args)
 
     # ---- CPU baseline (rank 0, N=1) ----
     cpu = None
@@ -445,20 +488,16 @@ def main():
                        "input_gen_s": round(t_gen, 1)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": "k_spmm32_nz<4,4,0,1> (dynamic chunk tickets; k_zero_empty for the empty rows runs concurrently on the aux stream, inside the timed leaf window)", "peak_source": peak_src,
+                         "kernel": "k_spmm32_nz<4,3> (cp.async ring of 4 slots, dynamic chunk tickets; k_zero_empty for the empty rows runs concurrently on the aux stream, inside the timed leaf window)", "peak_source": peak_src,
                          "bytes_per_launch": per_launch, "leaf_ms": leaf_avg,
+                         "traffic_source": ("ncu dram__bytes_read.sum + dram__bytes_write.sum of one leaf launch, "
+                                            "child process of this run (scripts/prof_spmm.py)") if traffic else None,
                          "frac_vs_8tbs_nominal": (achieved / 8000.0) if achieved else None},
             "phases_ms_max_over_ranks": phases,
+            "configs": configs,
             "clocks": clock_summary,
             "gpu_launches": launches,
             "placement": placement,
-            "spmv": {"workload": "SpMV a(i)=B(i,j)*c(j) on the same R-MAT, nonzero split",
-                     "value": 2.0 * nnz / (ms_v * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms_v,
-                     "effective_gbs": spmv_bytes / (ms_v * 1e-3) / 1e9,
-                     "roofline": {"bound": "hbm", "achieved": (spmv_bytes / world) / (leaf_v * 1e-3) / 1e9 if leaf_v else None,
-                                  "peak": peak, "unit": "GB/s",
-                                  "frac": (spmv_bytes / world) / (leaf_v * 1e-3) / 1e9 / peak if leaf_v else None,
-                                  "kernel": "k_spmv_rows", "leaf_ms": leaf_v}},
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
@@ -466,6 +505,38 @@ def main():
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_traffic(args):
+    """DRAM bytes of one headline-leaf launch (dram__bytes_read.sum +
+    dram__bytes_write.sum), measured in this run by ncu on a child process
+    that builds the same matrix and runs the leaf (scripts/prof_spmm.py); the
+    bench's own numbers are never taken under the profiler.  None when ncu is
+    unavailable or fails."""
+    import shutil
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None
+    cmd = [ncu, "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum", "-k", "regex:k_spmm32_nz",
+           "-s", "1", "-c", "1", "--csv", sys.executable, os.path.join(ROOT, "scripts", "prof_spmm.py"),
+           "--steps", "2", "--scale", str(args.scale)]
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    except (OSError, subprocess.TimeoutExpired):
+        return None
+    vals = {}
+    for ln in r.stdout.splitlines():
+        f = [x.strip('"') for x in ln.split('","')]
+        if len(f) >= 3 and f[-3] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            try:
+                unit, v = f[-2], float(f[-1].replace(",", ""))
+            except ValueError:
+                continue
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}.get(unit, 1)
+            vals[f[-3]] = v * scale
+    if len(vals) != 2:
+        return None
+    return int(vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"])
 
 
 def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, C_d, N):

@@ -433,22 +433,10 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmv_rows(WalkGeom g, NzView z
 }
 
 // ---------------------------------------------------------------------------
-// SpMM N == 32 over the compacted view (the C2 leaf).  Half a warp per stored
-// position: lane l gathers columns 2(l%16), 2(l%16)+1 of C(k,:) with one
-// 128-bit load, so a warp instruction covers two positions.  Per 32-position
-// window the warp loads the window's int32 columns and values (one per lane,
-// the next window prefetched) and the row-start mask.  Per group of 2*UNR
-// positions it issues UNR gathers unconditionally (positions past the chunk
-// end read column 0 and are never added) and, when no row starts in a full
-// group, 2*UNR FMAs -- no per-position row logic.  A group holding row starts
-// walks only its starts: the products before each start are added under a
-// predicate, the finished row is flushed (the halves' partials summed with one
-// xor-shuffle) and the next row's id is read from the register cursor.  The
-// cursor keeps row starts relative to the chunk and row ids as 32-bit values
-// (rows < 2^31), so the walk fits 64 registers (32 warps / SM) without spills.
-// The previous leaf issued ~16 warp instructions per position, mostly 64-bit
-// address arithmetic and per-position row tests
-// (profiles/r02_spmm_leaf_base_ncu.txt); this one issues ~5.
+// Register cursor of the N == 32 SpMM leaf: 64 consecutive compacted rows
+// (two 32-lane blocks) with their starts relative to the chunk start and
+// their ids as 32-bit values (rows < 2^31), so the walk fits the register
+// budget that leaves room for 24 warps per SM.
 struct NzCur32 {
   int64_t cb;  // block base (compacted row index)
   int off;     // current compacted row - cb, in [0, 32) between windows
@@ -468,15 +456,49 @@ __device__ __forceinline__ int shfl_pair(int v0, int v1, int idx) {
   return idx < 32 ? a : b;
 }
 
-template <int UNR, int MINB>
+// ---------------------------------------------------------------------------
+// SpMM N == 32 over the compacted view (the C2 leaf).  Half a warp per stored
+// position: lane l copies columns 2(l%16), 2(l%16)+1 of C(k,:), so a warp
+// instruction covers two positions.  Per 32-position window the warp holds
+// the window's int32 columns and values (one per lane; columns two windows
+// ahead, values one) and the row-start mask.  The 256-byte C rows land in a
+// per-warp shared-memory ring through cp.async (16 B per lane, L2 evict_last):
+// the warp keeps S-1 groups of 8 positions in flight while it consumes the
+// oldest, so the bytes in flight per SM do not cost registers.  Each lane
+// reads back exactly the 16 bytes it copied: no warp barrier.  A full group
+// without a row start is 8 FMAs per lane; a group holding row starts walks
+// only its starts (products before each start added under a predicate, the
+// finished row flushed with one xor-shuffle, the next row's id read from the
+// register cursor).  Positions past the chunk end copy row 0 and are never
+// added.  Measured history (profiles/r02_*): the round-1 leaf issued ~16
+// instructions per position (64-bit address arithmetic, per-position row
+// tests) and stalled on register-held gathers; the register-lean rewrite cut
+// that to ~11 but stayed gather-latency bound (16 warps stalled per issue);
+// the ring holds 3 groups ahead per warp and moves DRAM to ~65% of its peak.
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint64_t pol) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int S, int MINB>
 __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z, const int32_t* __restrict__ crd32,
-                                                      const double* __restrict__ vals,
-                                                      const double* __restrict__ C, double* __restrict__ A,
-                                                      ChunkRecs rec, const int64_t* __restrict__ counters) {
-  static_assert(2 * UNR < 32 && 32 % (2 * UNR) == 0, "groups tile the 32-position window");
-  constexpr unsigned kGroupMask = (1u << (2 * UNR)) - 1u;
+                                                        const double* __restrict__ vals,
+                                                        const double* __restrict__ C, double* __restrict__ A,
+                                                        ChunkRecs rec, const int64_t* __restrict__ counters) {
+  static_assert(S >= 2 && S <= 5, "lookahead stays within the next window");
+  constexpr int UNR = 4;  // gathers per lane per group of 8 positions
+  extern __shared__ double2 smem_ring[];
   const int lane = lane_id();
   const int half = lane >> 4, hl = lane & 15;
+  // this warp's ring: S slots x 8 positions x 16 lanes of 16 bytes; lane
+  // (half, hl) owns element [slot][2i + half][hl]
+  double2* ring = smem_ring + (threadIdx.x >> 5) * (S * 8 * 16) + half * 16 + hl;
   z.m = nz_count(z);
   const int64_t begin = counters[1], end = counters[2];
   const double* Cl = C + 2 * hl;
@@ -489,53 +511,67 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
     }
     const int64_t s = ci.s;
     const int ne = (int)(ci.e - s);  // last offset of the chunk
+    const int ngroups = (ne + 8) / 8;
     const int32_t* cp = crd32 + s;
     const double* vp = vals + s;
     NzCur32 c;
-    c.cb = warp_owner(z.ptr, z.m, s);  // compacted row holding position s
+    c.cb = warp_owner(z.ptr, z.m, s);
     c.off = 0;
     nz32_load(z, c.cb, s, c.P0, c.I0);
     nz32_load(z, c.cb + 32, s, c.P1, c.I1);
-    bool head = __shfl_sync(FULL, c.P0, 0) < 0;  // the chunk's first row began before it
-    int cur = __shfl_sync(FULL, c.I0, 0);        // id of the current row
+    bool head = __shfl_sync(FULL, c.P0, 0) < 0;
+    int cur = __shfl_sync(FULL, c.I0, 0);
     int head_row = -1;
     double2 acc = make_double2(0.0, 0.0);
-    int kn = 0;
-    double vn = 0.0;
-    if (lane <= ne) {
-      kn = ld_i32_hint(cp + lane, pol_stream);
-      vn = ld_f64_hint(vp + lane, pol_stream);
-    }
+    // column indices of windows w, w+1, w+2 and values of windows w, w+1
+    int k0 = lane <= ne ? ld_i32_hint(cp + lane, pol_stream) : 0;
+    int k1 = 32 + lane <= ne ? ld_i32_hint(cp + 32 + lane, pol_stream) : 0;
+    int k2 = 64 + lane <= ne ? ld_i32_hint(cp + 64 + lane, pol_stream) : 0;
+    double v0 = lane <= ne ? ld_f64_hint(vp + lane, pol_stream) : 0.0;
+    double v1 = 32 + lane <= ne ? ld_f64_hint(vp + 32 + lane, pol_stream) : 0.0;
+    // issue group gi (positions 8 gi .. 8 gi + 7) from the window registers
+    // (kw: the column indices of gi's window)
+    auto issue = [&](int gi, int kw) {
+      if (gi < ngroups) {
+        double2* slot = ring + (gi % S) * (8 * 16);
+#pragma unroll
+        for (int i = 0; i < UNR; i++) {
+          const int kk = __shfl_sync(FULL, kw, ((gi & 3) << 3) + 2 * i + half);
+          cp_async16(slot + i * 32, Cl + (int64_t)kk * 32, pol_keep);
+        }
+      }
+      cp_async_commit();
+    };
+#pragma unroll
+    for (int gi = 0; gi < S - 1; gi++) issue(gi, k0);
     for (int b0 = 0; b0 <= ne; b0 += 32) {
       const int cnt = min(32, ne - b0 + 1);
-      const int my_k = kn;
-      const double my_v = vn;
-      kn = 0;
-      vn = 0.0;
-      if (b0 + 32 + lane <= ne) {
-        kn = ld_i32_hint(cp + b0 + 32 + lane, pol_stream);
-        vn = ld_f64_hint(vp + b0 + 32 + lane, pol_stream);
-      }
-      // row starts after the current row inside [b0, b0 + cnt)
       const int last = b0 + cnt - 1;
       unsigned bm = __reduce_or_sync(
           FULL, (lane > c.off && c.P0 >= b0 && c.P0 <= last) ? 1u << (c.P0 - b0) : 0u);
       if (__shfl_sync(FULL, c.P0, 31) <= last)
         bm |= __reduce_or_sync(FULL, (c.P1 >= b0 && c.P1 <= last) ? 1u << (c.P1 - b0) : 0u);
-      int j = c.off + 1;  // cursor slot of the next row to start
+      int j = c.off + 1;
+      const int gw = b0 >> 3;  // first group of this window
 #pragma unroll 1
-      for (int u = 0; u < cnt; u += 2 * UNR) {
+      for (int u = 0; u < cnt; u += 8) {
+        const int gi = gw + (u >> 3);
+        // keep S-1 groups in flight: issue gi + S - 1 (its window is this one or the next)
+        {
+          const int ga = gi + S - 1;
+          issue(ga, (ga >> 2) == (gi >> 2) ? k0 : k1);
+        }
+        cp_async_wait<S - 1>();
+        const double2* slot = ring + (gi % S) * (8 * 16);
         double2 cv[UNR];
         double bv[UNR];
 #pragma unroll
         for (int i = 0; i < UNR; i++) {
-          const int p = u + 2 * i + half;
-          const int kk = __shfl_sync(FULL, my_k, p);
-          bv[i] = __shfl_sync(FULL, my_v, p);
-          cv[i] = ld_f64x2_hint(Cl + (int64_t)kk * 32, pol_keep);
+          cv[i] = slot[i * 32];
+          bv[i] = __shfl_sync(FULL, v0, u + 2 * i + half);
         }
-        unsigned gm = (bm >> u) & kGroupMask;
-        if (gm == 0u && u + 2 * UNR <= cnt) {
+        unsigned gm = (bm >> u) & 0xffu;
+        if (gm == 0u && u + 8 <= cnt) {
 #pragma unroll
           for (int i = 0; i < UNR; i++) {
             acc.x = fma(bv[i], cv[i].x, acc.x);
@@ -543,8 +579,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
           }
           continue;
         }
-        // segments [lo, hi) of the group between row starts (and the chunk end)
-        const int lim = min(2 * UNR, cnt - u);
+        const int lim = min(8, cnt - u);
         int lo = 0;
         for (;;) {
           const int hi = gm ? __ffs(gm) - 1 : lim;
@@ -557,7 +592,6 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
             }
           }
           if (!gm) break;
-          // row `cur` ends before offset hi: flush it
           double2 o;
           o.x = acc.x + __shfl_xor_sync(FULL, acc.x, 16);
           o.y = acc.y + __shfl_xor_sync(FULL, acc.y, 16);
@@ -576,15 +610,21 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
         }
       }
       c.off = j - 1;
-      if (c.off >= 32) {  // slide the register window; the new block is far ahead
+      if (c.off >= 32) {
         c.cb += 32;
         c.off -= 32;
         c.P0 = c.P1;
         c.I0 = c.I1;
         nz32_load(z, c.cb + 32, s, c.P1, c.I1);
       }
+      // advance the window registers: w+1 becomes current, w+3 is prefetched
+      k0 = k1;
+      k1 = k2;
+      k2 = b0 + 96 + lane <= ne ? ld_i32_hint(cp + b0 + 96 + lane, pol_stream) : 0;
+      v0 = v1;
+      v1 = b0 + 64 + lane <= ne ? ld_f64_hint(vp + b0 + 64 + lane, pol_stream) : 0.0;
     }
-    // chunk end: the current row ends exactly at the chunk end, or continues past it
+    cp_async_wait<0>();  // drain the look-ahead past the chunk (empty groups)
     double2 o;
     o.x = acc.x + __shfl_xor_sync(FULL, acc.x, 16);
     o.y = acc.y + __shfl_xor_sync(FULL, acc.y, 16);

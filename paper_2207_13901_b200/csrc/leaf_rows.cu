@@ -1174,11 +1174,18 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
         SPD_SPMMV(128, 2, 4)
 #undef SPD_SPMMV
       }
-    } else if (a.op == Op::SpMM) {  // N == 32 (C2): the lean compacted-row leaf
+    } else if (a.op == Op::SpMM) {  // N == 32 (C2): cp.async ring of 4 slots, 3 CTAs / SM
       const int32_t* c32 = crd32_index(ctx, const_cast<spd_tensor*>(B));
+      constexpr int kS = 4, kMinB = 3;
+      const int smem = (kBlock / 32) * kS * 8 * 16 * (int)sizeof(double2);
       static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmm32_nz<4, 4>);
-      k_spmm32_nz<4, 4><<<grid, kBlock, 0, s>>>(g, z, c32, B->vals, a.x, a.out, rec, col.counters);
+      if (!grid) {
+        SPD_CUDA(cudaFuncSetAttribute(k_spmm32_nz<kS, kMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        int per_sm = 0;
+        SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmm32_nz<kS, kMinB>, kBlock, smem));
+        grid = ctx->num_sms * (per_sm > 0 ? per_sm : 1);
+      }
+      k_spmm32_nz<kS, kMinB><<<grid, kBlock, smem, s>>>(g, z, c32, B->vals, a.x, a.out, rec, col.counters);
     } else if (spmv_rows_mode(nnz, z.m)) {  // short rows: a lane per row
       // 6 CTAs/SM (40 registers, a few spills) wins on large matrices
       // (R-MAT leaf 1.11 -> 1.045 ms), 4 on small ones (C1 / C4)

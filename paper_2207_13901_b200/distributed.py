@@ -69,3 +69,48 @@ def assemble(parts, W, width: int, nrows: int):
         if lo <= hi:
             out[lo:hi + 1] = np.asarray(parts[r]).reshape(nrows, width)[lo:hi + 1]
     return out
+
+
+def assemble_positions(parts, spans, npos: int):
+    """Output vals on an input's pattern (SDDMM, SpTTV's fibre level) from
+    every rank's full-size buffer, keeping rank c's position span spans[c]
+    (the colour's q range for SDDMM, its owned fibres for SpTTV)."""
+    out = np.zeros(npos)
+    for r, (lo, hi) in enumerate(spans):
+        if lo <= hi:
+            out[lo:hi + 1] = np.asarray(parts[r]).reshape(-1)[lo:hi + 1]
+    return out
+
+
+def leaf_rowptr(rp1, rp2):
+    """Rows i of a dss CSF -> leaf positions (rp2[rp1[i]]), the derived row
+    pointer the SpMTTKRP leaf walks (k_leaf_rowptr, leaf_rows.cu)."""
+    return np.asarray(rp2)[np.asarray(rp1)]
+
+
+def csr_offsets(counts):
+    """Global position offset of every rank's row-block piece of an assembled
+    CSR output (SpAdd3): the exclusive prefix sum of the all-gathered piece
+    sizes (spd_spadd3 with a communicator, spd_tensor_global_span)."""
+    c = np.asarray(counts, dtype=np.int64)
+    return np.concatenate([[0], np.cumsum(c)[:-1]]), int(c.sum())
+
+
+def assemble_csr(pieces, nrows: int):
+    """One CSR from row-block pieces [(row_lo, row_hi, rowptr_local, crd,
+    vals)] in rank order; rowptr_local has row_hi - row_lo + 2 entries from 0."""
+    rp = np.zeros(nrows + 1, np.int64)
+    crds, vals = [], []
+    base = 0
+    for lo, hi, lrp, c, v in pieces:
+        if lo <= hi:
+            rp[lo + 1:hi + 2] = base + np.asarray(lrp)[1:]
+        crds.append(np.asarray(c))
+        vals.append(np.asarray(v))
+        base += len(c)
+    # rows outside every piece keep the running offset
+    for i in range(1, nrows + 1):
+        if rp[i] < rp[i - 1]:
+            rp[i] = rp[i - 1]
+    return rp, (np.concatenate(crds) if crds else np.zeros(0, np.int64)), \
+        (np.concatenate(vals) if vals else np.zeros(0))
