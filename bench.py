@@ -382,6 +382,48 @@ def main():
             print(f"[trace rank {r}] " + " ".join(f"{k}={x * 1e3:.1f}us" for k, x in zip(names, v.cpu().numpy())),
                   file=sys.stderr, flush=True)
 
+    # ---- N > 1: the distributed result against all colours on one GPU ----
+    # Every rank's owned output rows W_c (after the NCCL boundary combine)
+    # are sent to rank 0 and compared bit-exactly with rank 0 running all N
+    # colours of the same partition on its own GPU (same combine order, so the
+    # same bits).  Outside the timed region.
+    mgpu_check = None
+    if world > 1:
+        from paper_2207_13901_b200.distributed import owned_rows
+        cols = H.partition_nonzero(ctx, Bstep, 1, pieces)  # host copy of the colours (syncs)
+        rp_host = rp_d.cpu().numpy()
+        W = owned_rows(cols, rp_host, "nonzero", n)
+        H.partition_nonzero(ctx, Bstep, 1, pieces, host=False)
+        H.spmm(ctx, Bstep, C_d, N, A_d, first=first, count=count, pieces=pieces, stats=False)
+        torch.cuda.synchronize()
+        ok = True
+        if rank == 0:
+            A_ref = torch.empty_like(A_d)
+            ctx1 = H.Context(local)  # no communicator: every colour on this GPU
+            B1 = H.DeviceTensor.wrap(ctx1, (n, n), fmt, [rp_d.data_ptr()], [crd_d.data_ptr()], vals_d.data_ptr())
+            H.partition_nonzero(ctx1, B1, 1, pieces, host=False)
+            H.spmm(ctx1, B1, C_d, N, A_ref, pieces=pieces, stats=False)
+            torch.cuda.synchronize()
+        for r, (lo, hi) in enumerate(W):
+            if lo > hi:
+                continue
+            if r == 0 and rank == 0:
+                ok = ok and bool(torch.equal(A_d[lo * N:(hi + 1) * N], A_ref[lo * N:(hi + 1) * N]))
+            elif rank == r:
+                dist.send(A_d[lo * N:(hi + 1) * N].contiguous(), 0)
+            elif rank == 0:
+                buf = torch.empty((hi - lo + 1) * N, dtype=torch.float64, device=dev)
+                dist.recv(buf, r)
+                ok = ok and bool(torch.equal(buf, A_ref[lo * N:(hi + 1) * N]))
+        if rank == 0:
+            B1.close()
+            ctx1.close()
+            del A_ref
+        mgpu_check = {"bit_exact_vs_one_gpu": ok,
+                      "what": "every rank's owned rows W_c after the NCCL boundary combine vs all colours of the "
+                              "same partition on rank 0's GPU (the restatement comparison at one GPU is "
+                              "tests/test_gpu_fullsize.py)"}
+
     flops = 2.0 * nnz * N
     value = flops / (ms * 1e-3) / 1e9
 
@@ -498,6 +540,7 @@ def main():
             "clocks": clock_summary,
             "gpu_launches": launches,
             "placement": placement,
+            "multi_gpu_check": mgpu_check,
             "e2e": e2e,
             "cpu_baseline": cpu,
         }

@@ -1195,6 +1195,8 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
       }();
       const int minb = minb_env ? minb_env : (nnz >= (int64_t(1) << 26) || a.op == Op::SpTTV ? 6 : 4);
       const int64_t ncols = B->dims[B->mode_order[B->groups.back()[0]]];
+      const int32_t* c32 = nullptr;  // compacted columns (SpMV over a wide x)
+      const double* xv = a.x;
       if (a.op == Op::SpMV && xc_wanted(ctx, B, ncols)) {  // compacted x, int32 crd
         spd_tensor* Bm = const_cast<spd_tensor*>(B);
         xc_index(ctx, Bm, ncols);
@@ -1205,29 +1207,23 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
           SPD_CHECK_LAUNCH();
           launches++;
         }
-#define SPD_ROWS_XC(MB)                                                                                   \
-  do {                                                                                                    \
-    static int gr = 0;                                                                                    \
-    if (!gr) gr = occupancy_grid(ctx, k_spmv_rows<MB, int32_t>);                                         \
-    k_spmv_rows<MB, int32_t><<<gr, kBlock, 0, s>>>(g, z, Bm->crdc, B->vals, xc, a.out, rec, col.counters); \
-  } while (0)
-        if (minb == 6) SPD_ROWS_XC(6);
-        else if (minb == 8) SPD_ROWS_XC(8);
-        else SPD_ROWS_XC(4);
-#undef SPD_ROWS_XC
-      } else if (minb == 6) {
-        static int grid6 = 0;
-        if (!grid6) grid6 = occupancy_grid(ctx, k_spmv_rows<6>);
-        k_spmv_rows<6><<<grid6, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
-      } else if (minb == 8) {
-        static int grid8 = 0;
-        if (!grid8) grid8 = occupancy_grid(ctx, k_spmv_rows<8>);
-        k_spmv_rows<8><<<grid8, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
-      } else {
-        static int grid = 0;
-        if (!grid) grid = occupancy_grid(ctx, k_spmv_rows<4>);
-        k_spmv_rows<4><<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
+        c32 = Bm->crdc;
+        xv = xc;
       }
+#define SPD_LEAF(KERN, CI, CRD)                                                                         \
+  do {                                                                                                  \
+    static int gr = 0;                                                                                  \
+    if (!gr) gr = occupancy_grid(ctx, KERN);                                                            \
+    KERN<<<gr, kBlock, 0, s>>>(g, z, (const CI*)(CRD), B->vals, xv, a.out, rec, col.counters);          \
+  } while (0)
+      if (c32) {
+        if (minb == 6) SPD_LEAF((k_spmv_rows<6, int32_t>), int32_t, c32);
+        else SPD_LEAF((k_spmv_rows<4, int32_t>), int32_t, c32);
+      } else {
+        if (minb == 6) SPD_LEAF((k_spmv_rows<6, int64_t>), int64_t, leaf.crd);
+        else SPD_LEAF((k_spmv_rows<4, int64_t>), int64_t, leaf.crd);
+      }
+#undef SPD_LEAF
     } else {
       static int grid = 0;
       if (!grid) grid = occupancy_grid(ctx, k_spmv_nz);

@@ -39,6 +39,14 @@ def _ob():
     return ob
 
 
+def _sk():
+    """The six kernels' expressions and schedules as the reference states
+    them (tests/spd_kernels.py), for the CPU baseline's reference runs."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import spd_kernels
+    return spd_kernels
+
+
 class Env:
     def __init__(self, ctx, torch, dev, rank, world, args, peak, host_cores, cpu_model):
         self.ctx, self.torch, self.dev = ctx, torch, dev
@@ -113,7 +121,7 @@ def cpu_reference(env, kernel, schedule, out_fmt, tensors, flops, pieces, what):
     """The reference's plan() + execute() (par mode; its pool is min(cores,
     tasks) threads, sim.cpp:958-961) on host buffers: the CPU baseline."""
     ob = _ob()
-    import spd_kernels as SK
+    SK = _sk()
     spec = SK.KERNELS[kernel]
     run = ob.RefRun(spec["expr"], schedule, pieces, out_fmt, tensors, mode="par").ok()
     t = run.exec_seconds() + run.plan_seconds()
@@ -241,7 +249,7 @@ def config_c1(env, H, synth):
         if not env.args.no_cpu_baseline:
             Bh = _csr_host(H, n, n, rp, crd, vals)
             xh = H.SparseTensor.from_parts((n,), H.parse_format("d"), [H.Level("d", dom=(n,))], x)
-            import spd_kernels as SK
+            SK = _sk()
             cb, run = cpu_reference(env, "spmv", SK.ROW, "d", {"B": (Bh, "ds"), "c": (xh, "d")}, flops,
                                     env.host_cores, "C1 at full size (1M x 1M, 10M samples)")
             cb["matches_gpu"] = bool(np.allclose(run.output()[1], y_h.numpy(), rtol=1e-10, atol=0))
@@ -292,7 +300,7 @@ def config_spmv_rmat(env, H, rm, x_seed):
             x2 = rm["dense"](n2, x_seed)
             Bh = _csr_host(H, n2, n2, rp2, crd2, vals2)
             xh = H.SparseTensor.from_parts((n2,), H.parse_format("d"), [H.Level("d", dom=(n2,))], x2)
-            import spd_kernels as SK
+            SK = _sk()
             out["cpu_baseline"], _ = cpu_reference(
                 env, "spmv", SK.KERNELS["spmv"]["nonzero"], "d", {"B": (Bh, "ds"), "c": (xh, "d")},
                 2.0 * len(crd2), max(1, min(env.host_cores, 64)),
@@ -360,7 +368,7 @@ def config_c3(env, H, rm):
                                            rm["dense"](n2 * K, 44))
             Dh = H.SparseTensor.from_parts((K, n2), H.parse_format("dd:1,0"), [H.Level("d", dom=(n2, K))],
                                            rm["dense"](n2 * K, 45))
-            import spd_kernels as SK
+            SK = _sk()
             out["cpu_baseline"], _ = cpu_reference(
                 env, "sddmm", SK.KERNELS["sddmm"]["nonzero"], "ds",
                 {"B": (Bh, "ds"), "C": (Ch, "dd"), "D": (Dh, "dd:1,0")}, 2.0 * len(crd2) * K,
@@ -452,7 +460,7 @@ def config_c4(env, H, synth):
         res["C4-SpMTTKRP"]["e2e"] = e2e_loop(env, one_mttkrp, 3.0 * nnz * R, nbytes + (J + Kd) * R * 8, I * R * 8)
         st["t"].close()
         if not env.args.no_cpu_baseline:
-            import spd_kernels as SK
+            SK = _sk()
             t = H.SparseTensor.from_rowptrs((I, J, Kd), fmt, [rp1, rp2], [crd1, crd2], vals)
             ch = H.SparseTensor.from_parts((Kd,), H.parse_format("d"), [H.Level("d", dom=(Kd,))], c)
             Ch = H.SparseTensor.from_parts((J, R), H.parse_format("dd"), [H.Level("d", dom=(J, R))], Cm)
@@ -540,7 +548,7 @@ def config_c5(env, H, rm):
             sc = env.args.sddmm_ref_scale
             ins = rm["spadd3_inputs"](sc)
             n2 = len(ins[0][0]) - 1
-            import spd_kernels as SK
+            SK = _sk()
             tens = {nm: (_csr_host(H, n2, n2, *o), "ds") for nm, o in zip("BCD", ins)}
             out["cpu_baseline"], _ = cpu_reference(
                 env, "spadd3", SK.ROW, "ds", tens, float(sum(len(o[1]) for o in ins)), 8,
