@@ -93,6 +93,8 @@ const char* spd_last_error(void);
 int spd_abi_version(void);
 
 /* ---- (1) context: one per GPU (one process per GPU) -------------------- */
+/* Number of CUDA devices visible to this process (0 without a GPU). */
+int spd_device_count(int* count);
 /* device: CUDA ordinal.  stream: a cudaStream_t to enqueue on (cudaStreamLegacy
  * (0x1) selects the legacy default stream), or NULL for a context-owned
  * non-blocking stream. */
@@ -101,7 +103,12 @@ int spd_context_destroy(spd_context* ctx);
 int spd_context_synchronize(spd_context* ctx);
 /* Multi-GPU: rank/world of this context inside one NCCL communicator over
  * NVLink.  `unique_id` is the 128-byte ncclUniqueId created by rank 0
- * (spd_nccl_unique_id) and broadcast by the host's launcher. */
+ * (spd_nccl_unique_id) and broadcast by the host's launcher.  Collective
+ * calls check their arguments before the first collective they enqueue, and
+ * spd_tensor_place broadcasts the root's input status first, so argument
+ * errors fail on every rank together; a runtime failure on one rank after
+ * the others entered a collective leaves them waiting -- destroy the context
+ * on every rank (ncclCommDestroy) to recover. */
 int spd_nccl_unique_id(void* out128);
 int spd_context_init_comm(spd_context* ctx, const void* unique_id128, int rank, int world);
 int spd_context_rank(const spd_context* ctx, int* rank, int* world);
@@ -279,6 +286,23 @@ int spd_deppart_by_bounds(spd_context* ctx, int rank, const int64_t* extents, in
  * up to `cap` indices and returns the count in *count. */
 int spd_partition_materialize(spd_context* ctx, const spd_tensor* t, int level, int which,
                               int64_t color, int64_t* out, int64_t cap, int64_t* count);
+/* Universe split of an inner compressed level (LevelPartitioner::finalize,
+ * compressed universe entry, level_partition.cpp:193-205; bucketCoords in the
+ * rendered plan): colour c holds the positions of `level` whose coordinate
+ * lies in divide_bounds(the level mode's extent, pieces)[c] -- coordinate
+ * buckets, not contiguous position spans; the second distributed mode of a
+ * 2-D grid (rows over M.x, the columns j of SDDMM or SpTTV over M.y).
+ * Bucketed on the GPU (a stable radix sort of the positions by colour, so a
+ * colour's positions stay ascending).  counts_out[c] = |colour c| (pieces
+ * entries, may be NULL).  The split stays on the context for: */
+int spd_partition_bucket(spd_context* ctx, const spd_tensor* t, int level, int64_t pieces, int64_t* counts_out);
+/* the positions of one colour (host copy, ascending; count = its size) -- the
+ * crd partition of the reference's bundle; */
+int spd_bucket_positions(spd_context* ctx, int64_t color, int64_t* out, int64_t cap, int64_t* count);
+/* and, for `nspans` spans [lo, hi] of the bucketed level's positions (the row
+ * blocks of the grid's first loop), the leaf positions of every (span,
+ * colour) cell: out[x * pieces + y] -- the 2-D grid's per-worker work. */
+int spd_bucket_grid_work(spd_context* ctx, const int64_t* spans, int64_t nspans, int64_t* out);
 
 /* ---- (4) leaf kernels + combine (one execute of a plan) ---------------- */
 /* Every op runs the colours [first_color, first_color + ncolors) of the last
@@ -341,6 +365,12 @@ int spd_gather_rows(spd_context* ctx, const spd_tensor* A, int root, spd_tensor*
 /* Per-colour Stats::PerWorker::work of the last op (sim.cpp:352), `pieces`
  * entries. */
 int spd_last_work(spd_context* ctx, int64_t* work, int64_t pieces);
+
+/* Output rows (fibres for SpTTV) that colours [first, first + count) stored in
+ * the last SpMV / SpMM / SpTTV / SpMTTKRP: the union of their write ranges W_c
+ * (DESIGN.md section 5), lo > hi when none -- what a caller copies back from
+ * this GPU's output buffer when the colours ran on several GPUs. */
+int spd_last_owned(spd_context* ctx, int64_t first, int64_t count, int64_t* lo, int64_t* hi);
 
 /* CUDA graphs: capture the ops enqueued on `ctx` between begin and end
  * (e.g. spd_partition_* with colors_out NULL + a leaf op with stats NULL)

@@ -23,7 +23,10 @@
 //   work through tuple_worker, imbalance over every worker of the machine,
 //   and bytes_by_tensor from the Residency (the reference's ledger).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <exception>
+#include <thread>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -51,7 +54,7 @@ void check(int st) {
 
 struct Ctx {
   spd_context* h = nullptr;
-  Ctx() { check(spd_context_create(0, nullptr, &h)); }
+  explicit Ctx(int device = 0) { check(spd_context_create(device, nullptr, &h)); }
   ~Ctx() { spd_context_destroy(h); }
 };
 
@@ -332,104 +335,271 @@ ExecResult execute_batched(const Plan& plan, const TensorSet& tensors, const Mac
   return r;
 }
 
-ExecResult execute_gpu(const Plan& plan, const TensorSet& tensors, const MachineGrid& machine,
-                       const Residency& residency) {
-  if (plan.loops.size() == 2) {
-    const std::string k = kernel_of(plan);
-    if (k == "spmm" || k == "spmttkrp") return execute_batched(plan, tensors, machine, residency, k);
+// 2-D grids of SDDMM / SpTTV (PAPER.md:1328-1330 shape, test_planner.cpp:
+// 193-225): rows i over loop 0 (a universe split of the dense top level),
+// the columns j -- the compressed level 1's coordinate -- over loop 1, the
+// bucket split (level_partition.cpp:193-205; spd_partition_bucket).  The
+// outputs live on B's pattern (SDDMM) or on its fibres (SpTTV), so every
+// (x, y) cell writes only its own entries: one op over the row colours
+// computes all cells, and each cell's work is counted on the GPU from the
+// bucket split (spd_bucket_grid_work).
+ExecResult execute_grid(const Plan& plan, const TensorSet& tensors, const MachineGrid& machine,
+                        const Residency& residency, const std::string& kernel) {
+  const PlanLoop& lx = plan.loops[0];
+  const PlanLoop& ly = plan.loops[1];
+  const auto& t = plan.stmt.terms[0];
+  const std::string out_name = plan.stmt.lhs.tensor;
+  const SparseTensor& Bt = tensors.at(t[0].tensor);
+  if (lx.position_space || ly.position_space || plan.combine)
+    throw ValidationError("unsupported on gpu: a 2-D " + kernel + " grid needs two universe loops and no combine");
+  const int64_t Px = lx.pieces, Py = ly.pieces;
+  Ctx ctx;
+  DevTensor B;
+  upload(ctx, Bt, B);
+  std::vector<spd_color> cols(Px);
+  check(spd_partition_universe(ctx.h, B.h, Px, cols.data()));
+  for (int64_t c = 0; c < Px; c++) {
+    const CoordRange& want = lx.color_bounds[c];
+    const bool same = cols[c].color.lo == want.lo && cols[c].color.hi == want.hi;
+    if (!same && !(cols[c].color.lo > cols[c].color.hi && want.empty()))
+      throw std::logic_error("gpu partition differs from plan() colour bounds");
   }
-  if (plan.loops.size() != 1)
-    throw ValidationError("unsupported on gpu: one distributed loop, or the batched two-loop SpMM / SpMTTKRP");
+  // the columns' bucket split, checked against the planner's coordinate bounds
+  std::vector<int64_t> counts(Py);
+  check(spd_partition_bucket(ctx.h, B.h, 1, Py, counts.data()));
+  const int64_t extent = Bt.dims()[Bt.format().mode_order[1]];
+  for (int64_t c = 0; c < Py; c++) {
+    const int64_t block = extent / Py;
+    const int64_t lo = c * block, hi = c + 1 == Py ? extent - 1 : lo + block - 1;
+    const CoordRange& want = ly.color_bounds[c];
+    if (!((lo == want.lo && hi == want.hi) || (lo > hi && want.empty())))
+      throw std::logic_error("gpu bucket split differs from plan() colour bounds");
+  }
+  std::map<std::string, DevTensor> dev;
+  for (const auto& a : t)
+    if (a.tensor != t[0].tensor && !dev.count(a.tensor)) upload(ctx, tensors.at(a.tensor), dev[a.tensor]);
+  const SparseTensor& outstub = tensors.at(out_name);
+  DevTensor outbuf;
+  upload(ctx, outstub, outbuf);
+  double* outp = const_cast<double*>(dense_vals_dev(outbuf.h));
+  spd_stats st{};
+  int64_t mult = 1;
+  std::vector<int64_t> spans(2 * Px);
+  for (int64_t x = 0; x < Px; x++) {  // each row colour's span of level-1 positions
+    const spd_range r = kernel == "sddmm" ? cols[x].q : cols[x].par;
+    spans[2 * x] = r.lo, spans[2 * x + 1] = r.hi;
+  }
+  if (kernel == "sddmm") {
+    const SparseTensor& Ct = tensors.at(t[1].tensor);
+    const SparseTensor& Dt = tensors.at(t[2].tensor);
+    const int64_t K = Ct.dims()[1];
+    const bool jmajor = Dt.format().mode_order[0] == 1;
+    check(spd_sddmm(ctx.h, B.h, dense_vals_dev(dev[t[1].tensor].h), dense_vals_dev(dev[t[2].tensor].h), K,
+                    jmajor ? 1 : Dt.dims()[1], jmajor ? K : 1, outp, 0, Px, &st));
+    mult = K;
+  } else {
+    check(spd_spttv(ctx.h, B.h, dense_vals_dev(dev[t[1].tensor].h), outp, 0, Px, &st));
+  }
+  std::vector<int64_t> cell(Px * Py);
+  check(spd_bucket_grid_work(ctx.h, spans.data(), Px, cell.data()));
+  std::vector<double> vals(outstub.leaf_count());
+  check(spd_tensor_download_vals(outbuf.h, vals.data()));
+  std::vector<LevelStorage> levels;
+  for (int l = 0; l < outstub.num_levels(); l++) levels.push_back(outstub.level(l));
+  ExecResult r{SparseTensor::from_parts(plan.dims.at(out_name), plan.formats.at(out_name), std::move(levels),
+                                        std::move(vals)),
+               Stats{}};
+  const std::vector<Task> tasks = tasks_of(plan, machine);
+  std::vector<int64_t> task_work;
+  for (const auto& tk : tasks) task_work.push_back(cell[tk.colors[0] * Py + tk.colors[1]] * mult);
+  r.stats = make_stats(ctx.h, plan, tensors, machine, residency, tasks, task_work);
+  r.stats.combines = 0;
+  return r;
+}
+
+// The GPUs a one-loop plan's colours are spread over: every visible device,
+// at most one per colour, capped by DSPAR_GPUS when set.  Each GPU runs one
+// contiguous block of ceil(P / G) colours, the way execute() hands colour
+// tasks to its thread pool (sim.cpp:833-847, 958-980).
+static int gpus_for(int64_t pieces) {
+  int n = 1;
+  check(spd_device_count(&n));
+  if (const char* e = std::getenv("DSPAR_GPUS")) n = std::min(n, std::max(1, std::atoi(e)));
+  int64_t g = std::min<int64_t>(n, std::max<int64_t>(pieces, 1));
+  const int64_t cmax = (pieces + g - 1) / std::max<int64_t>(g, 1);
+  return static_cast<int>(std::max<int64_t>(1, (pieces + cmax - 1) / cmax));  // every GPU gets >= 1 colour
+}
+
+// One GPU's share of execute_gpu: uploads, the partition step (checked
+// against the planner's colour bounds), its block of colours -- the
+// cross-GPU boundary combine and SpAdd3's offsets run over NCCL inside the
+// backend -- and the copy of the output ranges it owns into `out`.
+struct GpuPart {
+  int device = 0, rank = 0, world = 1;
+  const void* uid = nullptr;
+  int64_t first = 0, count = 0;
+  std::vector<int64_t> work;
+  int64_t combines = 0;
+  SparseTensor spadd3_out;  // rank 0, SpAdd3 only
+};
+
+static void run_part(const Plan& plan, const TensorSet& tensors, const std::string& kernel, GpuPart& g,
+                     std::vector<double>& out) {
   const PlanLoop& loop = plan.loops[0];
-  const std::string kernel = kernel_of(plan);
   const auto& terms = plan.stmt.terms;
   const std::string out_name = plan.stmt.lhs.tensor;
   const std::string b_name = terms[0][0].tensor;
   const SparseTensor& Bt = tensors.at(b_name);
-
-  Ctx ctx;
+  const int64_t P = loop.pieces;
+  Ctx ctx(g.device);
+  if (g.world > 1) check(spd_context_init_comm(ctx.h, g.uid, g.rank, g.world));
   DevTensor B;
   upload(ctx, Bt, B);
-  std::vector<spd_color> cols(loop.pieces);
+  std::vector<spd_color> cols(P);
   if (loop.position_space)
-    check(spd_partition_nonzero(ctx.h, B.h, loop.split_level, loop.pieces, cols.data()));
+    check(spd_partition_nonzero(ctx.h, B.h, loop.split_level, P, cols.data()));
   else
-    check(spd_partition_universe(ctx.h, B.h, loop.pieces, cols.data()));
-  for (int64_t c = 0; c < loop.pieces; c++) {  // the GPU's partition must be the planner's
+    check(spd_partition_universe(ctx.h, B.h, P, cols.data()));
+  for (int64_t c = 0; c < P; c++) {  // the GPU's partition must be the planner's
     const CoordRange& want = loop.color_bounds[c];
     bool same = cols[c].color.lo == want.lo && cols[c].color.hi == want.hi;
     bool both_empty = cols[c].color.lo > cols[c].color.hi && want.empty();
     if (!same && !both_empty) throw std::logic_error("gpu partition differs from plan() colour bounds");
   }
-
   spd_stats st{};
   const std::vector<int64_t>& od = plan.dims.at(out_name);
-  SparseTensor out;
-
-  // Operands and the output buffer.
   std::map<std::string, DevTensor> dev;
   for (const auto& term : terms)
     for (const auto& a : term)
       if (a.tensor != b_name && !dev.count(a.tensor)) upload(ctx, tensors.at(a.tensor), dev[a.tensor]);
   const SparseTensor& outstub = tensors.at(out_name);
   DevTensor outbuf;
-  upload(ctx, outstub, outbuf);  // dense: zeros sized like the output; sparse: B's pattern reuse
-  double* outp = const_cast<double*>(dense_vals_dev(outbuf.h));
-
+  if (kernel != "spadd3") upload(ctx, outstub, outbuf);  // dense: zeros; sparse: B's pattern reuse
+  double* outp = kernel != "spadd3" ? const_cast<double*>(dense_vals_dev(outbuf.h)) : nullptr;
+  const int64_t f = g.first, n = g.count;
   if (kernel == "spmv") {
-    const std::string c = terms[0][1].tensor;
-    check(spd_spmv(ctx.h, B.h, dense_vals_dev(dev[c].h), outp, 0, loop.pieces, &st));
+    check(spd_spmv(ctx.h, B.h, dense_vals_dev(dev[terms[0][1].tensor].h), outp, f, n, &st));
   } else if (kernel == "spmm") {
-    const std::string c = terms[0][1].tensor;
-    check(spd_spmm(ctx.h, B.h, dense_vals_dev(dev[c].h), od[1], outp, 0, loop.pieces, &st));
+    check(spd_spmm(ctx.h, B.h, dense_vals_dev(dev[terms[0][1].tensor].h), od[1], outp, f, n, &st));
   } else if (kernel == "sddmm") {
     const SparseTensor& Ct = tensors.at(terms[0][1].tensor);
     const SparseTensor& Dt = tensors.at(terms[0][2].tensor);
-    int64_t K = Ct.dims()[1];
-    bool jmajor = Dt.format().mode_order[0] == 1;
-    check(spd_sddmm(ctx.h, B.h, dense_vals_dev(dev[terms[0][1].tensor].h),
-                    dense_vals_dev(dev[terms[0][2].tensor].h), K, jmajor ? 1 : Dt.dims()[1],
-                    jmajor ? K : 1, outp, 0, loop.pieces, &st));
+    const int64_t K = Ct.dims()[1];
+    const bool jmajor = Dt.format().mode_order[0] == 1;
+    check(spd_sddmm(ctx.h, B.h, dense_vals_dev(dev[terms[0][1].tensor].h), dense_vals_dev(dev[terms[0][2].tensor].h),
+                    K, jmajor ? 1 : Dt.dims()[1], jmajor ? K : 1, outp, f, n, &st));
   } else if (kernel == "spttv") {
-    check(spd_spttv(ctx.h, B.h, dense_vals_dev(dev[terms[0][1].tensor].h), outp, 0, loop.pieces, &st));
+    check(spd_spttv(ctx.h, B.h, dense_vals_dev(dev[terms[0][1].tensor].h), outp, f, n, &st));
   } else if (kernel == "spmttkrp") {
     check(spd_spmttkrp(ctx.h, B.h, dense_vals_dev(dev[terms[0][1].tensor].h),
-                       dense_vals_dev(dev[terms[0][2].tensor].h), od[1], outp, 0, loop.pieces, &st));
-  } else {  // spadd3: two-phase assembly on the GPU
+                       dense_vals_dev(dev[terms[0][2].tensor].h), od[1], outp, f, n, &st));
+  } else {  // spadd3: two-phase assembly per GPU, the row blocks gathered on rank 0
     spd_tensor* A = nullptr;
-    check(spd_spadd3(ctx.h, B.h, dev[terms[1][0].tensor].h, dev[terms[2][0].tensor].h, &A, 0,
-                     loop.pieces, &st));
-    DevTensor Ah;
+    check(spd_spadd3(ctx.h, B.h, dev[terms[1][0].tensor].h, dev[terms[2][0].tensor].h, &A, f, n, &st));
+    DevTensor Ah, Af;
     Ah.h = A;
-    int64_t par = 0, nnz = 0;
-    int k;
-    check(spd_tensor_level(A, 1, &k, &par, &nnz));
-    std::vector<CoordRange> pos(par);
-    std::vector<int64_t> crd(nnz);
-    std::vector<double> vals(nnz);
-    check(spd_tensor_download_level(A, 1, reinterpret_cast<int64_t*>(pos.data()), crd.data()));
-    check(spd_tensor_download_vals(A, vals.data()));
-    std::vector<LevelStorage> levels{std::get<DenseLevel>(Bt.level(0)),
-                                     CompressedLevel{Region::ranges(IndexSpace({par}), std::move(pos), nnz),
-                                                     Region::coordinates(IndexSpace({nnz}), std::move(crd))}};
-    out = SparseTensor::from_parts(od, plan.formats.at(out_name), std::move(levels), std::move(vals));
+    spd_tensor* whole = A;
+    if (g.world > 1) {
+      check(spd_gather_rows(ctx.h, A, 0, &Af.h));
+      whole = Af.h;
+    }
+    if (g.rank == 0) {
+      int64_t par = 0, nnz = 0;
+      int k;
+      check(spd_tensor_level(whole, 1, &k, &par, &nnz));
+      std::vector<CoordRange> pos(par);
+      std::vector<int64_t> crd(nnz);
+      std::vector<double> vals(nnz);
+      check(spd_tensor_download_level(whole, 1, reinterpret_cast<int64_t*>(pos.data()), crd.data()));
+      check(spd_tensor_download_vals(whole, vals.data()));
+      std::vector<LevelStorage> levels{std::get<DenseLevel>(Bt.level(0)),
+                                       CompressedLevel{Region::ranges(IndexSpace({par}), std::move(pos), nnz),
+                                                       Region::coordinates(IndexSpace({nnz}), std::move(crd))}};
+      g.spadd3_out = SparseTensor::from_parts(od, plan.formats.at(out_name), std::move(levels), std::move(vals));
+    }
   }
-  if (kernel != "spadd3") {
-    std::vector<double> vals(outstub.leaf_count());
-    check(spd_tensor_download_vals(outbuf.h, vals.data()));
+  if (kernel != "spadd3") {  // copy back the output range these colours own
+    int64_t lo = 0, hi = -1, width = 1;
+    if (kernel == "sddmm") {  // vals on B's pattern: the colours' positions
+      lo = cols[f].q.lo, hi = cols[f + n - 1].q.hi;
+      for (int64_t c = f; c < f + n; c++)
+        if (cols[c].q.lo <= cols[c].q.hi) lo = std::min(lo, cols[c].q.lo), hi = std::max(hi, cols[c].q.hi);
+    } else {
+      check(spd_last_owned(ctx.h, f, n, &lo, &hi));
+      if (kernel == "spmm" || kernel == "spmttkrp") width = od[1];
+    }
+    if (g.world == 1) {
+      lo = 0, hi = static_cast<int64_t>(out.size()) / width - 1;
+    }
+    if (lo <= hi) check(spd_tensor_download_vals_range(outbuf.h, lo * width, (hi - lo + 1) * width, out.data() + lo * width));
+  }
+  if (g.rank == 0) {
+    g.work.assign(P, 0);
+    check(spd_last_work(ctx.h, g.work.data(), P));
+    g.combines = st.combines;
+  }
+}
+
+ExecResult execute_gpu(const Plan& plan, const TensorSet& tensors, const MachineGrid& machine,
+                       const Residency& residency) {
+  if (plan.loops.size() == 2) {
+    const std::string k = kernel_of(plan);
+    if (k == "spmm" || k == "spmttkrp") return execute_batched(plan, tensors, machine, residency, k);
+    if (k == "sddmm" || k == "spttv") return execute_grid(plan, tensors, machine, residency, k);
+  }
+  if (plan.loops.size() != 1)
+    throw ValidationError("unsupported on gpu: one distributed loop, or a two-loop grid of SpMM / SpMTTKRP "
+                          "(batched) or SDDMM / SpTTV (rows x bucketed columns)");
+  const PlanLoop& loop = plan.loops[0];
+  const std::string kernel = kernel_of(plan);
+  const std::string out_name = plan.stmt.lhs.tensor;
+  const int64_t P = loop.pieces;
+  const int G = gpus_for(P);
+  const int64_t cmax = (P + G - 1) / G;
+  std::vector<GpuPart> parts(G);
+  std::vector<unsigned char> uid(128, 0);
+  if (G > 1) check(spd_nccl_unique_id(uid.data()));
+  const SparseTensor& outstub = tensors.at(out_name);
+  std::vector<double> out(kernel == "spadd3" ? 0 : static_cast<size_t>(outstub.leaf_count()), 0.0);
+  for (int r = 0; r < G; r++) {
+    parts[r].device = r, parts[r].rank = r, parts[r].world = G, parts[r].uid = uid.data();
+    parts[r].first = r * cmax;
+    parts[r].count = std::min<int64_t>(cmax, P - r * cmax);
+  }
+  if (G == 1) {
+    parts[0].first = 0, parts[0].count = P;
+    run_part(plan, tensors, kernel, parts[0], out);
+  } else {  // one host thread per GPU; errors are captured per thread and rethrown (sim.cpp:958-980)
+    std::vector<std::thread> pool;
+    std::vector<std::exception_ptr> errors(G);
+    for (int r = 0; r < G; r++)
+      pool.emplace_back([&, r] {
+        try {
+          run_part(plan, tensors, kernel, parts[r], out);
+        } catch (...) {
+          errors[r] = std::current_exception();
+        }
+      });
+    for (auto& t : pool) t.join();
+    for (auto& e : errors)
+      if (e) std::rethrow_exception(e);
+  }
+  SparseTensor result;
+  if (kernel == "spadd3") {
+    result = std::move(parts[0].spadd3_out);
+  } else {
     std::vector<LevelStorage> levels;
     for (int l = 0; l < outstub.num_levels(); l++) levels.push_back(outstub.level(l));
-    out = SparseTensor::from_parts(od, plan.formats.at(out_name), std::move(levels), std::move(vals));
+    result = SparseTensor::from_parts(plan.dims.at(out_name), plan.formats.at(out_name), std::move(levels),
+                                      std::move(out));
   }
-
-  ExecResult r{std::move(out), Stats{}};
-  std::vector<int64_t> work(loop.pieces);
-  check(spd_last_work(ctx.h, work.data(), loop.pieces));
+  ExecResult r{std::move(result), Stats{}};
   const std::vector<Task> tasks = tasks_of(plan, machine);
   std::vector<int64_t> task_work;
-  for (const auto& tk : tasks) task_work.push_back(work[static_cast<size_t>(tk.colors[0])]);
-  r.stats = make_stats(ctx.h, plan, tensors, machine, residency, tasks, task_work);
-  r.stats.combines = st.combines;
+  for (const auto& tk : tasks) task_work.push_back(parts[0].work[static_cast<size_t>(tk.colors[0])]);
+  Ctx lctx(0);  // the ledger's set counting
+  r.stats = make_stats(lctx.h, plan, tensors, machine, residency, tasks, task_work);
+  r.stats.combines = parts[0].combines;
   return r;
 }
 

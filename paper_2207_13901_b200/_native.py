@@ -42,6 +42,7 @@ class spd_stats(C.Structure):
 SIGNATURES = {
     "spd_last_error": (C.c_char_p, []),
     "spd_abi_version": (C.c_int, []),
+    "spd_device_count": (C.c_int, [C.POINTER(C.c_int)]),
     "spd_context_create": (C.c_int, [C.c_int, vp, C.POINTER(vp)]),
     "spd_context_destroy": (C.c_int, [vp]),
     "spd_context_synchronize": (C.c_int, [vp]),
@@ -89,6 +90,9 @@ SIGNATURES = {
     "spd_partition_universe": (C.c_int, [vp, vp, i64, C.POINTER(spd_color)]),
     "spd_partition_nonzero": (C.c_int, [vp, vp, C.c_int, i64, C.POINTER(spd_color)]),
     "spd_partition_materialize": (C.c_int, [vp, vp, C.c_int, C.c_int, i64, i64p, i64, i64p]),
+    "spd_partition_bucket": (C.c_int, [vp, vp, C.c_int, i64, i64p]),
+    "spd_bucket_positions": (C.c_int, [vp, i64, i64p, i64, i64p]),
+    "spd_bucket_grid_work": (C.c_int, [vp, i64p, i64, i64p]),
     "spd_spmv": (C.c_int, [vp, vp, vp, vp, i64, i64, C.POINTER(spd_stats)]),
     "spd_spmm": (C.c_int, [vp, vp, vp, i64, vp, i64, i64, C.POINTER(spd_stats)]),
     "spd_sddmm": (C.c_int, [vp, vp, vp, vp, i64, i64, i64, vp, i64, i64, C.POINTER(spd_stats)]),
@@ -109,6 +113,7 @@ SIGNATURES = {
     "spd_tensor_pack": (C.c_int, [vp, C.c_int, i64p, C.POINTER(C.c_int), C.POINTER(C.c_int), i64,
                                   C.POINTER(i64p), dblp, C.c_int, C.POINTER(vp)]),
     "spd_last_work": (C.c_int, [vp, i64p, i64]),
+    "spd_last_owned": (C.c_int, [vp, i64, i64, i64p, i64p]),
     "spd_context_timing": (C.c_int, [vp, C.c_int]),
     "spd_context_read_timing": (C.c_int, [vp, dblp, i64, i64p]),
     "spd_context_launches": (C.c_int, [vp, i64p]),

@@ -238,6 +238,16 @@ struct spd_context {
 
   std::vector<int64_t> last_work;    // per colour
   std::vector<spd_tensor*> pending_restage;  // tensors whose last restage verdict is still on its way
+  // Last bucket split (spd_partition_bucket): positions of the level sorted by
+  // colour (ascending within a colour), colour offsets, prefix sums of the
+  // leaf counts under the sorted positions.
+  struct Bucket {
+    const spd_tensor* tensor = nullptr;
+    int level = 0;
+    int64_t n = 0, pieces = 0;
+    int64_t *pos = nullptr, *pref = nullptr, *off = nullptr;
+    spd::DeviceBuffer keys, tmp, pos_buf, pref_buf, off_buf;
+  } bucket;
   spd::DeviceBuffer scratch[8];  // [7]: compacted x (SpMV)
   spd::DeviceBuffer counters;        // small int64 device counters
   int64_t* pinned_counters = nullptr;

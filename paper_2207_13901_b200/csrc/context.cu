@@ -337,7 +337,16 @@ void require_partition(spd_context* ctx, const spd_tensor* t, int64_t first, int
   if (first < 0 || count < 1 || first + count > ctx->pieces)
     throw ValidationError("colour range outside the partition");
   bool all = first == 0 && count == ctx->pieces;
-  bool one_per_rank = ctx->comm && count == 1 && ctx->pieces == ctx->world && first == ctx->rank;
+  // With a communicator a GPU runs one contiguous block of colours: rank r
+  // runs [r * cmax, min(P, (r + 1) * cmax)), cmax = ceil(P / world) -- one
+  // colour per GPU when P == world (the bench), several when the plan has
+  // more colours than GPUs (the integration adapter on a smaller box).
+  bool one_per_rank = false;
+  if (ctx->comm && ctx->pieces >= ctx->world) {
+    const int64_t cmax = ceil_div(ctx->pieces, ctx->world);
+    const int64_t f = ctx->rank * cmax;
+    one_per_rank = first == f && count >= 1 && count == std::min<int64_t>(cmax, ctx->pieces - f);
+  }
   // 2-D machine grid (x major, y minor; MachineGrid::worker_id, machine.cpp:88-92)
   // with the row loop on x: rank r runs row colour r / (world / pieces) of a
   // universe split -- rows never straddle colours, so no cross-GPU combine.
@@ -346,8 +355,8 @@ void require_partition(spd_context* ctx, const spd_tensor* t, int64_t first, int
                   first == ctx->rank / (ctx->world / ctx->pieces);
   if (!all && !one_per_rank && !grid_row)
     throw ValidationError(
-        "a GPU runs either every colour of the partition, or (with a communicator) exactly the "
-        "colour equal to its rank with pieces == world (row loops of a 2-D grid: colour rank / (world / pieces))");
+        "a GPU runs either every colour of the partition, or (with a communicator) its block of colours "
+        "[rank * ceil(pieces / world), ...) (row loops of a 2-D grid: colour rank / (world / pieces))");
 }
 
 void fill_stats(spd_context* ctx, spd_stats* st, int64_t combines, const std::vector<int64_t>& work,
@@ -435,6 +444,18 @@ int spd_context_launches(const spd_context* ctx, int64_t* count) {
 const char* spd_last_error(void) { return g_last_error.c_str(); }
 int spd_abi_version(void) { return 100; }
 
+int spd_device_count(int* count) {
+  return guarded([&] {
+    if (!count) throw ValidationError("null out pointer");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    *count = n;
+  });
+}
+
 int spd_context_create(int device, void* stream, spd_context** out) {
   return guarded([&] {
     if (!out) throw ValidationError("null out pointer");
@@ -477,6 +498,9 @@ int spd_context_destroy(spd_context* ctx) {
     ctx->colors_dev.release();
     for (auto& b : ctx->scratch) b.release();
     ctx->counters.release();
+    for (auto* b : {&ctx->bucket.keys, &ctx->bucket.tmp, &ctx->bucket.pos_buf, &ctx->bucket.pref_buf,
+                    &ctx->bucket.off_buf})
+      b->release();
     if (ctx->pinned_counters) cudaFreeHost(ctx->pinned_counters);
     for (cudaEvent_t e : ctx->timing_events) cudaEventDestroy(e);
     if (ctx->aux) cudaStreamSynchronize(ctx->aux), cudaStreamDestroy(ctx->aux);
@@ -1025,6 +1049,7 @@ int spd_tensor_destroy(spd_tensor* t) {
       ctx->split = SplitKind::None;
       ctx->split_tensor = nullptr;
     }
+    if (ctx->bucket.tensor == t) ctx->bucket.tensor = nullptr;
     if (t->restage_pending) {  // the verdict is dropped with the tensor
       cudaEventSynchronize(t->restage_done);
       auto& pend = ctx->pending_restage;
@@ -1181,6 +1206,24 @@ int spd_tensor_download_vals_range(const spd_tensor* t, int64_t first, int64_t c
       SPD_CUDA(cudaMemcpyAsync(vals, t->vals + first, sizeof(double) * count,
                                cudaMemcpyDeviceToHost, ctx->stream));
     SPD_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int spd_last_owned(spd_context* ctx, int64_t first, int64_t count, int64_t* lo, int64_t* hi) {
+  return guarded([&] {
+    checked(ctx);
+    if (!lo || !hi) throw ValidationError("null argument");
+    if (first < 0 || count < 1 || first + count > ctx->pieces) throw ValidationError("colour range outside the partition");
+    activate(ctx);
+    std::vector<DevColor> d(count);
+    SPD_CUDA(cudaMemcpyAsync(d.data(), (const DevColor*)ctx->colors_dev.ptr + first, sizeof(DevColor) * count,
+                             cudaMemcpyDeviceToHost, ctx->stream));
+    SPD_CUDA(cudaStreamSynchronize(ctx->stream));
+    *lo = INT64_MAX;
+    *hi = -1;
+    for (const DevColor& c : d)
+      if (c.w_lo <= c.w_hi) *lo = std::min(*lo, c.w_lo), *hi = std::max(*hi, c.w_hi);
+    if (*hi < 0) *lo = 0;
   });
 }
 

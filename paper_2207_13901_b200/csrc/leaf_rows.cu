@@ -1061,7 +1061,14 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   rec.cont = (int*)ctx->scratch[1].reserve(sizeof(int) * max_chunks);
   rec.val = (double*)ctx->scratch[2].reserve(sizeof(double) * 2 * max_chunks * W);
   ColorRecs col;
-  col.head_pack = (int64_t*)ctx->scratch[3].reserve(sizeof(int64_t) * P * (W + 2));
+  // colour blocks per GPU (require_partition): the head records of rank r's
+  // block sit at slots [r * cmax, r * cmax + cmax) so one all-gather of cmax
+  // slots per rank lays every colour's record at its own slot
+  const bool cross_gpu = ctx->comm && ctx->world > 1 && P > 1 && ctx->split != SplitKind::Universe &&
+                         !(first == 0 && count == P);
+  const int64_t cmax = cross_gpu ? ceil_div(P, ctx->world) : 1;
+  const int64_t pack_slots = cross_gpu ? cmax * ctx->world : P;
+  col.head_pack = (int64_t*)ctx->scratch[3].reserve(sizeof(int64_t) * pack_slots * (W + 2));
   char* cr = (char*)ctx->scratch[4].reserve(sizeof(int64_t) * (P + 4) + sizeof(double) * P * W);
   col.counters = (int64_t*)cr;
   col.tail_row = col.counters + 4;
@@ -1071,7 +1078,7 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   int64_t launches = 0;
   if (stats) SPD_CUDA(cudaEventRecord(ctx->ev0, s));
   trace_mark(ctx);
-  SPD_CUDA(cudaMemsetAsync(col.head_pack, 0xff, sizeof(int64_t) * P * (W + 2), s));
+  SPD_CUDA(cudaMemsetAsync(col.head_pack, 0xff, sizeof(int64_t) * pack_slots * (W + 2), s));
   SPD_CUDA(cudaMemsetAsync(col.counters, 0, sizeof(int64_t) * 4, s));
   SPD_CUDA(cudaMemsetAsync(col.tail_row, 0xff, sizeof(int64_t) * P, s));
   ht.mark("scratch");
@@ -1293,10 +1300,9 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
     launches++;
   }
   trace_mark(ctx);
-  if (ctx->comm && count == 1 && P > 1 && ctx->split != SplitKind::Universe) {  // rows cut between GPUs
-    const size_t bytes = sizeof(int64_t) * (W + 2);
-    SPD_NCCL(ncclAllGather(col.head_pack + first * (W + 2), col.head_pack, bytes, ncclUint8,
-                           ctx->comm, s));
+  if (cross_gpu) {  // rows cut between GPUs: every colour's head record to every GPU
+    const size_t bytes = sizeof(int64_t) * cmax * (W + 2);
+    SPD_NCCL(ncclAllGather(col.head_pack + first * (W + 2), col.head_pack, bytes, ncclUint8, ctx->comm, s));
   }
   trace_mark(ctx);
   k_colour_combine<<<(unsigned)ceil_div(P * 32, 256), 256, 0, s>>>(

@@ -16,6 +16,7 @@
 //     of the ends are project_to_universe's [min, max] (planner.cpp:50-69).
 // One warp per colour; O(P) probes, so this is a latency kernel.
 #include <algorithm>
+#include <cub/cub.cuh>
 
 #include "common.cuh"
 
@@ -161,9 +162,180 @@ __global__ void k_flag_preimage(const int64_t* __restrict__ rowptr, int64_t lo, 
   }
 }
 
+
+// ---- universe split of a compressed level (bucketCoords) ------------------
+// LevelPartitioner::finalize, compressed universe entry
+// (level_partition.cpp:193-205): colour c holds the positions of the level
+// whose coordinate lies in divide_bounds(extent, P)[c] -- bucketed by
+// coordinate, not contiguous in position space.
+__device__ __forceinline__ int64_t bucket_of(int64_t j, int64_t extent, int64_t pieces) {
+  const int64_t block = extent / pieces;  // divide_bounds: the last colour takes the rest
+  if (block == 0) return pieces - 1;
+  const int64_t c = j / block;
+  return c < pieces - 1 ? c : pieces - 1;
+}
+
+__global__ void k_bucket_keys(const int64_t* __restrict__ crd, int64_t n, int64_t extent, int64_t pieces,
+                              int32_t* __restrict__ keys, int64_t* __restrict__ pos) {
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < n; q += (int64_t)gridDim.x * blockDim.x) {
+    keys[q] = (int32_t)bucket_of(__ldg(crd + q), extent, pieces);
+    pos[q] = q;
+  }
+}
+
+// weight of a bucketed position: its leaf count (the rows of the next level
+// it spans, product of dense extents below) -- 1 on the leaf level
+__global__ void k_bucket_weights(const int64_t* __restrict__ sorted_pos, int64_t n,
+                                 const int64_t* __restrict__ next_rowptr, int64_t* __restrict__ w) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t q = sorted_pos[i];
+    w[i] = next_rowptr ? __ldg(next_rowptr + q + 1) - __ldg(next_rowptr + q) : 1;
+  }
+}
+
+// colour boundaries in the sorted keys
+__global__ void k_bucket_bounds(const int32_t* __restrict__ keys, int64_t n, int64_t pieces,
+                                int64_t* __restrict__ off) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c <= pieces; c += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = 0, hi = n;  // first index with key >= c
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < c) lo = mid + 1; else hi = mid;
+    }
+    off[c] = lo;
+  }
+}
+
+// leaf positions of bucket y inside level-position span x: two searches in
+// the bucket's ascending positions, a difference of the weight prefix sums
+__global__ void k_bucket_grid(const int64_t* __restrict__ pos, const int64_t* __restrict__ pref,
+                              const int64_t* __restrict__ off, int64_t Y, const int64_t* __restrict__ spans,
+                              int64_t X, int64_t* __restrict__ out) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= X * Y) return;
+  const int64_t x = t / Y, y = t % Y;
+  const int64_t lo = spans[2 * x], hi = spans[2 * x + 1];
+  if (lo > hi) {
+    out[t] = 0;
+    return;
+  }
+  int64_t a = off[y], b = off[y + 1];
+  while (a < b) {
+    const int64_t mid = (a + b) >> 1;
+    if (pos[mid] < lo) a = mid + 1; else b = mid;
+  }
+  int64_t c = a, d = off[y + 1];
+  while (c < d) {
+    const int64_t mid = (c + d) >> 1;
+    if (pos[mid] <= hi) c = mid + 1; else d = mid;
+  }
+  out[t] = pref[c] - pref[a];
+}
+
 }  // namespace spd
 
 using namespace spd;
+
+static void run_bucket(spd_context* ctx, const spd_tensor* t, int level, int64_t pieces, int64_t* counts_out) {
+  checked(ctx);
+  if (!t) throw ValidationError("null tensor");
+  if (pieces < 1) throw ValidationError("pieces must be positive");
+  if (level < 1 || level >= (int)t->levels.size() || t->levels[level].kind != SPD_COMPRESSED)
+    throw ValidationError("unsupported on gpu: the bucket split needs an inner compressed level");
+  if (t->piece) throw ValidationError("unsupported on gpu: bucket split of a placed piece");
+  activate(ctx);
+  settle_restage(t);
+  const spd_level_store& L = t->levels[level];
+  const int64_t n = L.positions;
+  const int64_t extent = t->dims[t->mode_order[t->groups[level][0]]];
+  cudaStream_t s = ctx->stream;
+  auto& B = ctx->bucket;
+  B.n = n;
+  B.pieces = pieces;
+  int32_t* keys = (int32_t*)B.keys.reserve(sizeof(int32_t) * 2 * (n > 0 ? n : 1));
+  int32_t* keys_out = keys + (n > 0 ? n : 1);
+  int64_t* pos_in = (int64_t*)B.tmp.reserve(sizeof(int64_t) * 2 * (n + 1));
+  int64_t* w = pos_in + (n + 1);
+  B.pos = (int64_t*)B.pos_buf.reserve(sizeof(int64_t) * (n > 0 ? n : 1));
+  B.pref = (int64_t*)B.pref_buf.reserve(sizeof(int64_t) * (n + 1));
+  B.off = (int64_t*)B.off_buf.reserve(sizeof(int64_t) * (pieces + 1));
+  const unsigned grid = (unsigned)std::min<int64_t>(std::max<int64_t>(ceil_div(n, 256), 1), ctx->num_sms * 16);
+  SPD_CUDA(cudaMemsetAsync(B.pref, 0, sizeof(int64_t), s));
+  if (n > 0) {
+    k_bucket_keys<<<grid, 256, 0, s>>>(L.crd, n, extent, pieces, keys, pos_in);
+    SPD_CHECK_LAUNCH();
+    int bits = 1;
+    while ((int64_t(1) << bits) < pieces) bits++;
+    size_t bytes = 0;  // stable: positions stay ascending within a colour
+    SPD_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys, keys_out, pos_in, B.pos, n, 0, bits, s));
+    void* tmp = ctx->scratch[5].reserve(bytes);
+    SPD_CUDA(cub::DeviceRadixSort::SortPairs(tmp, bytes, keys, keys_out, pos_in, B.pos, n, 0, bits, s));
+    const bool leaf = level + 1 == (int)t->levels.size();
+    k_bucket_weights<<<grid, 256, 0, s>>>(B.pos, n, leaf ? nullptr : t->levels[level + 1].rowptr, w);
+    SPD_CHECK_LAUNCH();
+    bytes = 0;
+    SPD_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, w, B.pref + 1, n, s));
+    tmp = ctx->scratch[5].reserve(bytes);
+    SPD_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, w, B.pref + 1, n, s));
+    ctx->launches += 4;
+  }
+  k_bucket_bounds<<<(unsigned)ceil_div(pieces + 1, 256), 256, 0, s>>>(keys_out, n, pieces, B.off);
+  SPD_CHECK_LAUNCH();
+  ctx->launches++;
+  B.tensor = t;
+  B.level = level;
+  std::vector<int64_t> off(pieces + 1);
+  SPD_CUDA(cudaMemcpyAsync(off.data(), B.off, sizeof(int64_t) * (pieces + 1), cudaMemcpyDeviceToHost, s));
+  SPD_CUDA(cudaStreamSynchronize(s));
+  if (counts_out)
+    for (int64_t c = 0; c < pieces; c++) counts_out[c] = off[c + 1] - off[c];
+}
+
+extern "C" {
+
+int spd_partition_bucket(spd_context* ctx, const spd_tensor* t, int level, int64_t pieces, int64_t* counts_out) {
+  return guarded([&] { run_bucket(ctx, t, level, pieces, counts_out); });
+}
+
+int spd_bucket_positions(spd_context* ctx, int64_t color, int64_t* out, int64_t cap, int64_t* count) {
+  return guarded([&] {
+    checked(ctx);
+    auto& B = ctx->bucket;
+    if (!B.tensor) throw ValidationError("no bucket split on the context: call spd_partition_bucket first");
+    if (color < 0 || color >= B.pieces) throw ValidationError("no such colour");
+    if (!count) throw ValidationError("null argument");
+    activate(ctx);
+    int64_t o[2];
+    SPD_CUDA(cudaMemcpy(o, B.off + color, sizeof(o), cudaMemcpyDeviceToHost));
+    *count = o[1] - o[0];
+    const int64_t k = std::min<int64_t>(*count, cap);
+    if (k > 0 && out) SPD_CUDA(cudaMemcpy(out, B.pos + o[0], sizeof(int64_t) * k, cudaMemcpyDeviceToHost));
+  });
+}
+
+int spd_bucket_grid_work(spd_context* ctx, const int64_t* spans, int64_t nspans, int64_t* out) {
+  return guarded([&] {
+    checked(ctx);
+    auto& B = ctx->bucket;
+    if (!B.tensor) throw ValidationError("no bucket split on the context: call spd_partition_bucket first");
+    if (nspans < 0 || (nspans > 0 && (!spans || !out))) throw ValidationError("null argument");
+    if (nspans == 0) return;
+    activate(ctx);
+    cudaStream_t s = ctx->stream;
+    const int64_t cells = nspans * B.pieces;
+    int64_t* d = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (2 * nspans + cells));
+    SPD_CUDA(cudaMemcpyAsync(d, spans, sizeof(int64_t) * 2 * nspans, cudaMemcpyHostToDevice, s));
+    k_bucket_grid<<<(unsigned)ceil_div(cells, 256), 256, 0, s>>>(B.pos, B.pref, B.off, B.pieces, d, nspans,
+                                                                  d + 2 * nspans);
+    SPD_CHECK_LAUNCH();
+    ctx->launches++;
+    SPD_CUDA(cudaMemcpyAsync(out, d + 2 * nspans, sizeof(int64_t) * cells, cudaMemcpyDeviceToHost, s));
+    SPD_CUDA(cudaStreamSynchronize(s));
+    dev_free(ctx, d);
+  });
+}
+
+}  // extern "C"
 
 static void run_partition(spd_context* ctx, const spd_tensor* t, int level, int64_t pieces,
                           bool nonzero, spd_color* colors_out) {

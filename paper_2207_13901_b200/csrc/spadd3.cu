@@ -412,7 +412,7 @@ static void run_spadd3(spd_context* ctx, const spd_tensor* B, const spd_tensor* 
   Csr c{C->levels[1].rowptr, C->levels[1].crd, C->vals};
   Csr d{D->levels[1].rowptr, D->levels[1].crd, D->vals};
   const int64_t nc = C->levels[1].positions, nd = D->levels[1].positions;
-  const bool distributed = ctx->comm && count == 1 && ctx->pieces > 1;
+  const bool distributed = ctx->comm && ctx->world > 1 && ctx->pieces > 1 && !(first == 0 && count == ctx->pieces);
   // rows of this call: the colours' row blocks (a universe split is contiguous)
   const auto& hc = host_colors(ctx);
   int64_t lo = n, hi = -1;

@@ -114,3 +114,15 @@ def assemble_csr(pieces, nrows: int):
             rp[i] = rp[i - 1]
     return rp, (np.concatenate(crds) if crds else np.zeros(0, np.int64)), \
         (np.concatenate(vals) if vals else np.zeros(0))
+
+
+def colour_blocks(pieces: int, gpus: int):
+    """The colour-to-GPU mapping of a P-colour plan on G GPUs (the
+    integration adapter's execute_gpu, the library's require_partition):
+    cmax = ceil(P / G) consecutive colours per GPU, rank r running
+    [r * cmax, min(P, (r + 1) * cmax)); only as many GPUs as get a colour are
+    used.  Returns [(first, count)] per used GPU."""
+    g = max(1, min(gpus, max(pieces, 1)))
+    cmax = -(-max(pieces, 1) // g)
+    used = max(1, -(-max(pieces, 1) // cmax))
+    return [(r * cmax, min(cmax, pieces - r * cmax)) for r in range(used)]

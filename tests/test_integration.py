@@ -195,3 +195,88 @@ def test_transposed_storage_is_rejected(gpu_lib, case):
     if run.status == 2 and "unsupported on gpu" not in run.error:
         pytest.skip(f"the reference itself rejects this schedule: {run.error}")
     assert run.status == 2 and "unsupported on gpu" in run.error, run.error
+
+
+@pytest.mark.parametrize("kernel", list(KERNELS))
+def test_every_visible_gpu_gives_the_one_gpu_result(gpu_lib, kernel):
+    """execute_gpu spreads the colours over every visible GPU (one host thread
+    per GPU, NCCL boundary combine, SpAdd3 row blocks gathered); capped to one
+    GPU with DSPAR_GPUS=1 it runs them all on device 0.  Both give the same
+    output and Stats as the reference (on a one-GPU box both runs take the
+    one-GPU path)."""
+    import torch
+
+    spec = KERNELS[kernel]
+    sched = spec["nonzero"] or ROW
+    rng = np.random.default_rng(31)
+    for pieces in (3, 5):
+        t = K.instance(kernel, rng, integers=True)
+        args = (spec["expr"], sched, pieces, spec["formats"][OUTPUT[kernel]], ref_inputs(kernel, t))
+        want = ob.RefRun(*args, mode="par", use_placements=True).ok()
+        outs = []
+        for cap in (None, "1"):
+            if cap:
+                os.environ["DSPAR_GPUS"] = cap
+            try:
+                got = ob.RefRun(*args, mode="gpu", use_placements=True, lib=gpu_lib).ok()
+            finally:
+                os.environ.pop("DSPAR_GPUS", None)
+            outs.append(got.output())
+            assert _stats_json(got) == _stats_json(want), (kernel, pieces, cap, torch.cuda.device_count())
+        (l0, v0), (l1, v1) = outs
+        assert np.array_equal(v0, v1) and np.array_equal(v0, want.output()[1])
+
+
+GRID = ("divide(i, io, ii, M.x); divide(j, jo, ji, M.y); reorder(io, jo, ii, ji, k); "
+        "distribute(io, M.x); distribute(jo, M.y)")
+
+
+@pytest.mark.parametrize("kernel", ["sddmm", "spttv"])
+@pytest.mark.parametrize("grid", ["x=2,y=2", "x=3,y=2", "x=1,y=4", "x=4,y=3"])
+def test_two_dimensional_grid_with_bucketed_columns(gpu_lib, kernel, grid):
+    """Rows over M.x, the compressed level's coordinate j over M.y (the inner
+    universe split, level_partition.cpp:193-205): output, per-worker work,
+    imbalance and the ledger equal the reference's execute."""
+    spec = KERNELS[kernel]
+    rng = np.random.default_rng(17)
+    for _ in range(2):
+        t = K.instance(kernel, rng, integers=True, max_dim=30)
+        args = (spec["expr"], GRID, grid, spec["formats"]["A"], ref_inputs(kernel, t))
+        want = ob.RefRun(*args, mode="par", use_placements=True).ok()
+        got = ob.RefRun(*args, mode="gpu", use_placements=True, lib=gpu_lib).ok()
+        assert np.array_equal(want.output()[1], got.output()[1])
+        assert _stats_json(got) == _stats_json(want)
+
+
+@pytest.mark.parametrize("kernel", ["sddmm", "spttv"])
+@pytest.mark.parametrize("pieces", [1, 2, 3, 5, 40])
+def test_bucket_split_equals_the_reference_bundle(gpu_lib, kernel, pieces):
+    """spd_partition_bucket's colour sets are the reference's crd partition of
+    B's level 1 for the bucketed loop (bucketCoords), empty colours included."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2207_13901_b200 import _native as N
+    from paper_2207_13901_b200 import host as H
+
+    spec = KERNELS[kernel]
+    rng = np.random.default_rng(pieces)
+    t = K.instance(kernel, rng, integers=True, max_dim=30)
+    run = ob.RefRun(spec["expr"], GRID, f"x=1,y={pieces}", spec["formats"]["A"], ref_inputs(kernel, t),
+                    execute=False).ok()
+    ctx = H.Context(0)
+    try:
+        dev = H.DeviceTensor.upload(ctx, t["B"])
+        counts = np.zeros(pieces, np.int64)
+        N.check(N.lib().spd_partition_bucket(ctx.h, dev.h, 1, pieces, counts.ctypes.data_as(N.i64p)))
+        for c in range(pieces):
+            want = run.subset("B", 1, "crd", c, k=1)
+            buf = np.zeros(max(int(counts[c]), 1), np.int64)
+            n = C.c_int64()
+            N.check(N.lib().spd_bucket_positions(ctx.h, c, buf.ctypes.data_as(N.i64p), len(buf), C.byref(n)))
+            assert n.value == counts[c] == len(want)
+            assert np.array_equal(buf[:n.value], want)
+        dev.close()
+    finally:
+        ctx.close()

@@ -246,3 +246,22 @@ def test_two_rank_protocol(worker):
     target = {"sddmm": _sddmm_worker, "spttv": _spttv_worker, "spmttkrp": _spmttkrp_worker,
               "spadd3": _spadd3_worker}[worker]
     assert _run(target)
+
+
+def test_colour_blocks_tile_the_partition():
+    """Every colour runs on exactly one GPU, in ascending blocks, every used
+    GPU gets at least one colour (the execute_gpu / require_partition rule)."""
+    from paper_2207_13901_b200.distributed import colour_blocks
+
+    for P in range(1, 40):
+        for G in range(1, 10):
+            blocks = colour_blocks(P, G)
+            assert 1 <= len(blocks) <= min(P, G)
+            cmax = blocks[0][1]
+            seen = []
+            for r, (f, c) in enumerate(blocks):
+                assert c >= 1 and f == r * cmax and c <= cmax
+                seen += list(range(f, f + c))
+            assert seen == list(range(P))
+    assert colour_blocks(8, 8) == [(c, 1) for c in range(8)]  # the bench: one colour per GPU
+    assert colour_blocks(5, 4) == [(0, 2), (2, 2), (4, 1)]
