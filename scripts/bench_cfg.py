@@ -31,6 +31,7 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+L2_GATHER_PEAK_GBS = 20776.5  # profiles/r02_probe_gather.jsonl, uniform_16MB, best variant
 
 
 def _ob():
@@ -434,6 +435,16 @@ def config_c4(env, H, synth):
                      "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms, "gpu_launches": nl,
                      "roofline": roofline(env, by / env.world, leaf, kern),
                      "effective_gbs": by / (ms * 1e-3) / 1e9}
+        if "MTT" in name and leaf > 0:
+            # both factors (C 2.4 MB, D 7.4 MB) sit in L2: the leaf is bound by
+            # L2 -> SM bytes, two 256-byte row reads per position, against the
+            # measured L2-resident gather ceiling (profiles/r02_probe_gather.jsonl)
+            l2b = 2.0 * 256 * nnz / env.world
+            ach = l2b / (leaf * 1e-3) / 1e9
+            res[name]["roofline_l2"] = {"bound": "l2", "achieved": ach, "peak": L2_GATHER_PEAK_GBS, "unit": "GB/s",
+                                        "frac": ach / L2_GATHER_PEAK_GBS, "bytes_per_launch": l2b,
+                                        "peak_source": "measured: 256-byte row gathers from a 16 MB working set, "
+                                                       "scripts/probe_gather.py"}
     Bt.close()
     if env.world == 1:
         rs, nbytes, st = _restager(env, H, (I, J, Kd), fmt, [rp1, rp2], [crd1, crd2], vals)
