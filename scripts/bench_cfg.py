@@ -316,26 +316,71 @@ def config_c3(env, H, rm):
     n, Bstep = rm["n"], rm["Bstep"]
     nnz = rm["crd_d"].numel()
     from paper_2207_13901_b200 import _native as NN
-    C_d = torch.empty(n * K, dtype=torch.float64, device=env.dev)
-    D_d = torch.empty(n * K, dtype=torch.float64, device=env.dev)
-    if env.rank == 0:  # generated on the device side in slabs from pinned staging
-        for dst, seed in ((C_d, 44), (D_d, 45)):
-            host = torch.empty(n * K, dtype=torch.float64).pin_memory()
-            NN.synth().syn_dense(n * K, seed, 0, C.cast(host.data_ptr(), NN.dblp))
-            dst.copy_(host)
-            if dst is C_d:
-                C_h = host
-            else:
-                D_h = host
-    if env.world > 1:
-        env.dist.broadcast(C_d, 0)
-        env.dist.broadcast(D_d, 0)
-    A_d = torch.empty(nnz, dtype=torch.float64, device=env.dev)
     first, count, P = env.colours()
+    placement = None
+    C_h = D_h = None
+    if env.rank == 0:  # host operands, pinned (the e2e leg copies them every step)
+        C_h = torch.empty(n * K, dtype=torch.float64).pin_memory()
+        NN.synth().syn_dense(n * K, 44, 0, C.cast(C_h.data_ptr(), NN.dblp))
+        D_h = torch.empty(n * K, dtype=torch.float64).pin_memory()
+        NN.synth().syn_dense(n * K, 45, 0, C.cast(D_h.data_ptr(), NN.dblp))
+    if env.world == 1:
+        C_d = C_h.to(env.dev)
+        D_d = D_h.to(env.dev)
+        C_ptr = C_d
+    else:
+        # D block-distributed over the GPUs, then all-gathered over
+        # NVLink (spd_allgather) -- reported as placement, outside the step;
+        # C held only as the projected row slab of this GPU's colour
+        # (planner.cpp:278-293): the leaf reads rows [top.lo, top.hi] only.
+        dist = env.dist
+        cols = H.partition_nonzero(env.ctx, Bstep, 1, P)
+        per = -(-n // env.world)
+        D_d = torch.zeros(env.world * per * K, dtype=torch.float64, device=env.dev)
+        t_lo, t_hi = cols[env.rank].top
+        rows = max(t_hi - t_lo + 1, 0)
+        C_slab = torch.empty(max(rows, 1) * K, dtype=torch.float64, device=env.dev)
+        for r in range(env.world):
+            d_lo, d_hi = r * per, min(n, (r + 1) * per) - 1
+            c_lo, c_hi = cols[r].top
+            if env.rank == 0:
+                dblk = D_h[d_lo * K:(d_hi + 1) * K].to(env.dev) if d_hi >= d_lo else None
+                cblk = C_h[c_lo * K:(c_hi + 1) * K].to(env.dev) if c_hi >= c_lo else None
+                if r == 0:
+                    if dblk is not None:
+                        D_d[d_lo * K:(d_hi + 1) * K].copy_(dblk)
+                    if cblk is not None:
+                        C_slab[:cblk.numel()].copy_(cblk)
+                else:
+                    if dblk is not None:
+                        dist.send(dblk, r)
+                    if cblk is not None:
+                        dist.send(cblk, r)
+            elif env.rank == r:
+                if d_hi >= d_lo:
+                    dist.recv(D_d[d_lo * K:(d_hi + 1) * K], 0)
+                if c_hi >= c_lo:
+                    buf = torch.empty((c_hi - c_lo + 1) * K, dtype=torch.float64, device=env.dev)
+                    dist.recv(buf, 0)
+                    C_slab[:buf.numel()].copy_(buf)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        env.ctx.allgather(D_d, per * K * 8)
+        e1.record()
+        torch.cuda.synchronize()
+        ag_ms = env.maxr([e0.elapsed_time(e1)])[0]
+        placement = {"D_allgather_ms": ag_ms, "D_bytes_received_per_gpu": (env.world - 1) * per * K * 8,
+                     "C_slab_rows": rows, "C_slab_bytes": rows * K * 8,
+                     "note": "D (n x 128, j-major) block-distributed then all-gathered over NVLink; C held as "
+                             "this GPU's projected row slab; outside the timed step"}
+        C_ptr = C_slab.data_ptr() - t_lo * K * 8  # global row i at C_ptr + i*K
+    A_d = torch.empty(nnz, dtype=torch.float64, device=env.dev)
 
     def step():
         H.partition_nonzero(env.ctx, Bstep, 1, P, host=False)
-        H.sddmm(env.ctx, Bstep, C_d, D_d, K, 1, K, A_d, first=first, count=count, pieces=P, stats=False)
+        H.sddmm(env.ctx, Bstep, C_ptr, D_d, K, 1, K, A_d, first=first, count=count, pieces=P, stats=False)
 
     ms, leaf, nl = measure(env, step)
     flops = 2.0 * nnz * K
@@ -344,7 +389,7 @@ def config_c3(env, H, rm):
                        f"j-major (dd:1,0), nonzero split into {P} colour(s)",
            "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms, "gpu_launches": nl,
            "roofline": roofline(env, by / env.world, leaf, "k_sddmm_nz<4,3>"),
-           "effective_gbs": by / (ms * 1e-3) / 1e9}
+           "effective_gbs": by / (ms * 1e-3) / 1e9, "placement": placement}
     if env.world == 1:
         rp, crd, vals = rm["host"]
         rs, nbytes, st = _restager(env, H, (n, n), H.parse_format("ds"), [rp], [crd], vals)
@@ -360,7 +405,6 @@ def config_c3(env, H, rm):
 
         out["e2e"] = e2e_loop(env, one, flops, nbytes + 2 * n * K * 8, nnz * 8)
         st["t"].close()
-        del C_h, D_h
         if not env.args.no_cpu_baseline:
             sc = env.args.sddmm_ref_scale
             n2, rp2, crd2, vals2 = rm["gen"](sc)
@@ -376,7 +420,7 @@ def config_c3(env, H, rm):
                 max(1, min(env.host_cores, 16)),
                 f"bounded sample: R-MAT scale {sc} ({n2} rows, {len(crd2)} nnz) -- execute() allocates a dense "
                 f"accumulator of the whole output space per task (sim.cpp:949-950), so scale 24 cannot run")
-    del C_d, D_d, A_d
+    del D_d, A_d, C_h, D_h
     return out
 
 
