@@ -757,6 +757,7 @@ static void restage_piece(spd_context* ctx, spd_tensor* t, const int64_t* const*
   t->cref = nullptr;
   t->nref = -1;
   if (ctx->split_tensor == t) ctx->split = SplitKind::None, ctx->split_tensor = nullptr;
+  if (ctx->bucket.tensor == t) ctx->bucket.tensor = nullptr;
 }
 
 // 3-level trees (dss / sss, the CSF of SpTTV / SpMTTKRP): the upper levels
@@ -987,6 +988,7 @@ int spd_tensor_restage(spd_context* ctx, spd_tensor* t, const int64_t* const* po
     dev_free(ctx, t->leaf_rowptr);
     t->leaf_rowptr = nullptr;
     if (ctx->split_tensor == t) ctx->split = SplitKind::None, ctx->split_tensor = nullptr;
+    if (ctx->bucket.tensor == t) ctx->bucket.tensor = nullptr;  // a function of the old pattern
     ht.mark("queued");
   });
 }
