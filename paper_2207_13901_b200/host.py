@@ -751,6 +751,14 @@ def spmv(ctx, B: DeviceTensor, c, a, first=0, count=None, pieces=None, stats=Tru
     return _stats(ctx, st, pieces) if stats else None
 
 
+def last_owned(ctx, first, count):
+    """spd_last_owned: (lo, hi) output rows (fibres for SpTTV) the colours
+    [first, first + count) stored in the last row-reducing op."""
+    lo, hi = C.c_int64(), C.c_int64()
+    check(N.lib().spd_last_owned(ctx.h, first, count, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
 def spmm(ctx, B: DeviceTensor, Cd, n_cols, A, first=0, count=None, pieces=None, stats=True):
     st = N.spd_stats()
     count = pieces - first if count is None else count

@@ -151,6 +151,40 @@ def e2e_loop(env, one_step, flops, h2d, d2h):
             "d2h_bytes_per_step": int(d2h), "ms_per_step": dt * 1e3}
 
 
+def mgpu_check(env, H, out_d, width, span, reference):
+    """N > 1: this rank's share of the distributed output (`span` = (lo, hi)
+    rows / fibres / positions it stores, `width` values each) is sent to rank
+    0 and compared bit-exactly with `reference()` -- rank 0 running every
+    colour of the same partition on its own GPU without a communicator (same
+    combine order, same bits).  Outside the timed region."""
+    torch, dist = env.torch, env.dist
+    spans = [None] * env.world
+    dist.all_gather_object(spans, tuple(int(x) for x in span))
+    ref = reference() if env.rank == 0 else None
+    ok = True
+    for r, (lo, hi) in enumerate(spans):
+        if lo > hi:
+            continue
+        if r == env.rank == 0:
+            ok = ok and bool(torch.equal(out_d[lo * width:(hi + 1) * width], ref[lo * width:(hi + 1) * width]))
+        elif env.rank == r:
+            dist.send(out_d[lo * width:(hi + 1) * width].contiguous(), 0)
+        elif env.rank == 0:
+            buf = torch.empty((hi - lo + 1) * width, dtype=out_d.dtype, device=env.dev)
+            dist.recv(buf, r)
+            ok = ok and bool(torch.equal(buf, ref[lo * width:(hi + 1) * width]))
+    t = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device=env.dev)
+    dist.broadcast(t, 0)
+    return {"bit_exact_vs_one_gpu": bool(t[0] > 0.5),
+            "what": "this config's distributed output (each rank's owned share) vs all colours of the same "
+                    "partition on rank 0's GPU"}
+
+
+def _ctx1(env, H):
+    """A communicator-free context on this GPU (every colour locally)."""
+    return H.Context(env.dev.index)
+
+
 def _pinned(torch, arr):
     t = torch.from_numpy(np.ascontiguousarray(arr))
     return t.pin_memory()
@@ -230,6 +264,22 @@ def config_c1(env, H, synth):
            "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms, "gpu_launches": nl,
            "roofline": roofline(env, by / env.world, leaf, "k_spmv_rows<4>"),
            "effective_gbs": by / (ms * 1e-3) / 1e9}
+    if env.world > 1:
+        step()
+
+        def ref():
+            c1 = _ctx1(env, H)
+            B1 = H.DeviceTensor.wrap(c1, (n, n), H.parse_format("ds"), [rp_d.data_ptr()], [crd_d.data_ptr()],
+                                     vals_d.data_ptr())
+            y1 = torch.empty_like(y_d)
+            H.partition_universe(c1, B1, P, host=False)
+            H.spmv(c1, B1, x_d, y1, pieces=P, stats=False)
+            torch.cuda.synchronize()
+            B1.close()
+            c1.close()
+            return y1
+
+        out["multi_gpu_check"] = mgpu_check(env, H, y_d, 1, H.last_owned(env.ctx, first, count), ref)
     B.close()
     if env.world == 1:
         rs, nbytes, st = _restager(env, H, (n, n), H.parse_format("ds"), [rp], [crd], vals)
@@ -279,6 +329,22 @@ def config_spmv_rmat(env, H, rm, x_seed):
            "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms, "gpu_launches": nl,
            "roofline": roofline(env, by / env.world, leaf, "k_spmv_rows<6,int> over compacted columns"),
            "effective_gbs": by / (ms * 1e-3) / 1e9}
+    if env.world > 1:
+        step()
+
+        def ref():
+            c1 = _ctx1(env, H)
+            B1 = H.DeviceTensor.wrap(c1, (n, n), H.parse_format("ds"), [rp_d.data_ptr()], [crd_d.data_ptr()],
+                                     vals_d.data_ptr())
+            y1 = torch.empty_like(y_d)
+            H.partition_nonzero(c1, B1, 1, P, host=False)
+            H.spmv(c1, B1, x_d, y1, pieces=P, stats=False)
+            torch.cuda.synchronize()
+            B1.close()
+            c1.close()
+            return y1
+
+        out["multi_gpu_check"] = mgpu_check(env, H, y_d, 1, H.last_owned(env.ctx, first, count), ref)
     if env.world == 1:
         rp, crd, vals = rm["host"]
         rs, nbytes, st = _restager(env, H, (n, n), H.parse_format("ds"), [rp], [crd], vals)
@@ -390,6 +456,24 @@ def config_c3(env, H, rm):
            "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms, "gpu_launches": nl,
            "roofline": roofline(env, by / env.world, leaf, "k_sddmm_nz<4,3>"),
            "effective_gbs": by / (ms * 1e-3) / 1e9, "placement": placement}
+    if env.world > 1:
+        step()
+
+        def ref():
+            c1 = _ctx1(env, H)
+            B1 = H.DeviceTensor.wrap(c1, (n, n), H.parse_format("ds"), [rm["rp_d"].data_ptr()],
+                                     [rm["crd_d"].data_ptr()], rm["vals_d"].data_ptr())
+            Cfull = C_h.to(env.dev)
+            a1 = torch.empty_like(A_d)
+            H.partition_nonzero(c1, B1, 1, P, host=False)
+            H.sddmm(c1, B1, Cfull, D_d, K, 1, K, a1, pieces=P, stats=False)
+            torch.cuda.synchronize()
+            B1.close()
+            c1.close()
+            del Cfull
+            return a1
+
+        out["multi_gpu_check"] = mgpu_check(env, H, A_d, 1, tuple(cols[env.rank].q), ref)
     if env.world == 1:
         rp, crd, vals = rm["host"]
         rs, nbytes, st = _restager(env, H, (n, n), H.parse_format("ds"), [rp], [crd], vals)
@@ -470,15 +554,39 @@ def config_c4(env, H, synth):
 
     res = {}
     bB = 8 * (I + 1) + 8 * F + 8 * (F + 1) + 16 * nnz
+
+    def ref_of(name):
+        def ref():
+            c1 = _ctx1(env, H)
+            B1 = H.DeviceTensor.wrap(c1, (I, J, Kd), fmt, [arrs[0].data_ptr(), arrs[2].data_ptr()],
+                                     [arrs[1].data_ptr(), arrs[3].data_ptr()], arrs[4].data_ptr())
+            H.partition_nonzero(c1, B1, 2, P, host=False)
+            if name == "C4-SpTTV":
+                o = torch.empty_like(Av)
+                H.spttv(c1, B1, c_d, o, pieces=P, stats=False)
+            else:
+                o = torch.empty_like(A_d)
+                H.spmttkrp(c1, B1, C_d, D_d, R, o, pieces=P, stats=False)
+            torch.cuda.synchronize()
+            B1.close()
+            c1.close()
+            return o
+        return ref
+
     for name, step, flops, by, kern in (
             ("C4-SpTTV", step_ttv, 2.0 * nnz, bB + 8 * Kd + 8 * F, "k_spmv_rows<6> over fibres"),
             ("C4-SpMTTKRP", step_mttkrp, 3.0 * nnz * R, bB + 8 * (J + Kd + I) * R, "k_mttkrp32_nz<4,3>")):
         ms, leaf, nl = measure(env, step)
+        check = None
+        if env.world > 1:
+            step()
+            out_d, width = (Av, 1) if name == "C4-SpTTV" else (A_d, R)
+            check = mgpu_check(env, H, out_d, width, H.last_owned(env.ctx, first, count), ref_of(name))
         res[name] = {"workload": f"{name[3:]} on a {I}x{J}x{Kd} power-law dss tensor ({nnz} nnz, {F} fibres), "
                                  f"nonzero split into {P} colour(s)" + (", R=32" if "MTT" in name else ""),
                      "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms, "gpu_launches": nl,
                      "roofline": roofline(env, by / env.world, leaf, kern),
-                     "effective_gbs": by / (ms * 1e-3) / 1e9}
+                     "effective_gbs": by / (ms * 1e-3) / 1e9, "multi_gpu_check": check}
         if "MTT" in name and leaf > 0:
             # both factors (C 2.4 MB, D 7.4 MB) sit in L2: the leaf is bound by
             # L2 -> SM bytes, two 256-byte row reads per position, against the
@@ -569,6 +677,30 @@ def config_c5(env, H, rm):
            "roofline": roofline(env, by / env.world, ms,
                                 "the SpAdd3 step (count, scan, allocate, fill; leaf = whole step)"),
            "effective_gbs": by / (ms * 1e-3) / 1e9}
+    if env.world > 1:
+        # the row blocks gathered on rank 0 (spd_gather_rows) vs every colour on rank 0's GPU
+        whole = A.gather_rows(0)
+        ok = True
+        if env.rank == 0:
+            got = whole.download()
+            whole.close()
+            c1 = _ctx1(env, H)
+            Bs1 = [H.DeviceTensor.wrap(c1, (n, n), H.parse_format("ds"), [d._keep[0].data_ptr()],
+                                       [d._keep[1].data_ptr()], d._keep[2].data_ptr()) for d in devs]
+            H.partition_universe(c1, Bs1[0], P, host=False)
+            A1, _ = H.spadd3(c1, Bs1[0], Bs1[1], Bs1[2], pieces=P, stats=False)
+            want = A1.download()
+            A1.close()
+            for b in Bs1:
+                b.close()
+            c1.close()
+            ok = (np.array_equal(got.levels[1].rowptr(), want.levels[1].rowptr()) and
+                  np.array_equal(got.levels[1].crd, want.levels[1].crd) and np.array_equal(got.vals, want.vals))
+        t = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device=env.dev)
+        env.dist.broadcast(t, 0)
+        out["multi_gpu_check"] = {"bit_exact_vs_one_gpu": bool(t[0] > 0.5),
+                                  "what": "the row blocks gathered on rank 0 (spd_gather_rows) vs every colour "
+                                          "of the same partition on rank 0's GPU: row pointer, crd, vals"}
     A.close()
     live["A"] = None
     if env.world == 1:
