@@ -122,9 +122,16 @@ __global__ void __launch_bounds__(kBlock) k_zero_empty(const int64_t* __restrict
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const uint64_t pol = l2_policy_evict_first();
-  for (int64_t g0 = lo + gw * 32; g0 <= hi; g0 += nw * 32) {
+  // the next group's row pointers are loaded before the current group's
+  // stores, so the dependent row-pointer latency overlaps them
+  int64_t g0 = lo + gw * 32;
+  int64_t ra = 0, rb = 0;
+  if (g0 + lane <= hi) ra = ld64(R + g0 + lane), rb = ld64(R + g0 + lane + 1);
+  for (; g0 <= hi; g0 += nw * 32) {
     const int64_t r = g0 + lane;
-    const bool empty = r <= hi && ld64(R + r + 1) == ld64(R + r);
+    const bool empty = r <= hi && rb == ra;
+    const int64_t gn = g0 + nw * 32;
+    if (gn + lane <= hi) ra = ld64(R + gn + lane), rb = ld64(R + gn + lane + 1);
     if (W == 1) {
       if (empty) out[r] = 0.0;
       continue;
@@ -133,12 +140,22 @@ __global__ void __launch_bounds__(kBlock) k_zero_empty(const int64_t* __restrict
     const int ne = __popc(m);
     if (W == 32) {  // a half-warp per row: one 128-bit store per lane writes two 256-byte rows
       const int half = lane >> 4, hl = lane & 15;
-      for (int t = 0; t < ne; t += 2) {
-        const int k = t + half;
-        if (k < ne) {
-          const int b = (int)__fns(m, 0, k + 1);
-          st_f64x2_hint(out + (g0 + b) * 32 + 2 * hl, make_double2(0.0, 0.0), pol);
-        }
+      double* base = out + g0 * 32 + 2 * hl;
+      if (m == FULL) {  // a fully empty group (the sparse tail): 8 KB of contiguous zeros
+#pragma unroll
+        for (int t = 0; t < 32; t += 2) st_f64x2_hint(base + (t + half) * 32, make_double2(0.0, 0.0), pol);
+        continue;
+      }
+      // otherwise the empty rows two at a time, lowest first (warp-uniform;
+      // the k-th-set-bit search it replaces dominated the kernel's issue)
+      unsigned left = m;
+      while (left) {
+        const int b0 = __ffs(left) - 1;
+        left &= left - 1u;
+        const int b1 = left ? __ffs(left) - 1 : -1;
+        if (left) left &= left - 1u;
+        const int b = half ? b1 : b0;
+        if (b >= 0) st_f64x2_hint(base + b * 32, make_double2(0.0, 0.0), pol);
       }
       continue;
     }
