@@ -279,6 +279,21 @@ int spd_deppart_preimage(spd_context* ctx, const int64_t* ranges, int64_t n, int
 int spd_deppart_by_bounds(spd_context* ctx, int rank, const int64_t* extents, int64_t pieces,
                           const int64_t* bounds, int64_t* out_off, int64_t* out_idx, int64_t cap,
                           int64_t* total, int* disjoint);
+/* Host-memory variants of image / preimage (same arguments and semantics,
+ * every array in host memory) for host callers such as the reference's own
+ * planner (integration/deppart_gpu.cpp): the inputs are staged once, the
+ * operator runs on the GPU, out_off / out_idx are written in host memory
+ * (out_idx when cap >= *total). */
+int spd_deppart_image_host(spd_context* ctx, const int64_t* ranges, int64_t n, int64_t dest_extent,
+                           int64_t pieces, const int64_t* off, const int64_t* idx, int64_t* out_off,
+                           int64_t* out_idx, int64_t cap, int64_t* total, int* disjoint);
+int spd_deppart_preimage_host(spd_context* ctx, const int64_t* ranges, int64_t n, int64_t dest_extent,
+                              int64_t pieces, const int64_t* dest_off, const int64_t* dest_idx,
+                              int64_t* out_off, int64_t* out_idx, int64_t cap, int64_t* total,
+                              int* disjoint);
+int spd_deppart_by_bounds_host(spd_context* ctx, int rank, const int64_t* extents, int64_t pieces,
+                               const int64_t* bounds, int64_t* out_off, int64_t* out_idx, int64_t cap,
+                               int64_t* total, int* disjoint);
 /* Test support (K2m): materialise colour `color`'s subset of a bundle region
  * exactly as the reference's Partition holds it (sorted unique indices).
  *   which: 0 dom, 1 pos, 2 crd of `level`; 3 vals.

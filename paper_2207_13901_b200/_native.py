@@ -57,6 +57,10 @@ SIGNATURES = {
     ),
     "spd_deppart_image": (C.c_int, [vp, vp, i64, i64, i64, vp, vp, vp, vp, i64, i64p, C.POINTER(C.c_int)]),
     "spd_deppart_preimage": (C.c_int, [vp, vp, i64, i64, i64, vp, vp, vp, vp, i64, i64p, C.POINTER(C.c_int)]),
+    "spd_deppart_image_host": (C.c_int, [vp, vp, i64, i64, i64, vp, vp, vp, vp, i64, i64p, C.POINTER(C.c_int)]),
+    "spd_deppart_preimage_host": (C.c_int, [vp, vp, i64, i64, i64, vp, vp, vp, vp, i64, i64p, C.POINTER(C.c_int)]),
+    "spd_deppart_by_bounds_host": (C.c_int, [vp, C.c_int, i64p, i64, i64p, i64p, i64p, i64, i64p,
+                                              C.POINTER(C.c_int)]),
     "spd_deppart_by_bounds": (C.c_int, [vp, C.c_int, i64p, i64, i64p, vp, vp, i64, i64p, C.POINTER(C.c_int)]),
     "spd_tensor_restage": (C.c_int, [vp, vp, C.POINTER(i64p), C.POINTER(i64p), dblp]),
     "spd_ledger_bytes": (C.c_int, [vp, vp, C.c_int, C.c_int, i64, i64p]),

@@ -475,3 +475,104 @@ extern "C" int spd_deppart_by_bounds(spd_context* ctx, int rank, const int64_t* 
                                      int64_t* total, int* disjoint) {
   return guarded([&] { run_by_bounds(ctx, rank, extents, pieces, bounds, out_off, out_idx, cap, total, disjoint); });
 }
+
+// Host-memory variants for host callers (the reference's own planner through
+// integration/deppart_gpu.cpp): inputs are staged to the device once, the
+// operator runs twice (size, then fill) on the device, the result comes
+// back into the caller's arrays.  cap < total: only out_off and *total.
+namespace {
+template <class Run>
+void host_call(spd_context* ctx, int64_t n_ranges, const int64_t* ranges, int64_t P, const int64_t* off,
+               const int64_t* idx, int64_t* out_off, int64_t* out_idx, int64_t cap, int64_t* total, int* disjoint,
+               Run run) {
+  checked(ctx);
+  if (P < 0 || n_ranges < 0) throw ValidationError("deppart: negative size");
+  if (!out_off || !total || (P > 0 && !off) || (n_ranges > 0 && !ranges)) throw ValidationError("deppart: null argument");
+  activate(ctx);
+  cudaStream_t s = ctx->stream;
+  const int64_t m = P > 0 ? off[P] : 0;
+  if (m > 0 && !idx) throw ValidationError("deppart: null argument");
+  int64_t* d_r = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * std::max<int64_t>(2 * n_ranges, 1));
+  int64_t* d_off = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (P + 1));
+  int64_t* d_idx = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * std::max<int64_t>(m, 1));
+  int64_t* d_out_off = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (P + 1));
+  int64_t* d_out_idx = nullptr;
+  auto release = [&] {
+    for (void* q : {(void*)d_r, (void*)d_off, (void*)d_idx, (void*)d_out_off, (void*)d_out_idx}) dev_free(ctx, q);
+  };
+  try {
+    if (n_ranges > 0) SPD_CUDA(cudaMemcpyAsync(d_r, ranges, sizeof(int64_t) * 2 * n_ranges, cudaMemcpyHostToDevice, s));
+    if (P >= 0) SPD_CUDA(cudaMemcpyAsync(d_off, off, sizeof(int64_t) * (P + 1), cudaMemcpyHostToDevice, s));
+    if (m > 0) SPD_CUDA(cudaMemcpyAsync(d_idx, idx, sizeof(int64_t) * m, cudaMemcpyHostToDevice, s));
+    int64_t t = 0;
+    run(d_r, d_off, d_idx, d_out_off, (int64_t*)nullptr, (int64_t)0, &t, (int*)nullptr);
+    *total = t;
+    if (out_idx && cap >= t) {
+      d_out_idx = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * std::max<int64_t>(t, 1));
+      run(d_r, d_off, d_idx, d_out_off, d_out_idx, t, &t, disjoint);
+      if (t > 0) SPD_CUDA(cudaMemcpyAsync(out_idx, d_out_idx, sizeof(int64_t) * t, cudaMemcpyDeviceToHost, s));
+    } else if (disjoint) {
+      *disjoint = -1;
+    }
+    SPD_CUDA(cudaMemcpyAsync(out_off, d_out_off, sizeof(int64_t) * (P + 1), cudaMemcpyDeviceToHost, s));
+    SPD_CUDA(cudaStreamSynchronize(s));
+  } catch (...) {
+    release();
+    throw;
+  }
+  release();
+}
+}  // namespace
+
+extern "C" int spd_deppart_image_host(spd_context* ctx, const int64_t* ranges, int64_t n, int64_t dest_extent,
+                                      int64_t pieces, const int64_t* off, const int64_t* idx, int64_t* out_off,
+                                      int64_t* out_idx, int64_t cap, int64_t* total, int* disjoint) {
+  return guarded([&] {
+    host_call(ctx, n, ranges, pieces, off, idx, out_off, out_idx, cap, total, disjoint,
+              [&](const int64_t* r, const int64_t* o, const int64_t* x, int64_t* oo, int64_t* oi, int64_t c,
+                  int64_t* t, int* d) { run_image(ctx, r, n, dest_extent, pieces, o, x, oo, oi, c, t, d); });
+  });
+}
+
+extern "C" int spd_deppart_preimage_host(spd_context* ctx, const int64_t* ranges, int64_t n, int64_t dest_extent,
+                                         int64_t pieces, const int64_t* off, const int64_t* idx, int64_t* out_off,
+                                         int64_t* out_idx, int64_t cap, int64_t* total, int* disjoint) {
+  return guarded([&] {
+    host_call(ctx, n, ranges, pieces, off, idx, out_off, out_idx, cap, total, disjoint,
+              [&](const int64_t* r, const int64_t* o, const int64_t* x, int64_t* oo, int64_t* oi, int64_t c,
+                  int64_t* t, int* d) { run_preimage(ctx, r, n, dest_extent, pieces, o, x, oo, oi, c, t, d); });
+  });
+}
+
+extern "C" int spd_deppart_by_bounds_host(spd_context* ctx, int rank, const int64_t* extents, int64_t pieces,
+                                          const int64_t* bounds, int64_t* out_off, int64_t* out_idx, int64_t cap,
+                                          int64_t* total, int* disjoint) {
+  return guarded([&] {
+    checked(ctx);
+    if (pieces < 0 || !out_off || !total) throw ValidationError("partition_by_bounds: bad arguments");
+    activate(ctx);
+    cudaStream_t s = ctx->stream;
+    int64_t* d_off = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * (pieces + 1));
+    int64_t* d_idx = nullptr;
+    try {
+      int64_t t = 0;
+      run_by_bounds(ctx, rank, extents, pieces, bounds, d_off, nullptr, 0, &t, nullptr);
+      *total = t;
+      if (out_idx && cap >= t) {
+        d_idx = (int64_t*)dev_alloc(ctx, sizeof(int64_t) * std::max<int64_t>(t, 1));
+        run_by_bounds(ctx, rank, extents, pieces, bounds, d_off, d_idx, t, &t, disjoint);
+        if (t > 0) SPD_CUDA(cudaMemcpyAsync(out_idx, d_idx, sizeof(int64_t) * t, cudaMemcpyDeviceToHost, s));
+      } else if (disjoint) {
+        *disjoint = -1;
+      }
+      SPD_CUDA(cudaMemcpyAsync(out_off, d_off, sizeof(int64_t) * (pieces + 1), cudaMemcpyDeviceToHost, s));
+      SPD_CUDA(cudaStreamSynchronize(s));
+    } catch (...) {
+      dev_free(ctx, d_off);
+      dev_free(ctx, d_idx);
+      throw;
+    }
+    dev_free(ctx, d_off);
+    dev_free(ctx, d_idx);
+  });
+}

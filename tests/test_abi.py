@@ -71,3 +71,17 @@ def test_product_never_touches_the_oracle():
 def test_synth_library_loads():
     s = N.synth()
     assert s.syn_max_threads() >= 1
+
+
+def test_gpu_dependent_partitioning_fails_loudly_without_a_gpu():
+    """The reference's planner linked with the GPU deppart has no CPU
+    fallback: without a device every partitioning call raises."""
+    import subprocess
+
+    import torch
+
+    exe = os.path.join(ROOT, "oracle", "_ref", "dspar_ref_tests_gpudeppart")
+    if torch.cuda.is_available() or not os.path.exists(exe):
+        pytest.skip("needs the GPU-deppart suite on a machine without a GPU")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert "deppart on gpu: no CUDA device available" in r.stderr

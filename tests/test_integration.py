@@ -280,3 +280,45 @@ def test_bucket_split_equals_the_reference_bundle(gpu_lib, kernel, pieces):
         dev.close()
     finally:
         ctx.close()
+
+
+def test_reference_suite_with_gpu_dependent_partitioning(gpu_lib):
+    """The reference's own doctest suite (64 cases, 1886 checks) linked with
+    integration/deppart_gpu.cpp in place of deppart.cpp: image, preimage,
+    partition_by_bounds and copy_partition on the GPU under the reference's
+    planner, LevelPartitioner and tests -- the same single known failure as
+    the CPU build (test_planner.cpp:233, a validation gap of planner.cpp:84)."""
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(ob.REF_TESTS), "dspar_ref_tests_gpudeppart")
+    if not os.path.exists(exe):
+        pytest.skip("GPU-deppart reference suite not built (make -C oracle integration)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    out = r.stdout + r.stderr
+    # the three render-golden cases read /root/reference/proj/tests/golden,
+    # which only exists where the reference is mounted (not on a GPU box):
+    # there they report "golden file created"; the rendered plans are
+    # compared library against library in test_rendered_plans_equal_with_gpu_deppart
+    missing = out.count("golden file created")
+    assert f"test cases: 64 | failed: {1 + missing}" in out, out[-3000:]
+    assert "test_planner.cpp:233" in r.stderr and r.stderr.count("CHECK FAILED") == 1 + missing
+
+
+@pytest.mark.parametrize("schedule,pieces", [("row", 2), ("row", 1), ("nonzero", 2), ("nonzero", 4)])
+def test_rendered_plans_equal_with_gpu_deppart(gpu_lib, schedule, pieces):
+    """render_plan of the reference's planner with the GPU dependent
+    partitioning equals the CPU build's, colour bounds and every bundle subset
+    included (the golden-file cases of test_planner.cpp:302-315, library
+    against library)."""
+    spec = KERNELS["spmv"]
+    sched = ROW if schedule == "row" else spec["nonzero"]
+    rng = np.random.default_rng(pieces)
+    t = K.instance("spmv", rng, integers=True, max_dim=30)
+    args = (spec["expr"], sched, pieces, "d", ref_inputs("spmv", t))
+    cpu = ob.RefRun(*args, execute=False).ok()
+    gpu = ob.RefRun(*args, execute=False, lib=gpu_lib).ok()
+    assert cpu.L.ref_rendered_plan(cpu.h) == gpu.L.ref_rendered_plan(gpu.h)
+    for c in range(pieces):
+        for lvl, region in ((0, "dom"), (1, "pos"), (1, "crd")):
+            a, b = cpu.subset("B", lvl, region, c), gpu.subset("B", lvl, region, c)
+            assert (a is None and b is None) or np.array_equal(a, b)
