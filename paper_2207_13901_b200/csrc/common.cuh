@@ -298,6 +298,25 @@ __device__ __forceinline__ int64_t warp_owner(const int64_t* __restrict__ rowptr
   return warp_upper_bound(rowptr, npos + 1, q) - 1;
 }
 
+// warp_owner over fewer than 2^31 rows, in 32-bit index arithmetic (keeps the
+// register-tight leaves free of spills).
+__device__ __forceinline__ int warp_owner32(const int64_t* __restrict__ rowptr, int npos, int64_t q) {
+  const int lane = lane_id();
+  int lo = 0, hi = npos + 1;  // answer in [lo, hi]
+  while (hi - lo > 32) {
+    const int step = (hi - lo + 31) / 32;
+    const int idx = lo + lane * step;
+    const unsigned m = __ballot_sync(0xffffffffu, idx < hi && __ldg(rowptr + idx) <= q);
+    const int cnt = __popc(m);
+    if (cnt == 0) return lo - 1;
+    const int nhi = lo + cnt * step;
+    lo = lo + (cnt - 1) * step + 1;
+    hi = nhi < hi ? nhi : hi;
+  }
+  const int idx = lo + lane;
+  return lo + __popc(__ballot_sync(0xffffffffu, idx < hi && __ldg(rowptr + idx) <= q)) - 1;
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

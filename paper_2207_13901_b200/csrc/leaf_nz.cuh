@@ -167,135 +167,6 @@ __global__ void __launch_bounds__(kBlock) k_zero_empty(const int64_t* __restrict
   }
 }
 
-// ---------------------------------------------------------------------------
-// SpMV / SpTTV over the compacted view: lane = position, 32-position windows
-// (kSpmvBatch of them loaded together), per window one segmented scan; the
-// rows completing in a window are handled one per lane: lane t finds the end
-// of row ic+t with __fns on the head mask.
-__global__ void __launch_bounds__(kBlock, 5) k_spmv_nz(WalkGeom g, NzView z, const int64_t* __restrict__ crd,
-                                                    const double* __restrict__ vals,
-                                                    const double* __restrict__ x, double* __restrict__ y,
-                                                    ChunkRecs rec, const int64_t* __restrict__ counters) {
-  const int lane = lane_id();
-  z.m = nz_count(z);
-  const int64_t begin = counters[1], end = counters[2];
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t pol_stream = l2_policy_evict_first();
-  for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
-    const ChunkInfo ci = chunk_info(g, v, begin);
-    if (ci.q_lo > ci.q_hi) {
-      zero_gap(y, 1, ci.w_lo, ci.w_hi);
-      if (lane == 0) rec.row[2 * ci.local] = -1, rec.row[2 * ci.local + 1] = -1, rec.cont[ci.local] = 0;
-      continue;
-    }
-    const int64_t k = ci.local, s = ci.s, e = ci.e;
-    NzCursor c;
-    nz_start(z, c, s);
-    bool head = __shfl_sync(FULL, c.P0, 0) < s;
-    int64_t head_row = -1;
-    int head_cont = 0;
-    double head_val = 0.0, acc = 0.0;
-    if (s == ci.q_lo && !head) zero_gap(y, 1, ci.w_lo, __shfl_sync(FULL, c.I0, 0) - 1);
-    for (int64_t bbase = s; bbase <= e; bbase += 32 * kSpmvBatch) {
-      int64_t kk[kSpmvBatch];
-      double vv[kSpmvBatch], prods[kSpmvBatch];
-#pragma unroll
-      for (int bi = 0; bi < kSpmvBatch; bi++) {
-        const int64_t q = bbase + 32 * bi + lane;
-        kk[bi] = 0;
-        vv[bi] = 0.0;
-        if (q <= e) {
-          kk[bi] = ld_i64_hint(crd + q, pol_stream);
-          vv[bi] = ld_f64_hint(vals + q, pol_stream);
-        }
-      }
-#pragma unroll
-      for (int bi = 0; bi < kSpmvBatch; bi++) {
-        const int64_t q = bbase + 32 * bi + lane;
-        prods[bi] = q <= e ? vv[bi] * __ldg(x + kk[bi]) : 0.0;
-      }
-#pragma unroll
-      for (int bi = 0; bi < kSpmvBatch; bi++) {
-        const int64_t base = bbase + 32 * bi;
-        if (base > e) break;
-        const int64_t last = min(base + 31, e);
-        const int cnt = (int)(last - base + 1);
-        const unsigned heads = nz_window_mask(c, base, last);
-        if (heads == 0u) {
-          acc += warp_sum(prods[bi]);
-          continue;
-        }
-        // segmented inclusive scan: lane l adds the partial of lane l-off
-        // unless a row starts in (l-off, l] -- read off the window mask
-        double sv = prods[bi];
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const double tv = __shfl_up_sync(FULL, sv, off);
-          const unsigned span = lane >= off ? ((((1u << off) - 1u) << (lane - off + 1))) : 0u;
-          if (lane >= off && (heads & span) == 0u) sv += tv;
-        }
-        const int nh = __popc(heads);
-        // lane t < nh: row ic + t ends just before the t-th head
-        const int endl = lane < nh ? (int)__fns(heads, 0, lane + 1) - 1 : -1;
-        double sum = __shfl_sync(FULL, sv, endl < 0 ? 0 : endl);
-        if (endl < 0) sum = 0.0;
-        if (lane == 0) sum += acc;
-        const int64_t id = nz_get(c.I0, c.I1, (int)(c.ic - c.cb) + lane);
-        const int64_t id_next = nz_get(c.I0, c.I1, (int)(c.ic - c.cb) + lane + 1);
-        if (lane < nh)  // empty rows between row ic+t and its successor
-          for (int64_t r = id + 1; r < id_next; r++) y[r] = 0.0;
-        if (lane < nh) {
-          if (lane == 0 && head) {
-            head_row = id;
-            head_val = sum;
-            head_cont = 0;
-          } else {
-            y[id] = sum;
-          }
-        }
-        head_row = __shfl_sync(FULL, head_row, 0);
-        head_val = __shfl_sync(FULL, head_val, 0);
-        head = false;
-        acc = __shfl_sync(FULL, sv, cnt - 1);
-        nz_advance(z, c, nh);
-      }
-    }
-    // chunk end: the current row ends exactly at e, or continues past it
-    const int64_t next = nz_get(c.P0, c.P1, (int)(c.ic - c.cb) + 1);
-    const int64_t id = nz_get(c.I0, c.I1, (int)(c.ic - c.cb));
-    int64_t tail_row = -1;
-    double tail_val = 0.0;
-    if (next == e + 1) {
-      if (head) head_row = id, head_val = acc, head_cont = 0;
-      else if (lane == 0) y[id] = acc;
-      const int64_t nid = nz_get(c.I0, c.I1, (int)(c.ic - c.cb) + 1);
-      zero_gap(y, 1, id + 1, nid < 0 ? ci.w_hi : min(nid - 1, ci.w_hi));
-    } else if (head) {
-      head_row = id, head_val = acc, head_cont = 1;
-    } else {
-      tail_row = id, tail_val = acc;
-    }
-    if (lane == 0) {
-      rec.row[2 * k] = head_row;
-      rec.row[2 * k + 1] = tail_row;
-      rec.cont[k] = head_cont;
-      rec.val[2 * k] = head_val;
-      rec.val[2 * k + 1] = tail_val;
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
-// SpMV / SpTTV for short rows (uniform matrices, CSF fibres): lane = one
-// compacted row of the chunk, summed serially in stored-position order (the
-// reference's own order, sim.cpp:326-354) with 4 independent gathers in
-// flight; rows longer than kRowsLong are summed by the whole warp instead
-// (coalesced loads, lane-strided partials + butterfly).  Per 32 positions
-// this issues ~20 warp instructions where the window scan of k_spmv_nz
-// issues ~300 when rows are ~10 long.  Chunk / colour records as k_spmv_nz.
-constexpr int kRowsLong = 48;
-
 __device__ __forceinline__ int64_t ld_crd_hint(const int64_t* p, uint64_t pol) { return ld_i64_hint(p, pol); }
 __device__ __forceinline__ int64_t ld_crd_hint(const int32_t* p, uint64_t pol) { return ld_i32_hint(p, pol); }
 
@@ -320,40 +191,33 @@ __global__ void k_gather_ref(const double* __restrict__ x, const int32_t* __rest
     xc[r] = __ldg(x + cref[r]);
 }
 
-template <typename CI>
-__device__ __forceinline__ double row_dot_serial(const CI* __restrict__ crd, const double* __restrict__ vals,
-                                                 const double* __restrict__ x, int64_t a, int64_t b) {
-  // L1-allocating loads: a lane walks consecutive positions of its row, so
-  // the 32-byte sectors it touches are reused from L1 by its next loads
-  double sum = 0.0;
-  int64_t q = a;
-  for (; q + 3 <= b; q += 4) {
-    const int64_t k0 = __ldg(crd + q), k1 = __ldg(crd + q + 1), k2 = __ldg(crd + q + 2), k3 = __ldg(crd + q + 3);
-    const double v0 = __ldg(vals + q), v1 = __ldg(vals + q + 1), v2 = __ldg(vals + q + 2), v3 = __ldg(vals + q + 3);
-    const double x0 = __ldg(x + k0), x1 = __ldg(x + k1), x2 = __ldg(x + k2), x3 = __ldg(x + k3);
-    sum += v0 * x0;
-    sum += v1 * x1;
-    sum += v2 * x2;
-    sum += v3 * x3;
-  }
-  if (q <= b) {  // up to 3 more, loads issued together
-    const int64_t k0 = __ldg(crd + q), k1 = q + 1 <= b ? __ldg(crd + q + 1) : 0, k2 = q + 2 <= b ? __ldg(crd + q + 2) : 0;
-    const double v0 = __ldg(vals + q), v1 = q + 1 <= b ? __ldg(vals + q + 1) : 0.0;
-    const double v2 = q + 2 <= b ? __ldg(vals + q + 2) : 0.0;
-    const double x0 = __ldg(x + k0), x1 = q + 1 <= b ? __ldg(x + k1) : 0.0, x2 = q + 2 <= b ? __ldg(x + k2) : 0.0;
-    sum += v0 * x0;
-    if (q + 1 <= b) sum += v1 * x1;
-    if (q + 2 <= b) sum += v2 * x2;
-  }
-  return sum;
-}
+// ---------------------------------------------------------------------------
+// SpMV / SpTTV, windowed: a warp streams its chunk in windows of kWin
+// positions.  Per window every lane loads kWin/32 positions lane-consecutive
+// (coalesced crd and vals, kWin/32 independent x gathers in flight per lane),
+// and the products go to the warp's shared-memory window.  The rows touching
+// the window are then reduced one per lane, serially in stored-position order
+// (sim.cpp:326-354) from shared memory; a row segment of kSegLong or more
+// positions is summed by the whole warp instead (lane-strided partials and a
+// butterfly).  A row continuing past the window carries its partial into the
+// next one, and a window lying inside one row that continues past it is summed
+// in registers (hub rows).  Versus a lane walking its own row in global memory
+// (the round-1 k_spmv_rows: 92 B of spills at 6 CTAs/SM), the stream loads
+// touch one or two lines per instruction instead of up to 32; measured
+// (profiles/README.md) C1 0.085 -> 0.073 ms, SpTTV 0.125 -> 0.121 ms, R-MAT
+// SpMV 0.960 -> 0.940 ms, and faster than the round-1 window scan (k_spmv_nz)
+// on long rows too, so it is the one SpMV / SpTTV leaf.
+constexpr int kWin = 256;
+constexpr int kSegLong = 64;
 
-template <int MINB, typename CI = int64_t>
-__global__ void __launch_bounds__(kBlock, MINB) k_spmv_rows(WalkGeom g, NzView z, const CI* __restrict__ crd,
-                                                      const double* __restrict__ vals,
-                                                      const double* __restrict__ x, double* __restrict__ y,
-                                                      ChunkRecs rec, const int64_t* __restrict__ counters) {
+template <int MINB, typename CI>
+__global__ void __launch_bounds__(kBlock, MINB) k_spmv_win(WalkGeom g, NzView z, const CI* __restrict__ crd,
+                                                     const double* __restrict__ vals,
+                                                     const double* __restrict__ x, double* __restrict__ y,
+                                                     ChunkRecs rec, const int64_t* __restrict__ counters) {
+  __shared__ double win_s[kBlock / 32][kWin];
   const int lane = lane_id();
+  double* buf = win_s[threadIdx.x >> 5];
   z.m = nz_count(z);
   const int64_t begin = counters[1], end = counters[2];
   const uint64_t pol = l2_policy_evict_first();
@@ -365,80 +229,134 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmv_rows(WalkGeom g, NzView z
       continue;
     }
     const int64_t k = ci.local, s = ci.s, e = ci.e;
-    const int64_t ic0 = warp_owner(z.ptr, z.m, s);  // the last row is found by the walk itself
-    const bool head = ld64(z.ptr + ic0) < s;
-    int64_t ic1 = z.m - 1;
-    if (s == ci.q_lo && !head) zero_gap(y, 1, ci.w_lo, ld64(z.id + ic0) - 1);
-    int64_t head_row = -1, tail_row = -1;
+    int64_t r = warp_owner(z.ptr, z.m, s);  // compacted row holding the window's first position
+    bool at_head = ld64(z.ptr + r) < s;     // r began before the chunk: its partial is the head record
+    if (s == ci.q_lo && !at_head) zero_gap(y, 1, ci.w_lo, ld64(z.id + r) - 1);
+    int64_t head_row = -1;
     int head_cont = 0;
-    double head_val = 0.0, tail_val = 0.0;
-    for (int64_t g0 = ic0; g0 <= ic1; g0 += 32) {
-      const int64_t r = g0 + lane;
-      const int64_t pa = r < z.m ? ld64(z.ptr + r) : INT64_MAX;
-      // rows of this group that start inside the chunk (or the head row)
-      const unsigned in = __ballot_sync(FULL, r == ic0 || pa <= e);
-      if (in != FULL) ic1 = g0 + 31 - __clz(in);  // the chunk's last row is in this group
-      const bool act = r <= ic1;
-      int64_t a = 0, b = -1, id = -1, nid = -1, rend = -1;
-      if (act) {
-        rend = ld64(z.ptr + r + 1) - 1;
-        a = max(pa, s);
-        b = min(rend, e);
-        id = ld64(z.id + r);
-        nid = r + 1 < z.m ? ld64(z.id + r + 1) : -1;
-      }
-      const bool lng = act && b - a + 1 > kRowsLong;
-      double sum = 0.0;
-      if (act && !lng) sum = row_dot_serial(crd, vals, x, a, b);
-      unsigned long_mask = __ballot_sync(FULL, lng);
-      while (long_mask) {
-        const int t = __ffs(long_mask) - 1;
-        long_mask &= long_mask - 1;
-        const int64_t aa = __shfl_sync(FULL, a, t), bb = __shfl_sync(FULL, b, t);
+    double head_val = 0.0, carry = 0.0;
+    int64_t rend = ld64(z.ptr + r + 1) - 1;  // last position of row r
+    for (int64_t wb = s; wb <= e; wb += kWin) {
+      const int64_t we = min(wb + kWin - 1, e);
+      if (rend > we) {  // the window lies inside row r, which continues: no row ends here
         double part = 0.0;
-        for (int64_t q = aa + lane; q <= bb; q += 32)
-          part += ld_f64_hint(vals + q, pol) * __ldg(x + ld_crd_hint(crd + q, pol));
-        part = warp_sum(part);
-        if (lane == t) sum = part;
+#pragma unroll
+        for (int h = 0; h < kWin / 32; h += 4) {
+          CI kk[4];
+          double vv[4];
+#pragma unroll
+          for (int i = 0; i < 4; i++) {
+            const int64_t q = wb + 32 * (h + i) + lane;
+            kk[i] = 0;
+            vv[i] = 0.0;
+            if (q <= we) kk[i] = ld_crd_hint(crd + q, pol), vv[i] = ld_f64_hint(vals + q, pol);
+          }
+#pragma unroll
+          for (int i = 0; i < 4; i++)
+            if (wb + 32 * (h + i) + lane <= we) part += vv[i] * __ldg(x + kk[i]);
+        }
+        carry += warp_sum(part);
+        continue;
       }
-      if (act) {
-        const bool is_head = r == ic0 && head;
-        const bool ends_here = rend <= e;
-        if (is_head) {
-          head_row = id;
-          head_val = sum;
-          head_cont = ends_here ? 0 : 1;
-        } else if (!ends_here) {
-          tail_row = id;
-          tail_val = sum;
-        } else {
-          y[id] = sum;
+#pragma unroll
+      for (int h = 0; h < kWin / 32; h += 4) {
+        CI kk[4];
+        double vv[4];
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const int64_t q = wb + 32 * (h + i) + lane;
+          kk[i] = 0;
+          vv[i] = 0.0;
+          if (q <= we) kk[i] = ld_crd_hint(crd + q, pol), vv[i] = ld_f64_hint(vals + q, pol);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) {
+          const int64_t q = wb + 32 * (h + i) + lane;
+          buf[32 * (h + i) + lane] = q <= we ? vv[i] * __ldg(x + kk[i]) : 0.0;
         }
       }
-      // empty rows up to the next non-empty one (bounded by W_c at a chunk
-      // end): short gaps by their lane, long ones by the whole warp
-      int64_t glo = 1, ghi = 0;
-      if (act && rend <= e) {
-        glo = id + 1;
-        ghi = rend == e ? (nid < 0 ? ci.w_hi : min(nid - 1, ci.w_hi)) : nid - 1;
+      __syncwarp();
+      for (;;) {  // the rows touching [wb, we], 32 at a time
+        const int64_t rr = r + lane;
+        const int64_t pa = rr < z.m ? ld64(z.ptr + rr) : INT64_MAX;
+        const bool act = pa <= we;  // lane 0's row holds wb
+        const int64_t pe = act ? ld64(z.ptr + rr + 1) - 1 : -1;
+        const int a = act ? (int)(max(pa, wb) - wb) : 0;
+        const int b = act ? (int)(min(pe, we) - wb) : -1;
+        double sum = lane == 0 ? carry : 0.0;
+        const bool lng = b - a + 1 >= kSegLong;
+        if (!lng)
+          for (int q = a; q <= b; q++) sum += buf[q];
+        unsigned long_mask = __ballot_sync(FULL, lng);
+        while (long_mask) {
+          const int t = __ffs(long_mask) - 1;
+          long_mask &= long_mask - 1;
+          const int aa = __shfl_sync(FULL, a, t), bb = __shfl_sync(FULL, b, t);
+          double part = 0.0;
+          for (int q = aa + lane; q <= bb; q += 32) part += buf[q];
+          part = warp_sum(part);
+          if (lane == t) sum += part;
+        }
+        // a row ending here is stored (or is the head record); the empty rows
+        // up to the next non-empty one are zeroed, bounded by W_c at the chunk end
+        int64_t glo = 1, ghi = 0;
+        if (act && pe <= we) {
+          const int64_t id = ld64(z.id + rr);
+          const int64_t nid = rr + 1 < z.m ? ld64(z.id + rr + 1) : -1;
+          if (lane == 0 && at_head) {
+            head_row = id;
+            head_val = sum;
+            head_cont = 0;
+          } else {
+            y[id] = sum;
+          }
+          glo = id + 1;
+          ghi = pe == e ? (nid < 0 ? ci.w_hi : min(nid - 1, ci.w_hi)) : nid - 1;
+        }
+        const bool long_gap = ghi - glo + 1 > 64;
+        if (!long_gap)
+          for (int64_t q = glo; q <= ghi; q++) y[q] = 0.0;
+        unsigned gaps = __ballot_sync(FULL, long_gap);
+        while (gaps) {
+          const int t = __ffs(gaps) - 1;
+          gaps &= gaps - 1;
+          zero_gap(y, 1, __shfl_sync(FULL, glo, t), __shfl_sync(FULL, ghi, t));
+        }
+        const unsigned am = __ballot_sync(FULL, act);
+        const int nact = __popc(am);
+        const int64_t pe_last = __shfl_sync(FULL, pe, nact - 1);
+        if (nact == 32 && pe_last < we) {  // more rows start in this window
+          r += 32;
+          carry = 0.0;
+          at_head = false;
+          continue;
+        }
+        if (pe_last <= we) {  // the window ends exactly at a row end
+          r += nact;
+          carry = 0.0;
+          at_head = false;
+          rend = r < z.m ? ld64(z.ptr + r + 1) - 1 : INT64_MAX;
+        } else {  // the last row continues: carry its partial
+          r += nact - 1;
+          carry = __shfl_sync(FULL, sum, nact - 1);
+          at_head = at_head && nact == 1;
+          rend = pe_last;
+        }
+        break;
       }
-      const bool long_gap = ghi - glo + 1 > 64;
-      if (!long_gap)
-        for (int64_t rr = glo; rr <= ghi; rr++) y[rr] = 0.0;
-      unsigned gaps = __ballot_sync(FULL, long_gap);
-      while (gaps) {
-        const int t = __ffs(gaps) - 1;
-        gaps &= gaps - 1;
-        zero_gap(y, 1, __shfl_sync(FULL, glo, t), __shfl_sync(FULL, ghi, t));
-      }
+      __syncwarp();
     }
-    // records of the chunk's first (head) and last (tail) rows
-    head_row = __shfl_sync(FULL, head_row, 0);  // the head row is lane 0 of the first group
+    // chunk end: a row still open continues past e
+    int64_t tail_row = -1;
+    double tail_val = 0.0;
+    if (r < z.m && ld64(z.ptr + r) <= e) {
+      const int64_t id = ld64(z.id + r);
+      if (at_head) head_row = id, head_val = carry, head_cont = 1;
+      else tail_row = id, tail_val = carry;
+    }
+    head_row = __shfl_sync(FULL, head_row, 0);
     head_val = __shfl_sync(FULL, head_val, 0);
     head_cont = __shfl_sync(FULL, head_cont, 0);
-    const int tl = (int)((ic1 - ic0) & 31);  // the tail row is lane (ic1 - ic0) % 32 of the last group
-    tail_row = __shfl_sync(FULL, tail_row, tl);
-    tail_val = __shfl_sync(FULL, tail_val, tl);
     if (lane == 0) {
       rec.row[2 * k] = head_row;
       rec.row[2 * k + 1] = tail_row;
@@ -520,7 +438,8 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
   const int64_t begin = counters[1], end = counters[2];
   const double* Cl = C + 2 * hl;
   const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
-  for (int64_t t = chunk_ticket(counters); t < end - begin; t = chunk_ticket(counters)) {
+  const int nchunks = (int)(end - begin);  // < 2^31 (positions < 2^31 here), one register
+  for (int t = (int)chunk_ticket(counters); t < nchunks; t = (int)chunk_ticket(counters)) {
     const ChunkInfo ci = chunk_info(g, begin + t, begin);
     if (ci.q_lo > ci.q_hi) {
       if (lane == 0) rec.row[2 * ci.local] = -1, rec.row[2 * ci.local + 1] = -1, rec.cont[ci.local] = 0;
@@ -532,7 +451,7 @@ __global__ void __launch_bounds__(kBlock, MINB) k_spmm32_nz(WalkGeom g, NzView z
     const int32_t* cp = crd32 + s;
     const double* vp = vals + s;
     NzCur32 c;
-    c.cb = warp_owner(z.ptr, z.m, s);
+    c.cb = warp_owner32(z.ptr, (int)z.m, s);
     c.off = 0;
     nz32_load(z, c.cb, s, c.P0, c.I0);
     nz32_load(z, c.cb + 32, s, c.P1, c.I1);
@@ -1091,8 +1010,9 @@ __global__ void __launch_bounds__(kBlock, MINB) k_sddmm_nz(WalkGeom g, NzView z,
   const uint64_t pol_stream = l2_policy_evict_first();
   const uint64_t pol_keep = l2_policy_evict_last();
   const int b4 = (lane >> 4) & 1, b3 = (lane >> 3) & 1;
-  for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
-    const ChunkInfo ci = chunk_info(g, v, begin);
+  const int nchunks = (int)(end - begin);
+  for (int t = (int)chunk_ticket(counters); t < nchunks; t = (int)chunk_ticket(counters)) {
+    const ChunkInfo ci = chunk_info(g, begin + t, begin);
     if (ci.q_lo > ci.q_hi) continue;
     const int64_t s = ci.s, e = ci.e;
     NzCursor c;

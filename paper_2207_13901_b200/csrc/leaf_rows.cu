@@ -242,12 +242,12 @@ __global__ void __launch_bounds__(kBlock) k_spmm_walk(WalkGeom g, const int64_t*
 // streamed data does not push the reused C rows out of L2.
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
   uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ uint64_t l2_policy_evict_first() {
   uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ double2 ld_f64x2_hint(const double* ptr, uint64_t pol) {
@@ -383,153 +383,6 @@ __device__ __forceinline__ void load_rows(const WalkGeom& g, int64_t rb, int64_t
   }
 }
 
-constexpr int kSpmvBatch = 4;  // 32-position windows whose loads are issued together
-
-__global__ void __launch_bounds__(kBlock) k_spmv_walk(WalkGeom g, const int64_t* __restrict__ crd,
-                                                      const double* __restrict__ vals,
-                                                      const double* __restrict__ x,
-                                                      double* __restrict__ y, ChunkRecs rec,
-                                                      const int64_t* __restrict__ counters) {
-  const int lane = lane_id();
-  const int64_t begin = counters[1], end = counters[2];
-  const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t pol_stream = l2_policy_evict_first();
-  for (int64_t v = begin + chunk_ticket(counters); v < end; v = begin + chunk_ticket(counters)) {
-    const ChunkInfo ci = chunk_info(g, v, begin);
-    if (ci.q_lo > ci.q_hi) {
-      empty_chunk(g, ci, y, rec);
-      continue;
-    }
-    const int64_t k = ci.local, s = ci.s, e = ci.e;
-    const int64_t r0 = warp_owner(g.R, g.nrows, s);
-    bool has_cur, cur_head;
-    int64_t cur = r0, cur_end, rb;
-    double acc = 0.0;
-    if (ld64(g.R + r0) < s) {
-      has_cur = true, cur_head = true, cur_end = ld64(g.R + r0 + 1), rb = r0 + 1;
-    } else {
-      has_cur = false, cur_head = false, cur_end = 0, rb = r0;
-    }
-    if (s == ci.q_lo) zero_rows(y, 1, ci.w_lo, r0 - 1);
-    int64_t head_row = -1, tail_row = -1;
-    int head_cont = 0;
-    double head_val = 0.0, tail_val = 0.0;
-    int64_t S, E;
-    load_rows(g, rb, S, E);
-    for (int64_t bbase = s; bbase <= e; bbase += 32 * kSpmvBatch) {
-      // Issue the batch's streamed loads, then its gathers, before any row logic.
-      int64_t kk[kSpmvBatch];
-      double vv[kSpmvBatch], prods[kSpmvBatch];
-#pragma unroll
-      for (int bi = 0; bi < kSpmvBatch; bi++) {
-        const int64_t q = bbase + 32 * bi + lane;
-        kk[bi] = 0;
-        vv[bi] = 0.0;
-        if (q <= e) {
-          kk[bi] = ld_i64_hint(crd + q, pol_stream);
-          vv[bi] = ld_f64_hint(vals + q, pol_stream);
-        }
-      }
-#pragma unroll
-      for (int bi = 0; bi < kSpmvBatch; bi++) {
-        const int64_t q = bbase + 32 * bi + lane;
-        prods[bi] = q <= e ? vv[bi] * __ldg(x + kk[bi]) : 0.0;
-      }
-#pragma unroll
-      for (int bi = 0; bi < kSpmvBatch; bi++) {
-        const int64_t base = bbase + 32 * bi;
-        if (base > e) break;
-        const int64_t last = min(base + 31, e);
-        const int cnt = (int)(last - base + 1);
-        const double prod = prods[bi];
-        if (has_cur && cur_end - 1 > last) {  // the whole window continues the current row
-          acc += warp_sum(prod);
-          continue;
-        }
-        // pass 1: heads of the non-empty rows starting in the window
-        unsigned heads = 0;
-        int ngroups = 1;
-        {
-          int64_t Sg = S, Eg = E, gb = rb;
-          for (;;) {
-            const bool hit = Eg > Sg && Sg <= last;
-            const unsigned bit = hit ? 1u << (int)(Sg - base) : 0u;
-            heads |= __reduce_or_sync(FULL, bit);
-            if (__shfl_sync(FULL, Sg, 31) > last) break;
-            gb += 32;
-            load_rows(g, gb, Sg, Eg);
-            ngroups++;
-          }
-        }
-        // segmented inclusive scan
-        double sv = prod;
-        unsigned f = (heads >> lane) & 1u;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-          const double tv = __shfl_up_sync(FULL, sv, off);
-          const unsigned tf = __shfl_up_sync(FULL, f, off);
-          if (lane >= off) {
-            if (!f) sv += tv;
-            f |= tf;
-          }
-        }
-        if (has_cur) {  // current row ends inside the window
-          const double tot = acc + __shfl_sync(FULL, sv, (int)(cur_end - 1 - base));
-          if (cur_head) {
-            head_row = cur, head_val = tot, head_cont = 0;
-          } else if (lane == 0) {
-            y[cur] = tot;
-          }
-          has_cur = false;
-          acc = 0.0;
-        }
-        // pass 2: rows starting in the window (and empty rows located in it)
-        int64_t Sg = S, Eg = E, gb = rb;
-        for (int gi = 0; gi < ngroups; gi++) {
-          if (gi > 0) {
-            gb += 32;
-            load_rows(g, gb, Sg, Eg);
-          }
-          const int64_t rr = gb + lane;
-          const bool valid = rr < g.nrows && Sg <= last;
-          const bool ne = Eg > Sg;
-          const int src = (valid && ne) ? (int)(min(Eg - 1, last) - base) : 0;
-          const double val = __shfl_sync(FULL, sv, src);
-          if (valid && rr >= ci.w_lo && rr <= ci.w_hi) {
-            if (!ne) y[rr] = 0.0;
-            else if (Eg - 1 <= last) y[rr] = val;
-          }
-          const unsigned cm = __ballot_sync(FULL, valid && ne && Eg - 1 > last);
-          if (cm) {
-            const int t = __ffs(cm) - 1;
-            has_cur = true;
-            cur_head = false;
-            cur = gb + t;
-            cur_end = __shfl_sync(FULL, Eg, t);
-            acc = __shfl_sync(FULL, sv, cnt - 1);
-          }
-          if (gi == ngroups - 1) rb = gb + __popc(__ballot_sync(FULL, valid));
-        }
-        load_rows(g, rb, S, E);
-      }
-    }
-    if (has_cur) {
-      if (cur_head) head_row = cur, head_val = acc, head_cont = 1;
-      else tail_row = cur, tail_val = acc;
-    } else if (rb < g.nrows) {
-      int64_t nb;
-      skip_empty_rows(g, rb, e + 1, nb, y, ci.w_lo, ci.w_hi);
-    }
-    if (lane == 0) {
-      rec.row[2 * k] = head_row;
-      rec.row[2 * k + 1] = tail_row;
-      rec.cont[k] = head_cont;
-      rec.val[2 * k] = head_val;
-      rec.val[2 * k + 1] = tail_val;
-    }
-  }
-}
 
 }  // namespace spd
 #include "leaf_nz.cuh"
@@ -887,21 +740,6 @@ static void xc_index(spd_context* ctx, spd_tensor* t, int64_t ncols) {
   t->nref = nref;
 }
 
-// SpMV / SpTTV leaf choice: the lane-per-row kernel when the non-empty rows
-// are not long on average (SPD_SPMV_ROWS: 1 always, 0 never, unset: average
-// <= kRowsAvg positions per non-empty row), else the window-scan walk.
-// Measured (profiles/README.md): C1 uniform 0.184 -> 0.117 ms, C4 SpTTV
-// 0.255 -> 0.19 ms, R-MAT SpMV leaf 1.32 -> 1.12 ms.
-constexpr int64_t kRowsAvg = 64;
-static bool spmv_rows_mode(int64_t nnz, int64_t m) {
-  static int v = [] {
-    const char* e = getenv("SPD_SPMV_ROWS");
-    return e ? atoi(e) : -1;
-  }();
-  if (v >= 0) return v != 0;
-  return m > 0 && nnz <= kRowsAvg * m;
-}
-
 // SDDMM over the compacted view (called by sddmm.cu): K = 128, D j-major.
 bool sddmm_nz_launch(spd_context* ctx, const spd_tensor* B, const WalkGeom& g, const double* C,
                      const double* D, int64_t K, int64_t dk, int64_t dj, double* Avals,
@@ -1193,9 +1031,8 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
         grid = ctx->num_sms * (per_sm > 0 ? per_sm : 1);
       }
       k_spmm32_nz<kS, kMinB><<<grid, kBlock, smem, s>>>(g, z, c32, B->vals, a.x, a.out, rec, col.counters);
-    } else if (spmv_rows_mode(nnz, z.m)) {  // short rows: a lane per row
-      // 6 CTAs/SM (40 registers, a few spills) wins on large matrices
-      // (R-MAT leaf 1.11 -> 1.045 ms), 4 on small ones (C1 / C4)
+    } else {  // SpMV / SpTTV: the windowed row reduction
+      // 6 CTAs/SM win on large matrices and CSF fibres, 4 on small ones (C1)
       static int minb_env = [] {
         const char* e = getenv("SPD_SPMV_MINB");
         return e ? atoi(e) : 0;
@@ -1224,27 +1061,16 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
     KERN<<<gr, kBlock, 0, s>>>(g, z, (const CI*)(CRD), B->vals, xv, a.out, rec, col.counters);          \
   } while (0)
       if (c32) {
-        if (minb == 6) SPD_LEAF((k_spmv_rows<6, int32_t>), int32_t, c32);
-        else SPD_LEAF((k_spmv_rows<4, int32_t>), int32_t, c32);
+        if (minb == 6) SPD_LEAF((k_spmv_win<6, int32_t>), int32_t, c32);
+        else SPD_LEAF((k_spmv_win<4, int32_t>), int32_t, c32);
       } else {
-        if (minb == 6) SPD_LEAF((k_spmv_rows<6, int64_t>), int64_t, leaf.crd);
-        else SPD_LEAF((k_spmv_rows<4, int64_t>), int64_t, leaf.crd);
+        if (minb == 6) SPD_LEAF((k_spmv_win<6, int64_t>), int64_t, leaf.crd);
+        else SPD_LEAF((k_spmv_win<4, int64_t>), int64_t, leaf.crd);
       }
 #undef SPD_LEAF
-    } else {
-      static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmv_nz);
-      k_spmv_nz<<<grid, kBlock, 0, s>>>(g, z, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
     }
   } else
-  switch (a.op) {
-    case Op::SpMV:
-    case Op::SpTTV: {
-      static int grid = 0;
-      if (!grid) grid = occupancy_grid(ctx, k_spmv_walk);
-      k_spmv_walk<<<grid, kBlock, 0, s>>>(g, leaf.crd, B->vals, a.x, a.out, rec, col.counters);
-      break;
-    }
+  switch (a.op) {  // SpMM at other widths, SpMTTKRP at other ranks
     case Op::SpMM: {
       if (a.W <= 32) {
         static int grid = 0;

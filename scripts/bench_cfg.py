@@ -262,7 +262,7 @@ def config_c1(env, H, synth):
     out = {"workload": f"C1: SpMV a(i)=B(i,j)*c(j), uniform 1M x 1M, 10M samples ({nnz} nnz), row split "
                        f"into {P} colour(s), one per GPU",
            "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms, "gpu_launches": nl,
-           "roofline": roofline(env, by / env.world, leaf, "k_spmv_rows<4>"),
+           "roofline": roofline(env, by / env.world, leaf, "k_spmv_win<4>"),
            "effective_gbs": by / (ms * 1e-3) / 1e9}
     if env.world > 1:
         step()
@@ -327,7 +327,7 @@ def config_spmv_rmat(env, H, rm, x_seed):
     out = {"workload": f"SpMV a(i)=B(i,j)*c(j) on the C2 R-MAT (scale {rm['scale']}, {nnz} nnz), nonzero split "
                        f"into {P} colour(s)",
            "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms, "gpu_launches": nl,
-           "roofline": roofline(env, by / env.world, leaf, "k_spmv_rows<6,int> over compacted columns"),
+           "roofline": roofline(env, by / env.world, leaf, "k_spmv_win<6,int> over compacted columns"),
            "effective_gbs": by / (ms * 1e-3) / 1e9}
     if env.world > 1:
         step()
@@ -574,7 +574,7 @@ def config_c4(env, H, synth):
         return ref
 
     for name, step, flops, by, kern in (
-            ("C4-SpTTV", step_ttv, 2.0 * nnz, bB + 8 * Kd + 8 * F, "k_spmv_rows<6> over fibres"),
+            ("C4-SpTTV", step_ttv, 2.0 * nnz, bB + 8 * Kd + 8 * F, "k_spmv_win<6> over fibres"),
             ("C4-SpMTTKRP", step_mttkrp, 3.0 * nnz * R, bB + 8 * (J + Kd + I) * R, "k_mttkrp32_nz<4,3>")):
         ms, leaf, nl = measure(env, step)
         check = None

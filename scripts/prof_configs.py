@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--config", required=True, choices=["c1", "spmv", "c3", "ttv", "mttkrp", "c5"])
+ap.add_argument("--config", required=True, choices=["c1", "spmv", "c3", "ttv", "mttkrp", "c5", "spmv_long", "spmv_dense"])
 ap.add_argument("--steps", type=int, default=3)
 ap.add_argument("--scale", type=int, default=24)
 a = ap.parse_args()
@@ -48,6 +48,22 @@ if a.config == "c1":
     x = torch.from_numpy(bench.dense_vals(n, 43)).to(dev)
     y = torch.empty(n, dtype=torch.float64, device=dev)
     ops.append(lambda: (H.partition_universe(ctx, B, 1, host=False), H.spmv(ctx, B, x, y, pieces=1, stats=False)))
+elif a.config in ("spmv_long", "spmv_dense"):
+    # long-row SpMV shapes (no BASELINE config): uniform 400K x 400K with 250
+    # per row, R-MAT scale 20 with edge factor 100
+    if a.config == "spmv_long":
+        n, nz = 400_000, 100_000_000
+        rp, crd, vals = np.empty(n + 1, np.int64), np.empty(nz, np.int64), np.empty(nz)
+        nnz = S.syn_uniform_csr(n, n, nz, 42, 0, rp.ctypes.data_as(N.i64p), crd.ctypes.data_as(N.i64p),
+                                vals.ctypes.data_as(N.dblp))
+        crd, vals = crd[:nnz], vals[:nnz]
+    else:
+        n, rp, crd, vals = bench.rmat_csr(20, 100, 42)
+    B = wrap(n, n, rp, crd, vals)
+    x = torch.from_numpy(bench.dense_vals(n, 44)).to(dev)
+    y = torch.empty(n, dtype=torch.float64, device=dev)
+    ops.append(lambda: (H.partition_nonzero(ctx, B, 1, 1, host=False),
+                        H.spmv(ctx, B, x, y, pieces=1, stats=False)))
 elif a.config in ("spmv", "c3", "c5"):
     n, rp, crd, vals = bench.rmat_csr(a.scale, 10, 42)
     B = wrap(n, n, rp, crd, vals)

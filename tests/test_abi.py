@@ -85,3 +85,23 @@ def test_gpu_dependent_partitioning_fails_loudly_without_a_gpu():
         pytest.skip("needs the GPU-deppart suite on a machine without a GPU")
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert "deppart on gpu: no CUDA device available" in r.stderr
+
+
+def test_production_leaves_do_not_spill():
+    """The SpMV / SpTTV leaf and the C2 SpMM leaf keep their working set in
+    registers at their launch bounds (ptxas log of the in-tree build; a
+    spill on these kernels costs a local-memory round trip per chunk)."""
+    log = os.path.join(PKG, "build", "leaf_rows.ptxas.log")
+    if not os.path.exists(log):
+        pytest.skip("library not built from source here")
+    cur, spills = None, {}
+    for line in open(log):
+        m = re.search(r"Compiling entry function '([^']*)'", line)
+        if m:
+            cur = m.group(1)
+        m = re.search(r"(\d+) bytes spill stores, (\d+) bytes spill loads", line)
+        if m and cur:
+            spills[cur] = int(m.group(1)) + int(m.group(2))
+    prod = {k: v for k, v in spills.items() if "k_spmv_win" in k or "k_spmm32_nz" in k}
+    assert len(prod) >= 5, sorted(spills)
+    assert all(v == 0 for v in prod.values()), prod

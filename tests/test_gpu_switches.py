@@ -16,8 +16,9 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 VARIANTS = [
-    {"SPD_SPMV_ROWS": "0"},  # window-scan SpMV (the long-row leaf) on every matrix
-    {"SPD_SPMV_ROWS": "1"},  # lane-per-row SpMV on every matrix
+    {"SPD_CH_SPMV": "100"},  # SpMV chunks shorter than a window, not a multiple of 32
+    {"SPD_CH_SPMV": "700"},  # several SpMV windows per chunk, a partial last one
+    {"SPD_SPMV_MINB": "6"},  # the 6-CTA SpMV instantiation on the small matrices too
     {"SPD_ZCONC": "0"},  # zero-fill before the leaf instead of concurrent with it
     {"SPD_CH": "64"},  # tiny SpMM / SpMTTKRP chunks: every row crosses chunk records
     {"SPD_XC": "2"},  # compacted-column SpMV on every matrix
