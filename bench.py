@@ -54,6 +54,11 @@ def parse():
     ap.add_argument("--no-traffic", action="store_true",
                     help="skip the ncu DRAM-traffic measurement of the headline leaf (N=1)")
     ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--balance-rounds", type=int, default=3,
+                    help="N > 1: rounds of measured block refinement after the cost model (warm-up)")
+    ap.add_argument("--colours-per-gpu", type=int, default=64,
+                    help="N > 1: colours of the nonzero split per GPU; the contiguous colour block of each GPU "
+                         "is balanced by the cost model (1: one colour per GPU)")
     ap.add_argument("--trace", action="store_true",
                     help="after the timed run, print per-phase device times of the SpMM step (stderr)")
     return ap.parse_args()
@@ -278,28 +283,83 @@ def main():
     A_d = torch.empty(n * N, dtype=torch.float64, device=dev)
     first, count = (rank, 1) if world > 1 else (0, 1)
     pieces = world
-    placement = None
-    Bstep = B
-    if world > 1:
+    blocks = None
+    if world > 1 and args.colours_per_gpu > 1:
+        # Over-decomposition: the reference's nonzero split into
+        # colours_per_gpu * N colours (its partition bounds, bit-exact), and
+        # each GPU runs a contiguous block of them chosen once per pattern by
+        # a cost model -- positions + 2.1 x non-empty rows + 2.7 x empty rows
+        # of the colour's output range, fitted to the per-rank leaf times of
+        # the one-colour-per-GPU run (the row-dense tail costs more per
+        # position: output rows and the zero-fill of empty rows).
+        pieces = args.colours_per_gpu * world
+        H.partition_nonzero(ctx, B, 1, pieces)
+        blocks = H.balance_colour_blocks(ctx, B, pieces, ROW_COST, EMPTY_ROW_COST)
+        pos, nrow, ne = H.colour_costs(ctx, B, pieces)
+        model_cost = (pos + ROW_COST * ne + EMPTY_ROW_COST * (nrow - ne)).astype(np.float64)
+        first, count = int(blocks[rank]), int(blocks[rank + 1] - blocks[rank])
+    def place_B():
         # B placed by its compute partition (spd_tensor_place): each GPU keeps
-        # the row pointer and only its colour's crd/vals -- the matched
+        # the row pointer and only its colour block's crd/vals -- the matched
         # distribution, so the step itself moves none of B.
         dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        Bstep, nbytes = H.DeviceTensor.place(ctx, B if rank == 0 else None, (n, n), fmt, "nonzero", root=0)
+        piece, nbytes = H.DeviceTensor.place(ctx, B if rank == 0 else None, (n, n), fmt, "nonzero", root=0)
         torch.cuda.synchronize()
         pt = torch.tensor([time.perf_counter() - t0, float(nbytes)], dtype=torch.float64, device=dev)
         dist.all_reduce(pt, op=dist.ReduceOp.MAX)
-        lo, hi = Bstep.piece_span()
-        placement = {"ms": float(pt[0]) * 1e3, "max_bytes_received_per_gpu": int(pt[1]),
-                     "piece_positions": int(hi - lo + 1),
-                     "note": "B scattered from rank 0 by the nonzero compute partition (NCCL broadcast of "
-                             "the row pointer + send/recv of crd/vals ranges); outside the timed step"}
+        lo, hi = piece.piece_span()
+        return piece, {"ms": float(pt[0]) * 1e3, "max_bytes_received_per_gpu": int(pt[1]),
+                       "piece_positions": int(hi - lo + 1),
+                       "note": "B scattered from rank 0 by the nonzero compute partition (NCCL broadcast of "
+                               "the row pointer + send/recv of crd/vals ranges); outside the timed step"}
+
+    placement = None
+    Bstep = B
+    if world > 1:
+        Bstep, placement = place_B()
 
     def step():
         H.partition_nonzero(ctx, Bstep, 1, pieces, host=False)
         H.spmm(ctx, Bstep, C_d, N, A_d, first=first, count=count, pieces=pieces, stats=False)
+
+    balance = None
+    if blocks is not None and args.balance_rounds > 0:
+        # Measured refinement (warm-up, outside the timed region): every GPU
+        # times its block's leaf, the times are all-gathered, each block's
+        # colours are re-weighted by measured / modelled cost and the blocks
+        # re-split -- identically on every rank, since all use the same
+        # gathered times.  B is re-placed for the new blocks.
+        cur = model_cost.copy()
+        balance = {"model": "positions + %.1f x non-empty rows + %.1f x empty rows" % (ROW_COST, EMPTY_ROW_COST),
+                   "rounds": []}
+        for _ in range(args.balance_rounds):
+            for _ in range(2):
+                step()
+            torch.cuda.synchronize()
+            ctx.timing(True)
+            for _ in range(4):
+                step()
+            torch.cuda.synchronize()
+            ctx.timing(False)
+            t = torch.tensor([float(np.median(ctx.read_timing()))], dtype=torch.float64, device=dev)
+            allt = [torch.zeros_like(t) for _ in range(world)]
+            dist.all_gather(allt, t)
+            lt = [float(x[0]) for x in allt]
+            balance["rounds"].append({"blocks": [int(b) for b in blocks], "leaf_ms": lt})
+            for r in range(world):
+                seg = slice(int(blocks[r]), int(blocks[r + 1]))
+                cur[seg] *= lt[r] / max(cur[seg].sum(), 1e-30)
+            nb = H.split_colour_blocks(cur, world)
+            if np.array_equal(nb, blocks):
+                break
+            blocks = nb
+            H.set_colour_blocks(ctx, pieces, blocks)
+            first, count = int(blocks[rank]), int(blocks[rank + 1] - blocks[rank])
+            Bstep.close()
+            Bstep, placement = place_B()
+        balance["final_blocks"] = [int(b) for b in blocks]
 
     def measure(step_fn, steps, warmup, with_clocks):
         """W warm-up steps, then exactly `steps` steps bracketed by barrier +
@@ -389,10 +449,10 @@ def main():
     # same bits).  Outside the timed region.
     mgpu_check = None
     if world > 1:
-        from paper_2207_13901_b200.distributed import owned_rows
+        from paper_2207_13901_b200.distributed import block_owned_rows, owned_rows
         cols = H.partition_nonzero(ctx, Bstep, 1, pieces)  # host copy of the colours (syncs)
         rp_host = rp_d.cpu().numpy()
-        W = owned_rows(cols, rp_host, "nonzero", n)
+        W = block_owned_rows(owned_rows(cols, rp_host, "nonzero", n), H.colour_blocks(ctx, pieces))
         H.partition_nonzero(ctx, Bstep, 1, pieces, host=False)
         H.spmm(ctx, Bstep, C_d, N, A_d, first=first, count=count, pieces=pieces, stats=False)
         torch.cuda.synchronize()
@@ -445,9 +505,11 @@ def main():
     if args.e2e_steps is None:
         args.e2e_steps = args.steps
     if args.e2e_steps > 0:
-        e2e = run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, C_d, N)
+        e2e = run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, C_d, N, pieces, blocks)
 
-    # ---- the other BASELINE configs, same run ----
+    # ---- the other BASELINE configs, same run (one colour per GPU) ----
+    if blocks is not None:
+        H.set_colour_blocks(ctx, pieces, None)
     configs = {}
     cfg = [c for c in args.configs.split(",") if c]
     if cfg:
@@ -522,8 +584,13 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "C2: SpMM A(i,j)=B(i,k)*C(k,j), R-MAT scale %d (a,b,c)=(0.57,0.19,0.19), "
-                                   "edge factor %d, nonzero split, one colour per GPU" % (args.scale, args.edge_factor),
+                                   "edge factor %d, nonzero split, %s" % (
+                                       args.scale, args.edge_factor,
+                                       "one colour per GPU" if blocks is None else
+                                       "%d colours, a contiguous cost-balanced block of them per GPU" % pieces),
                        "rows": n, "nnz": nnz, "cols": N, "pieces": pieces,
+                       "colour_blocks": None if blocks is None else [int(b) for b in blocks],
+                       "block_balance": balance,
                        "l2": "inputs (B 2.7 GB, C 4.3 GB) larger than L2; no flush needed",
                        "effective_gbs": alg_bytes_total / (ms * 1e-3) / 1e9,
                        "roofline_frac_step": alg_bytes_total / (ms * 1e-3) / 1e9 / peak,
@@ -582,7 +649,10 @@ def measure_traffic(args):
     return int(vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"])
 
 
-def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, C_d, N):
+ROW_COST, EMPTY_ROW_COST = 2.1, 2.7  # cost model of a colour (bench, N > 1), in positions per output row
+
+
+def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, C_d, N, pieces, blocks):
     """The metric through the C-ABI with HOST buffers, every step:
     H2D of B as the reference stores it (inclusive pos pairs + crd + vals,
     validated and converted on the GPU; at N > 1 only this GPU's colour of
@@ -597,7 +667,7 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
     import torch.distributed as dist
 
     from paper_2207_13901_b200 import _native as NN
-    from paper_2207_13901_b200.distributed import init_comm, owned_rows
+    from paper_2207_13901_b200.distributed import block_owned_rows, init_comm, owned_rows
 
     rp_h = rp_d.cpu()
     pairs = torch.stack([rp_h[:-1], rp_h[1:] - 1], dim=1).contiguous().pin_memory()
@@ -615,6 +685,10 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
     if world > 1:
         for cx in ctxs:
             init_comm(cx, dist, rank, world, dev)
+            if blocks is not None:
+                H.set_colour_blocks(cx, pieces, blocks)
+    first, count = (int(blocks[rank]), int(blocks[rank + 1] - blocks[rank])) if blocks is not None else (
+        rank if world > 1 else 0, 1)
     C_devs = [torch.empty_like(C_d) for _ in range(nbuf)]
     A_devs = [torch.empty(n * N, dtype=torch.float64, device=dev) for _ in range(nbuf)]
     fmt = H.parse_format("ds")
@@ -654,14 +728,14 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
                 cx.allgather(C_devs[j], per * 8)
             tt.append(time.perf_counter())
             if "owned" not in state:
-                cols = H.partition_nonzero(cx, Bs, 1, world)
-                state["owned"] = owned_rows(cols, rp_h.numpy(), "nonzero", n)[rank]
+                cols = H.partition_nonzero(cx, Bs, 1, pieces)
+                state["owned"] = block_owned_rows(owned_rows(cols, rp_h.numpy(), "nonzero", n),
+                                            H.colour_blocks(cx, pieces))[rank]
             else:  # the partition step on the device, no host read-back
-                H.partition_nonzero(cx, Bs, 1, world, host=False)
+                H.partition_nonzero(cx, Bs, 1, pieces, host=False)
             lo, hi = state["owned"]
             tt.append(time.perf_counter())
-            H.spmm(cx, Bs, C_devs[j], N, A_devs[j], first=rank if world > 1 else 0, count=1, pieces=world,
-                   stats=False)
+            H.spmm(cx, Bs, C_devs[j], N, A_devs[j], first=first, count=count, pieces=pieces, stats=False)
             tt.append(time.perf_counter())
             key = "A_h%d" % j
             if key not in state:

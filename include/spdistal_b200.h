@@ -377,6 +377,27 @@ int spd_tensor_piece_span(const spd_tensor* t, int64_t* lo, int64_t* hi);
  * other ranks. */
 int spd_gather_rows(spd_context* ctx, const spd_tensor* A, int root, spd_tensor** out);
 
+/* Colour blocks per GPU.  With a communicator rank r runs one contiguous
+ * block of colours; by default [r * ceil(P / world), ...).  A plan with more
+ * colours than GPUs (over-decomposition) can install its own blocks -- e.g.
+ * balanced by a cost model -- as bounds[0..world] (bounds[0] = 0, bounds[world]
+ * = pieces, every block non-empty); they apply to partitions of `pieces`
+ * colours and must be the same on every rank (the boundary combine's
+ * all-gather layout follows them).  bounds NULL restores the default.  The
+ * reference maps colours to processors in its mapper (sim.cpp:833-847); the
+ * partition itself (its bounds) is unchanged by the blocks. */
+int spd_context_set_colour_blocks(spd_context* ctx, int64_t pieces, const int64_t* bounds);
+/* The blocks a `pieces`-colour partition runs with on this context. */
+int spd_context_colour_blocks(spd_context* ctx, int64_t pieces, int64_t* bounds);
+/* Host-only (no GPU needed): contiguous blocks of near-equal total cost, the
+ * boundary r at the cost prefix nearest r / world of the total. */
+int spd_split_colour_blocks(const double* cost, int64_t pieces, int world, int64_t* bounds);
+/* Per colour of the current partition of the ds matrix t: its positions, the
+ * output rows it stores (W_c) and how many of those rows
+ * are non-empty -- the inputs of a cost model for the blocks above. */
+int spd_colour_costs(spd_context* ctx, const spd_tensor* t, int64_t* positions, int64_t* rows,
+                     int64_t* nonempty);
+
 /* Per-colour Stats::PerWorker::work of the last op (sim.cpp:352), `pieces`
  * entries. */
 int spd_last_work(spd_context* ctx, int64_t* work, int64_t pieces);

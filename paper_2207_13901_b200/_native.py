@@ -117,6 +117,10 @@ SIGNATURES = {
     "spd_tensor_pack": (C.c_int, [vp, C.c_int, i64p, C.POINTER(C.c_int), C.POINTER(C.c_int), i64,
                                   C.POINTER(i64p), dblp, C.c_int, C.POINTER(vp)]),
     "spd_last_work": (C.c_int, [vp, i64p, i64]),
+    "spd_context_set_colour_blocks": (C.c_int, [vp, i64, i64p]),
+    "spd_context_colour_blocks": (C.c_int, [vp, i64, i64p]),
+    "spd_split_colour_blocks": (C.c_int, [dblp, i64, C.c_int, i64p]),
+    "spd_colour_costs": (C.c_int, [vp, vp, i64p, i64p, i64p]),
     "spd_last_owned": (C.c_int, [vp, i64, i64, i64p, i64p]),
     "spd_context_timing": (C.c_int, [vp, C.c_int]),
     "spd_context_read_timing": (C.c_int, [vp, dblp, i64, i64p]),

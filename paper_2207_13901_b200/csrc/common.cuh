@@ -236,6 +236,13 @@ struct spd_context {
   std::vector<spd_color> colors_host;
   bool colors_host_valid = false;
 
+  // Colour blocks per GPU: rank r runs colours [blocks[r], blocks[r + 1]) of a
+  // `blocks_pieces`-colour partition (spd_context_set_colour_blocks); unset or
+  // set for another colour count: even blocks of ceil(P / world) colours.
+  std::vector<int64_t> blocks;
+  int64_t blocks_pieces = -1;
+  spd::DeviceBuffer blocks_dev;      // the same bounds on the device (head-record unpack)
+
   std::vector<int64_t> last_work;    // per colour
   std::vector<spd_tensor*> pending_restage;  // tensors whose last restage verdict is still on its way
   // Last bucket split (spd_partition_bucket): positions of the level sorted by
@@ -347,6 +354,18 @@ void activate(spd_context* ctx);
 const std::vector<spd_color>& host_colors(spd_context* ctx);  // syncs if needed
 void require_partition(spd_context* ctx, const spd_tensor* t, int64_t first, int64_t count,
                        bool allow_grid = false);
+// Colour block of rank r in a P-colour partition (see spd_context::blocks);
+// count 0 when r runs none.  The first form uses the current partition's P.
+void colour_block(const spd_context* ctx, int64_t P, int r, int64_t& first, int64_t& count);
+void colour_block(const spd_context* ctx, int r, int64_t& first, int64_t& count);
+// Colours of the compute partition a piece placement follows: the installed
+// blocks' colour count, else one colour per GPU.
+int64_t placement_pieces(const spd_context* ctx);
+// Leaf position span of every rank's block of a P-colour nonzero (split 2) or
+// row (split 1) partition of the CSR t (partitions t on ctx).
+std::vector<spd_range> rank_spans(spd_context* ctx, spd_tensor* t, int split, int64_t P);
+// Whether the blocks in force are the even ceil(P / world) ones.
+bool even_blocks(const spd_context* ctx);
 void fill_stats(spd_context* ctx, spd_stats* st, int64_t combines, const std::vector<int64_t>& work,
                 int64_t launches, bool timed);
 // Brackets the leaf kernel of an op with a timing event pair when enabled.

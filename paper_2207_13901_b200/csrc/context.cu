@@ -331,6 +331,51 @@ const std::vector<spd_color>& host_colors(spd_context* ctx) {
   return ctx->colors_host;
 }
 
+void colour_block(const spd_context* ctx, int64_t P, int r, int64_t& first, int64_t& count) {
+  if (ctx->blocks_pieces == P && (int)ctx->blocks.size() == ctx->world + 1) {
+    first = ctx->blocks[r];
+    count = ctx->blocks[r + 1] - first;
+    return;
+  }
+  const int64_t cmax = ceil_div(std::max<int64_t>(P, 1), ctx->world);
+  first = std::min<int64_t>(P, r * cmax);
+  count = std::max<int64_t>(0, std::min<int64_t>(cmax, P - first));
+}
+
+void colour_block(const spd_context* ctx, int r, int64_t& first, int64_t& count) {
+  colour_block(ctx, ctx->pieces, r, first, count);
+}
+
+int64_t placement_pieces(const spd_context* ctx) {
+  return (int)ctx->blocks.size() == ctx->world + 1 && ctx->blocks_pieces > 0 ? ctx->blocks_pieces : ctx->world;
+}
+
+std::vector<spd_range> rank_spans(spd_context* ctx, spd_tensor* t, int split, int64_t P) {
+  const int rc = split == 1 ? spd_partition_universe(ctx, t, P, nullptr) : spd_partition_nonzero(ctx, t, 1, P, nullptr);
+  if (rc != SPD_OK) throw ValidationError(spd_last_error());
+  const auto& hc = host_colors(ctx);
+  std::vector<spd_range> out(ctx->world, spd_range{0, -1});
+  for (int r = 0; r < ctx->world; r++) {
+    int64_t f, c;
+    colour_block(ctx, P, r, f, c);
+    int64_t lo = INT64_MAX, hi = -1;
+    for (int64_t k = f; k < f + c; k++)
+      if (hc[k].q.lo <= hc[k].q.hi) lo = std::min(lo, hc[k].q.lo), hi = std::max(hi, hc[k].q.hi);
+    if (lo <= hi) out[r] = spd_range{lo, hi};
+  }
+  return out;
+}
+
+bool even_blocks(const spd_context* ctx) {
+  const int64_t cmax = ceil_div(std::max<int64_t>(ctx->pieces, 1), ctx->world);
+  for (int r = 0; r < ctx->world; r++) {
+    int64_t f, c;
+    colour_block(ctx, r, f, c);
+    if (f != std::min<int64_t>(ctx->pieces, r * cmax)) return false;
+  }
+  return true;
+}
+
 void require_partition(spd_context* ctx, const spd_tensor* t, int64_t first, int64_t count, bool allow_grid) {
   if (ctx->split == SplitKind::None || ctx->split_tensor != t)
     throw ValidationError("no partition of this tensor on the context: call spd_partition_* first");
@@ -339,13 +384,14 @@ void require_partition(spd_context* ctx, const spd_tensor* t, int64_t first, int
   bool all = first == 0 && count == ctx->pieces;
   // With a communicator a GPU runs one contiguous block of colours: rank r
   // runs [r * cmax, min(P, (r + 1) * cmax)), cmax = ceil(P / world) -- one
-  // colour per GPU when P == world (the bench), several when the plan has
-  // more colours than GPUs (the integration adapter on a smaller box).
+  // colour per GPU when P == world, several when the plan has more colours
+  // than GPUs (the integration adapter on a smaller box) -- or the blocks set
+  // by spd_context_set_colour_blocks (cost-balanced over-decomposition).
   bool one_per_rank = false;
   if (ctx->comm && ctx->pieces >= ctx->world) {
-    const int64_t cmax = ceil_div(ctx->pieces, ctx->world);
-    const int64_t f = ctx->rank * cmax;
-    one_per_rank = first == f && count >= 1 && count == std::min<int64_t>(cmax, ctx->pieces - f);
+    int64_t f, c;
+    colour_block(ctx, ctx->rank, f, c);
+    one_per_rank = first == f && count >= 1 && count == c;
   }
   // 2-D machine grid (x major, y minor; MachineGrid::worker_id, machine.cpp:88-92)
   // with the row loop on x: rank r runs row colour r / (world / pieces) of a
@@ -356,7 +402,8 @@ void require_partition(spd_context* ctx, const spd_tensor* t, int64_t first, int
   if (!all && !one_per_rank && !grid_row)
     throw ValidationError(
         "a GPU runs either every colour of the partition, or (with a communicator) its block of colours "
-        "[rank * ceil(pieces / world), ...) (row loops of a 2-D grid: colour rank / (world / pieces))");
+        "(spd_context_colour_blocks: [rank * ceil(pieces / world), ...) unless set) (row loops of a 2-D grid: "
+        "colour rank / (world / pieces))");
 }
 
 void fill_stats(spd_context* ctx, spd_stats* st, int64_t combines, const std::vector<int64_t>& work,
@@ -496,6 +543,7 @@ int spd_context_destroy(spd_context* ctx) {
     cudaStreamSynchronize(ctx->stream);
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     ctx->colors_dev.release();
+    ctx->blocks_dev.release();
     for (auto& b : ctx->scratch) b.release();
     ctx->counters.release();
     for (auto* b : {&ctx->bucket.keys, &ctx->bucket.tmp, &ctx->bucket.pos_buf, &ctx->bucket.pref_buf,
@@ -591,12 +639,18 @@ namespace spd {
 // nonzero split, or over the rows for a row split -- then the positions of
 // that row block.  The pairs are not validated yet; only the two entries read
 // here are range-checked (the device checks the rest).
-static spd_range host_piece_range(const int64_t* pairs, int64_t nrows, int64_t nnz, int split, int world,
-                                  int rank) {
+static spd_range host_piece_range(const int64_t* pairs, int64_t nrows, int64_t nnz, int split,
+                                  const spd_context* ctx) {
+  // this GPU's block [f, f + c) of the placement's P-colour split
+  // (partition_nonzero / partition_universe: colour k of P covers
+  // [k * (n / P), ...), the last colour the remainder)
+  const int64_t P = placement_pieces(ctx);
+  int64_t f, c;
+  colour_block(ctx, P, ctx->rank, f, c);
   auto divide = [&](int64_t n) {
-    const int64_t block = n / world;
-    spd_range r{rank * block, rank < world - 1 ? rank * block + block - 1 : n - 1};
-    if (r.lo > r.hi) r = spd_range{0, -1};
+    const int64_t block = n / P;
+    spd_range r{f * block, f + c < P ? (f + c) * block - 1 : n - 1};
+    if (c < 1 || r.lo > r.hi) r = spd_range{0, -1};
     return r;
   };
   if (split == 2) return divide(nnz);
@@ -624,7 +678,7 @@ static void stage_piece(spd_context* ctx, spd_tensor* t, const int64_t* pairs, c
   spd_level_store& L = t->levels[1];
   const int64_t nrows = L.parent_positions, nnz = L.positions;
   if (nrows > 0 && !pairs) throw ValidationError("compressed level 1 needs pos");
-  const spd_range mine = host_piece_range(pairs, nrows, nnz, split, ctx->world, ctx->rank);
+  const spd_range mine = host_piece_range(pairs, nrows, nnz, split, ctx);
   const int64_t cnt = std::max<int64_t>(mine.hi - mine.lo + 1, 0);
   if (cnt > 0 && !crd) throw ValidationError("compressed level 1 needs crd");
   if (cnt > 0 && !vals) throw ValidationError("tensor: vals length does not match leaf count");
@@ -1226,6 +1280,67 @@ int spd_last_owned(spd_context* ctx, int64_t first, int64_t count, int64_t* lo, 
     for (const DevColor& c : d)
       if (c.w_lo <= c.w_hi) *lo = std::min(*lo, c.w_lo), *hi = std::max(*hi, c.w_hi);
     if (*hi < 0) *lo = 0;
+  });
+}
+
+int spd_split_colour_blocks(const double* cost, int64_t pieces, int world, int64_t* bounds) {
+  return guarded([&] {
+    if (!cost || !bounds) throw ValidationError("null argument");
+    if (world < 1 || pieces < world) throw ValidationError("need at least one colour per GPU");
+    std::vector<double> pre(pieces + 1, 0.0);
+    for (int64_t c = 0; c < pieces; c++) {
+      if (!(cost[c] >= 0.0)) throw ValidationError("colour costs must be non-negative");
+      pre[c + 1] = pre[c] + cost[c];
+    }
+    // boundary r at the prefix nearest r / world of the total, every block non-empty
+    bounds[0] = 0;
+    for (int r = 1; r < world; r++) {
+      const double target = pre[pieces] * r / world;
+      const int64_t lo = bounds[r - 1] + 1, hi = pieces - (world - r);
+      int64_t b = std::lower_bound(pre.begin() + lo, pre.begin() + hi + 1, target) - pre.begin();
+      if (b > hi) b = hi;
+      if (b > lo && target - pre[b - 1] <= pre[b] - target) b--;
+      bounds[r] = b;
+    }
+    bounds[world] = pieces;
+  });
+}
+
+int spd_context_set_colour_blocks(spd_context* ctx, int64_t pieces, const int64_t* bounds) {
+  return guarded([&] {
+    checked(ctx);
+    if (bounds == nullptr) {  // back to even blocks
+      ctx->blocks.clear();
+      ctx->blocks_pieces = -1;
+      return;
+    }
+    if (pieces < ctx->world) throw ValidationError("need at least one colour per GPU");
+    if (bounds[0] != 0 || bounds[ctx->world] != pieces) throw ValidationError("colour blocks must tile [0, pieces)");
+    for (int r = 0; r < ctx->world; r++)
+      if (bounds[r + 1] <= bounds[r]) throw ValidationError("every GPU needs a non-empty colour block");
+    activate(ctx);
+    ctx->blocks.assign(bounds, bounds + ctx->world + 1);
+    ctx->blocks_pieces = pieces;
+    SPD_CUDA(cudaMemcpyAsync(ctx->blocks_dev.reserve(sizeof(int64_t) * (ctx->world + 1)), bounds,
+                             sizeof(int64_t) * (ctx->world + 1), cudaMemcpyHostToDevice, ctx->stream));
+    SPD_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int spd_context_colour_blocks(spd_context* ctx, int64_t pieces, int64_t* bounds) {
+  return guarded([&] {
+    checked(ctx);
+    if (!bounds) throw ValidationError("null argument");
+    if (pieces < 1) throw ValidationError("pieces must be positive");
+    const int64_t saved = ctx->pieces;
+    ctx->pieces = pieces;  // the blocks a partition of `pieces` colours would get
+    for (int r = 0; r < ctx->world; r++) {
+      int64_t f, c;
+      colour_block(ctx, r, f, c);
+      bounds[r] = f;
+    }
+    bounds[ctx->world] = pieces;
+    ctx->pieces = saved;
   });
 }
 

@@ -21,26 +21,91 @@ namespace spd {
 
 // ---------------------------------------------------------------------------
 // Setup: output write ranges W_c and chunk starts for every colour, and the
-// chunk range of the colours this GPU runs.  One CTA; O(P).
-__global__ void k_setup(DevColor* __restrict__ cols, int64_t P, int split, int out_level,
-                        const int64_t* __restrict__ R, int64_t nrows, int64_t CH,
-                        int64_t c_first, int64_t c_count, int64_t* __restrict__ counters) {
-  const int lane = lane_id();
-  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int64_t c = warp; c < P; c += nw) {
-    const spd_color pc = cols[c].pub;
-    int64_t wl = 1, wh = 0;
-    if (split == (int)SplitKind::Universe) {
-      spd_range w = out_level == 0 ? pc.top : pc.par;
-      wl = w.lo, wh = w.hi;
-    } else if (pc.q.lo <= pc.q.hi) {
-      int64_t o = warp_owner(R, nrows, pc.q.lo);
-      wl = ld64(R + o) == pc.q.lo ? o : o + 1;  // first row starting inside the colour
-    }
-    if (lane == 0) cols[c].w_lo = wl, cols[c].w_hi = wh;
+// chunk range of the colours this GPU runs.  k_setup_rows: one warp per
+// colour finds the first row starting inside it (a 32-ary search);
+// k_setup: one CTA links the colours -- W_c of a nonzero split ends before
+// the next non-empty colour's first row -- and numbers the chunks (prefix
+// sum); O(log P) block steps up to 1024 colours, a serial pass above.
+__global__ void k_setup_rows(DevColor* __restrict__ cols, int64_t P, int split, int out_level,
+                             const int64_t* __restrict__ R, int64_t nrows) {
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (c >= P) return;
+  const spd_color pc = cols[c].pub;
+  int64_t wl = 1, wh = 0;
+  if (split == (int)SplitKind::Universe) {
+    spd_range w = out_level == 0 ? pc.top : pc.par;
+    wl = w.lo, wh = w.hi;
+  } else if (pc.q.lo <= pc.q.hi) {
+    int64_t o = warp_owner(R, nrows, pc.q.lo);
+    wl = ld64(R + o) == pc.q.lo ? o : o + 1;  // first row starting inside the colour
   }
-  __syncthreads();
-  if (threadIdx.x != 0) return;
+  if (lane_id() == 0) cols[c].w_lo = wl, cols[c].w_hi = wh;
+}
+
+constexpr int kSetupMax = 1024;
+
+__global__ void __launch_bounds__(kSetupMax) k_setup(DevColor* __restrict__ cols, int64_t P, int split,
+                                                     int64_t nrows, int64_t CH, int64_t c_first, int64_t c_count,
+                                                     int64_t* __restrict__ counters) {
+  __shared__ int64_t a[kSetupMax], b[kSetupMax];
+  const int t = threadIdx.x;
+  if (P <= kSetupMax) {
+    const bool live = t < P;
+    const bool ne = live && cols[t].pub.q.lo <= cols[t].pub.q.hi;
+    int64_t wl = live ? cols[t].w_lo : 0;
+    if (split == (int)SplitKind::NonZero) {
+      // nxt(t) = w_lo of the first non-empty colour after t (nrows if none):
+      // a suffix minimum (non-empty colours' w_lo ascend); first = the
+      // smallest non-empty colour
+      a[t] = ne ? wl : INT64_MAX;
+      b[t] = ne ? t : INT64_MAX;
+      __syncthreads();
+      for (int off = 1; off < kSetupMax; off <<= 1) {
+        const int64_t va = t + off < kSetupMax ? a[t + off] : INT64_MAX;
+        const int64_t vb = t >= off ? b[t - off] : INT64_MAX;
+        __syncthreads();
+        a[t] = min(a[t], va);
+        b[t] = min(b[t], vb);
+        __syncthreads();
+      }
+      const int64_t nxt_incl_next = t + 1 < kSetupMax ? a[t + 1] : INT64_MAX;
+      const int64_t nxt = nxt_incl_next == INT64_MAX ? nrows : nxt_incl_next;
+      const int64_t first_ne = b[kSetupMax - 1];
+      __syncthreads();
+      if (live) {
+        int64_t lo = ne ? wl : nxt, hi = nxt - 1;
+        if (first_ne == INT64_MAX) {  // no positions at all: the last colour stores the zero rows
+          if (t == P - 1) lo = 0, hi = nrows - 1;
+        } else if (t == first_ne) {
+          lo = 0;
+        }
+        cols[t].w_lo = lo, cols[t].w_hi = hi;
+        wl = lo;
+      }
+    }
+    // chunks per colour, exclusive prefix sum
+    int64_t n = 0;
+    if (live) {
+      const DevColor& d = cols[t];
+      n = ne ? (d.pub.q.hi - d.pub.q.lo + CH) / CH : (d.w_lo <= d.w_hi ? 1 : 0);
+    }
+    a[t] = n;
+    __syncthreads();
+    for (int off = 1; off < kSetupMax; off <<= 1) {
+      const int64_t v = t >= off ? a[t - off] : 0;
+      __syncthreads();
+      a[t] += v;
+      __syncthreads();
+    }
+    const int64_t run = a[t] - n;  // exclusive
+    if (live) {
+      cols[t].chunk_begin = run;
+      if (t == c_first) counters[1] = run;
+      if (t == c_first + c_count - 1) counters[2] = a[t];
+    }
+    return;
+  }
+  if (t != 0) return;
   if (split == (int)SplitKind::NonZero) {
     int64_t next = nrows, first_ne = -1;
     for (int64_t c = P - 1; c >= 0; c--) {
@@ -70,6 +135,14 @@ __global__ void k_setup(DevColor* __restrict__ cols, int64_t P, int split, int o
     run += n;
     if (c == c_first + c_count - 1) counters[2] = run;
   }
+}
+
+void launch_setup(cudaStream_t s, DevColor* cols, int64_t P, int split, int out_level, const int64_t* R,
+                  int64_t nrows, int64_t CH, int64_t c_first, int64_t c_count, int64_t* counters) {
+  k_setup_rows<<<(unsigned)ceil_div(P * 32, 256), 256, 0, s>>>(cols, P, split, out_level, R, nrows);
+  SPD_CHECK_LAUNCH();
+  k_setup<<<1, kSetupMax, 0, s>>>(cols, P, split, nrows, CH, c_first, c_count, counters);
+  SPD_CHECK_LAUNCH();
 }
 
 // ---------------------------------------------------------------------------
@@ -389,56 +462,119 @@ __device__ __forceinline__ void load_rows(const WalkGeom& g, int64_t rb, int64_t
 namespace spd {
 
 // ---------------------------------------------------------------------------
+// Non-empty rows in each colour's write range W_c (spd_colour_costs): the
+// compacted row ids inside [w_lo, w_hi], one warp per colour.
+__global__ void k_colour_nonempty(const DevColor* __restrict__ cols, int64_t P, NzView z, int64_t* __restrict__ out) {
+  z.m = nz_count(z);
+  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (c >= P) return;
+  const int64_t lo = cols[c].w_lo, hi = cols[c].w_hi;
+  // rows < lo and rows <= hi among the m sorted ids
+  const int64_t a = warp_upper_bound(z.id, z.m, lo - 1), b = warp_upper_bound(z.id, z.m, hi);
+  if (lane_id() == 0) out[c] = lo <= hi ? b - a : 0;
+}
+
+// ---------------------------------------------------------------------------
+// Uneven colour blocks: the all-gathered head records, cmax slots per rank,
+// to their colours' slots (the calling rank's own block is already there).
+__global__ void k_unpack_heads(const int64_t* __restrict__ stage, const int64_t* __restrict__ bounds, int world,
+                               int own, int64_t cmax, int64_t rec_words, int64_t* __restrict__ head_pack) {
+  const int64_t total = (int64_t)world * cmax * rec_words;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t slot = i / rec_words, w = i - slot * rec_words;
+    const int r = (int)(slot / cmax);
+    const int64_t j = slot - (int64_t)r * cmax;
+    if (r == own || j >= bounds[r + 1] - bounds[r]) continue;
+    head_pack[(bounds[r] + j) * rec_words + w] = stage[i];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Chunk fixup: sums each cut row's records in chunk order.  Rows cut by the
 // end of a colour become colour tail records; the head chain at the start of
 // a colour becomes its packed head record.
+// sum + vals[k0*stride], ..., vals[k1*stride] added in that order, 16 loads
+// in flight (a hub row's chain spans hundreds of chunk records)
+__device__ __forceinline__ double chain_sum(double sum, const double* __restrict__ vals, int64_t stride,
+                                            int64_t k0, int64_t k1) {
+  int64_t k2 = k0;
+  for (; k2 + 15 <= k1; k2 += 16) {
+    double t[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) t[i] = vals[(k2 + i) * stride];
+#pragma unroll
+    for (int i = 0; i < 16; i++) sum += t[i];
+  }
+  for (; k2 <= k1; k2++) sum += vals[k2 * stride];
+  return sum;
+}
+
 __device__ __forceinline__ int64_t chain_stop(const int* __restrict__ cont, int64_t from,
                                               int64_t to) {
   const int lane = lane_id();
-  for (int64_t b = from; b < to; b += 32) {
-    const int64_t k2 = b + lane;
-    const bool stop = k2 < to && cont[k2] == 0;
-    const unsigned m = __ballot_sync(FULL, stop);
-    if (m) return b + __ffs(m) - 1;
+  for (int64_t b = from; b < to; b += 128) {  // 128 flags per round, loads issued together
+    int f[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) f[i] = b + 32 * i + lane < to ? cont[b + 32 * i + lane] : 1;
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+      const unsigned m = __ballot_sync(FULL, b + 32 * i + lane < to && f[i] == 0);
+      if (m) return b + 32 * i + __ffs(m) - 1;
+    }
   }
   return to;
 }
 
+constexpr int kFixupColours = 1024;  // colours whose chunk starts the fixup keeps in shared memory
+
 __global__ void __launch_bounds__(kBlock) k_chunk_fixup(WalkGeom g, ChunkRecs rec, ColorRecs col,
                                                         double* __restrict__ out) {
+  // the chunk starts of this GPU's colours, so a chunk's colour is a search
+  // in shared memory instead of log2(P) dependent global loads
+  __shared__ int64_t cb_s[kFixupColours];
+  const bool in_smem = g.c_count <= kFixupColours;
+  if (in_smem)
+    for (int64_t i = threadIdx.x; i < g.c_count; i += blockDim.x) cb_s[i] = g.cols[g.c_first + i].chunk_begin;
+  __syncthreads();
   const int lane = lane_id();
   const int64_t begin = col.counters[1], end = col.counters[2];
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t W = g.W;
   for (int64_t v = begin + gw; v < end; v += nw) {
-    const int64_t c = colour_of_chunk(g, v);
+    int64_t c;
+    if (in_smem) {
+      int64_t lo = 0, hi = g.c_count - 1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (cb_s[mid] <= v) lo = mid; else hi = mid - 1;
+      }
+      c = g.c_first + lo;
+    } else {
+      c = colour_of_chunk(g, v);
+    }
     const int64_t k = v - begin;
     const int64_t cend =
-        (c + 1 < g.c_first + g.c_count ? g.cols[c + 1].chunk_begin : end) - begin;
+        (c + 1 < g.c_first + g.c_count ? (in_smem ? cb_s[c + 1 - g.c_first] : g.cols[c + 1].chunk_begin) : end) -
+        begin;
     const int64_t trow = rec.row[2 * k + 1];
     if (trow >= 0) {
       const int64_t stop = chain_stop(rec.cont, k + 1, cend);
       const int64_t last = stop < cend ? stop : cend - 1;
       for (int64_t j = lane; j < W; j += 32) {
-        double sum = rec.val[(2 * k + 1) * W + j];
-#pragma unroll 4
-        for (int64_t k2 = k + 1; k2 <= last; k2++) sum += rec.val[2 * k2 * W + j];
+        const double sum = chain_sum(rec.val[(2 * k + 1) * W + j], rec.val + j, 2 * W, k + 1, last);
         if (stop < cend) out[trow * W + j] = sum;
         else col.tail_val[c * W + j] = sum;
       }
       if (stop >= cend && lane == 0) col.tail_row[c] = trow;
     }
     const int64_t hrow = rec.row[2 * k];
-    if (v == g.cols[c].chunk_begin && hrow >= 0) {
+    if (v == (in_smem ? cb_s[c - g.c_first] : g.cols[c].chunk_begin) && hrow >= 0) {
       const int64_t stop = rec.cont[k] == 0 ? k : chain_stop(rec.cont, k + 1, cend);
       const int64_t last = stop < cend ? stop : cend - 1;
       int64_t* pack = col.head_pack + c * (W + 2);
       for (int64_t j = lane; j < W; j += 32) {
-        double sum = 0.0;
-#pragma unroll 4
-        for (int64_t k2 = k; k2 <= last; k2++) sum += rec.val[2 * k2 * W + j];
-        reinterpret_cast<double*>(pack)[2 + j] = sum;
+        reinterpret_cast<double*>(pack)[2 + j] = chain_sum(0.0, rec.val + j, 2 * W, k, last);
       }
       if (lane == 0) {
         pack[0] = hrow;
@@ -899,13 +1035,25 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   rec.cont = (int*)ctx->scratch[1].reserve(sizeof(int) * max_chunks);
   rec.val = (double*)ctx->scratch[2].reserve(sizeof(double) * 2 * max_chunks * W);
   ColorRecs col;
-  // colour blocks per GPU (require_partition): the head records of rank r's
-  // block sit at slots [r * cmax, r * cmax + cmax) so one all-gather of cmax
-  // slots per rank lays every colour's record at its own slot
+  // colour blocks per GPU (require_partition): with the even blocks rank r's
+  // head records sit at slots [r * cmax, r * cmax + cmax), so one all-gather
+  // of cmax slots per rank lays every colour's record at its own slot; with
+  // uneven blocks (spd_context_set_colour_blocks) the all-gather goes to a
+  // staging area of cmax = the largest block per rank and k_unpack_heads
+  // moves each record to its colour's slot
   const bool cross_gpu = ctx->comm && ctx->world > 1 && P > 1 && ctx->split != SplitKind::Universe &&
                          !(first == 0 && count == P);
-  const int64_t cmax = cross_gpu ? ceil_div(P, ctx->world) : 1;
-  const int64_t pack_slots = cross_gpu ? cmax * ctx->world : P;
+  const bool even = !cross_gpu || even_blocks(ctx);
+  int64_t cmax = 1;
+  if (cross_gpu)
+    for (int r = 0; r < ctx->world; r++) {
+      int64_t f, c;
+      colour_block(ctx, r, f, c);
+      cmax = std::max(cmax, c);
+    }
+  // even: every rank's window inside P rounded up; uneven: a short block's
+  // window may run past its colours (the extra slots are ignored)
+  const int64_t pack_slots = cross_gpu ? (even ? cmax * ctx->world : P + cmax) : P;
   col.head_pack = (int64_t*)ctx->scratch[3].reserve(sizeof(int64_t) * pack_slots * (W + 2));
   char* cr = (char*)ctx->scratch[4].reserve(sizeof(int64_t) * (P + 4) + sizeof(double) * P * W);
   col.counters = (int64_t*)cr;
@@ -920,10 +1068,9 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   SPD_CUDA(cudaMemsetAsync(col.counters, 0, sizeof(int64_t) * 4, s));
   SPD_CUDA(cudaMemsetAsync(col.tail_row, 0xff, sizeof(int64_t) * P, s));
   ht.mark("scratch");
-  k_setup<<<1, 1024, 0, s>>>((DevColor*)ctx->colors_dev.ptr, P, (int)ctx->split, out_level, g.R,
-                             g.nrows, g.CH, first, count, col.counters);
-  SPD_CHECK_LAUNCH();
-  launches++;
+  launch_setup(s, (DevColor*)ctx->colors_dev.ptr, P, (int)ctx->split, out_level, g.R, g.nrows, g.CH, first, count,
+               col.counters);
+  launches += 2;
 
   const spd_level_store& leaf = B->levels[nl - 1];
   const bool mttkrp32 = a.op == Op::SpMTTKRP && a.W == 32 && B->dims[1] < (int64_t(1) << 31) &&
@@ -1126,9 +1273,18 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
     launches++;
   }
   trace_mark(ctx);
-  if (cross_gpu) {  // rows cut between GPUs: every colour's head record to every GPU
+  if (cross_gpu && even) {  // rows cut between GPUs: every colour's head record to every GPU
     const size_t bytes = sizeof(int64_t) * cmax * (W + 2);
     SPD_NCCL(ncclAllGather(col.head_pack + first * (W + 2), col.head_pack, bytes, ncclUint8, ctx->comm, s));
+  } else if (cross_gpu) {
+    const size_t bytes = sizeof(int64_t) * cmax * (W + 2);
+    int64_t* stage = (int64_t*)ctx->scratch[6].reserve(bytes * ctx->world);
+    SPD_NCCL(ncclAllGather(col.head_pack + first * (W + 2), stage, bytes, ncclUint8, ctx->comm, s));
+    const int64_t words = cmax * ctx->world * (W + 2);
+    k_unpack_heads<<<(unsigned)std::min<int64_t>(ceil_div(words, 256), 1024), 256, 0, s>>>(
+        stage, (const int64_t*)ctx->blocks_dev.ptr, ctx->world, ctx->rank, cmax, W + 2, col.head_pack);
+    SPD_CHECK_LAUNCH();
+    launches++;
   }
   trace_mark(ctx);
   k_colour_combine<<<(unsigned)ceil_div(P * 32, 256), 256, 0, s>>>(
@@ -1186,6 +1342,40 @@ int spd_spmttkrp(spd_context* ctx, const spd_tensor* B, const double* C_dev,
   return guarded([&] {
     run_rowwalk(ctx, OpArgs{Op::SpMTTKRP, B, C_dev, D_dev, R, A_dev}, first_color, ncolors,
                 stats);
+  });
+}
+
+
+int spd_colour_costs(spd_context* ctx, const spd_tensor* t, int64_t* positions, int64_t* rows,
+                     int64_t* nonempty) {
+  return guarded([&] {
+    checked(ctx);
+    if (!t || !positions || !rows || !nonempty) throw ValidationError("null argument");
+    settle_restage(t);
+    if (ctx->split == SplitKind::None || ctx->split_tensor != t)
+      throw ValidationError("no partition of this tensor on the context: call spd_partition_* first");
+    if (t->levels.size() != 2 || t->levels[0].kind != SPD_DENSE || t->levels[1].kind != SPD_COMPRESSED)
+      throw ValidationError("colour costs: a ds (CSR-like) matrix");
+    activate(ctx);
+    cudaStream_t s = ctx->stream;
+    const int64_t P = ctx->pieces;
+    const spd_level_store& L = t->levels[1];
+    int64_t* cnt = (int64_t*)ctx->scratch[6].reserve(sizeof(int64_t) * (P + 4));
+    // W_c as the row-reducing ops store them, then the non-empty rows in W_c
+    launch_setup(s, (DevColor*)ctx->colors_dev.ptr, P, (int)ctx->split, 0, L.rowptr, L.parent_positions, 1024, 0,
+                 P, cnt + P);
+    NzView z = nz_view(ctx, const_cast<spd_tensor*>(t), L.rowptr, L.parent_positions);
+    k_colour_nonempty<<<(unsigned)ceil_div(P * 32, 256), 256, 0, s>>>((const DevColor*)ctx->colors_dev.ptr, P, z,
+                                                                     cnt);
+    SPD_CHECK_LAUNCH();
+    std::vector<DevColor> d(P);
+    SPD_CUDA(cudaMemcpyAsync(d.data(), ctx->colors_dev.ptr, sizeof(DevColor) * P, cudaMemcpyDeviceToHost, s));
+    SPD_CUDA(cudaMemcpyAsync(nonempty, cnt, sizeof(int64_t) * P, cudaMemcpyDeviceToHost, s));
+    SPD_CUDA(cudaStreamSynchronize(s));
+    for (int64_t c = 0; c < P; c++) {
+      positions[c] = d[c].pub.q.lo <= d[c].pub.q.hi ? d[c].pub.q.hi - d[c].pub.q.lo + 1 : 0;
+      rows[c] = d[c].w_lo <= d[c].w_hi ? d[c].w_hi - d[c].w_lo + 1 : 0;
+    }
   });
 }
 

@@ -87,12 +87,10 @@ void run_place(spd_context* ctx, int root, const spd_tensor* whole, int split, s
     t->piece = true;
     t->piece_split = split;
     set_whole_span(t);
-    // the compute partition, the same on every GPU (one colour per GPU)
-    const int rc = split == 1 ? spd_partition_universe(ctx, t, ctx->world, nullptr)
-                              : spd_partition_nonzero(ctx, t, 1, ctx->world, nullptr);
-    if (rc != SPD_OK) throw ValidationError(spd_last_error());
-    const auto& hc = host_colors(ctx);
-    const spd_range mine = hc[ctx->rank].q;
+    // the compute partition, the same on every GPU: one colour per GPU, or
+    // each GPU's block of the installed colour blocks (over-decomposition)
+    const std::vector<spd_range> span = rank_spans(ctx, t, split, placement_pieces(ctx));
+    const spd_range mine = span[ctx->rank];
     t->piece_lo = mine.lo;
     t->piece_hi = mine.hi;
     const int64_t cnt = std::max<int64_t>(mine.hi - mine.lo + 1, 0);
@@ -104,7 +102,7 @@ void run_place(spd_context* ctx, int root, const spd_tensor* whole, int split, s
     SPD_NCCL(ncclGroupStart());
     if (is_root) {
       for (int r = 0; r < ctx->world; r++) {
-        const spd_range q = hc[r].q;
+        const spd_range q = span[r];
         const int64_t c = q.hi - q.lo + 1;
         if (c <= 0) continue;
         if (r == root) {
@@ -148,14 +146,7 @@ void run_repartition(spd_context* ctx, const spd_tensor* t, int need_split, spd_
   cudaStream_t s = ctx->stream;
   spd_tensor* tm = const_cast<spd_tensor*>(t);
   const int W = ctx->world;
-  auto colours = [&](int split) {
-    const int rc = split == 1 ? spd_partition_universe(ctx, tm, W, nullptr)
-                              : spd_partition_nonzero(ctx, tm, 1, W, nullptr);
-    if (rc != SPD_OK) throw ValidationError(spd_last_error());
-    std::vector<spd_range> q;
-    for (const auto& c : host_colors(ctx)) q.push_back(c.q);
-    return q;
-  };
+  auto colours = [&](int split) { return rank_spans(ctx, tm, split, placement_pieces(ctx)); };
   const std::vector<spd_range> held = colours(t->piece_split);
   const std::vector<spd_range> need = colours(need_split);
   const int me = ctx->rank;

@@ -18,9 +18,8 @@ namespace spd {
 
 #define FULL 0xffffffffu
 
-__global__ void k_setup(DevColor* __restrict__ cols, int64_t P, int split, int out_level,
-                        const int64_t* __restrict__ R, int64_t nrows, int64_t CH,
-                        int64_t c_first, int64_t c_count, int64_t* __restrict__ counters);
+void launch_setup(cudaStream_t s, DevColor* cols, int64_t P, int split, int out_level, const int64_t* R,
+                  int64_t nrows, int64_t CH, int64_t c_first, int64_t c_count, int64_t* counters);
 
 bool sddmm_nz_launch(spd_context* ctx, const spd_tensor* B, const WalkGeom& g, const double* C,
                      const double* D, int64_t K, int64_t dk, int64_t dj, double* Avals,
@@ -135,10 +134,8 @@ static void run_sddmm(spd_context* ctx, const spd_tensor* B, const double* C, co
   int64_t launches = 0;
   if (stats) SPD_CUDA(cudaEventRecord(ctx->ev0, s));
   SPD_CUDA(cudaMemsetAsync(counters, 0, sizeof(int64_t) * 4, s));
-  k_setup<<<1, 1024, 0, s>>>((DevColor*)ctx->colors_dev.ptr, P, (int)ctx->split, 0, g.R, g.nrows,
-                             g.CH, first, count, counters);
-  SPD_CHECK_LAUNCH();
-  launches++;
+  launch_setup(s, (DevColor*)ctx->colors_dev.ptr, P, (int)ctx->split, 0, g.R, g.nrows, g.CH, first, count, counters);
+  launches += 2;
   const int64_t kt = ceil_div(K > 0 ? K : 1, 32);
   leaf_timing_begin(ctx);
   if (sddmm_nz_launch(ctx, B, g, C, D, K, dk, dj, Avals, counters)) {

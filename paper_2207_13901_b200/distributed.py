@@ -126,3 +126,30 @@ def colour_blocks(pieces: int, gpus: int):
     cmax = -(-max(pieces, 1) // g)
     used = max(1, -(-max(pieces, 1) // cmax))
     return [(r * cmax, min(cmax, pieces - r * cmax)) for r in range(used)]
+
+
+def block_owned_rows(W, bounds):
+    """Owned output rows per GPU under colour blocks (spd_context_colour_blocks):
+    GPU r stores the union of W_c over its block [bounds[r], bounds[r + 1]) --
+    contiguous, since the W_c tile the rows in colour order.  Returns
+    [(lo, hi)] per GPU, (0, -1) when its block stores no row."""
+    out = []
+    for r in range(len(bounds) - 1):
+        rng = [(lo, hi) for lo, hi in W[bounds[r]:bounds[r + 1]] if lo <= hi]
+        out.append((min(lo for lo, _ in rng), max(hi for _, hi in rng)) if rng else (0, -1))
+    return out
+
+
+def unpack_head_records(stage, bounds, own, cmax):
+    """Host mirror of k_unpack_heads: the all-gathered head records (cmax
+    slots per rank, rank r's block in its first bounds[r+1]-bounds[r] slots)
+    to one record per colour; the caller's own block is taken from `own`
+    (its records by colour).  Returns the per-colour list."""
+    P = int(bounds[-1])
+    out = [None] * P
+    for r in range(len(bounds) - 1):
+        for j in range(int(bounds[r + 1] - bounds[r])):
+            c = int(bounds[r]) + j
+            out[c] = own[c] if c in own else stage[r * cmax + j]
+    return out
+

@@ -231,6 +231,7 @@ class Context:
         h = C.c_void_p()
         check(N.lib().spd_context_create(device, C.c_void_p(stream) if stream else None, C.byref(h)))
         self.h = h
+        self.rank, self.world = 0, 1
 
     def synchronize(self):
         check(N.lib().spd_context_synchronize(self.h))
@@ -238,6 +239,7 @@ class Context:
     def init_comm(self, unique_id: bytes, rank: int, world: int):
         buf = C.create_string_buffer(unique_id, 128)
         check(N.lib().spd_context_init_comm(self.h, buf, rank, world))
+        self.rank, self.world = rank, world
 
     def capture(self):
         """Context manager: the ops enqueued inside become a Graph
@@ -757,6 +759,54 @@ def last_owned(ctx, first, count):
     lo, hi = C.c_int64(), C.c_int64()
     check(N.lib().spd_last_owned(ctx.h, first, count, C.byref(lo), C.byref(hi)))
     return lo.value, hi.value
+
+
+def split_colour_blocks(costs, world):
+    """spd_split_colour_blocks (host only): bounds[0..world] of contiguous
+    colour blocks of near-equal total cost."""
+    costs = np.ascontiguousarray(costs, dtype=np.float64)
+    b = np.zeros(world + 1, dtype=np.int64)
+    check(N.lib().spd_split_colour_blocks(costs.ctypes.data_as(N.dblp), len(costs), world,
+                                          b.ctypes.data_as(N.i64p)))
+    return b
+
+
+def set_colour_blocks(ctx, pieces, bounds):
+    """spd_context_set_colour_blocks; bounds None restores the even blocks."""
+    if bounds is None:
+        check(N.lib().spd_context_set_colour_blocks(ctx.h, pieces, None))
+        return
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    check(N.lib().spd_context_set_colour_blocks(ctx.h, pieces, b.ctypes.data_as(N.i64p)))
+
+
+def colour_blocks(ctx, pieces):
+    """spd_context_colour_blocks: the bounds[0..world] a `pieces`-colour
+    partition runs with; rank r runs [bounds[r], bounds[r + 1])."""
+    b = np.zeros(ctx.world + 1, dtype=np.int64)
+    check(N.lib().spd_context_colour_blocks(ctx.h, pieces, b.ctypes.data_as(N.i64p)))
+    return b
+
+
+def colour_costs(ctx, t: DeviceTensor, pieces):
+    """spd_colour_costs: per colour of the current partition of the ds matrix
+    t, (positions, output rows W_c, non-empty rows of W_c)."""
+    out = [np.zeros(pieces, dtype=np.int64) for _ in range(3)]
+    check(N.lib().spd_colour_costs(ctx.h, t.h, *(o.ctypes.data_as(N.i64p) for o in out)))
+    return tuple(out)
+
+
+def balance_colour_blocks(ctx, t: DeviceTensor, pieces, row_cost, empty_row_cost):
+    """Cost-balanced colour blocks for an over-decomposed plan (pieces >
+    world): cost_c = positions + row_cost * non-empty rows + empty_row_cost *
+    empty rows of W_c, split into contiguous blocks of near-equal cost and
+    installed on the context.  Deterministic, so every rank computes the same
+    blocks from the same partition.  Returns the bounds."""
+    pos, rows, ne = colour_costs(ctx, t, pieces)
+    cost = pos + row_cost * ne + empty_row_cost * (rows - ne)
+    b = split_colour_blocks(cost, ctx.world)
+    set_colour_blocks(ctx, pieces, b)
+    return b
 
 
 def spmm(ctx, B: DeviceTensor, Cd, n_cols, A, first=0, count=None, pieces=None, stats=True):

@@ -621,3 +621,48 @@ def test_spmv_wide_x_compacted_columns(ctx, schedule, pieces):
             assert st.work == want["work"] and st.combines == want["combines"]
     finally:
         dev.close()
+
+
+@pytest.mark.parametrize("schedule,pieces", [("nonzero", 1), ("nonzero", 7), ("row", 5)])
+def test_colour_costs_and_blocks(ctx, schedule, pieces):
+    """spd_colour_costs: per colour the positions, the output rows W_c the
+    row-reducing ops store and the non-empty ones among them, against the
+    host computation over the oracle's partition; colour blocks: defaults,
+    installation, validation."""
+    import torch
+
+    from paper_2207_13901_b200 import host as H
+    from paper_2207_13901_b200._native import SpdValidationError
+    from paper_2207_13901_b200.distributed import owned_rows
+
+    rng = np.random.default_rng(23)
+    n, m = 5000, 300
+    rows = np.concatenate([np.full(400, 7), rng.integers(0, 600, 3000), rng.integers(0, n, 500)])
+    cols = rng.integers(0, m, rows.shape[0])
+    B = H.SparseTensor.pack((n, m), H.parse_format("ds"), np.stack([rows, cols], 1),
+                            rng.integers(1, 5, rows.shape[0]).astype(float))
+    rp, crd, v = B.levels[1].rowptr(), B.levels[1].crd, B.vals
+    d = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (rp, crd, v)]
+    Bd = H.DeviceTensor.wrap(ctx, (n, m), H.parse_format("ds"), [d[0].data_ptr()], [d[1].data_ptr()],
+                             d[2].data_ptr(), keep=tuple(d))
+    try:
+        cols_h = (H.partition_nonzero(ctx, Bd, 1, pieces) if schedule == "nonzero"
+                  else H.partition_universe(ctx, Bd, pieces))
+        pos, nrows, ne = H.colour_costs(ctx, Bd, pieces)
+        W = owned_rows(cols_h, rp, schedule, n)
+        nonempty = np.diff(rp) > 0
+        for k, c in enumerate(cols_h):
+            lo, hi = c.q
+            assert pos[k] == max(hi - lo + 1, 0)
+            wl, wh = W[k]
+            assert nrows[k] == max(wh - wl + 1, 0)
+            assert ne[k] == (int(nonempty[wl:wh + 1].sum()) if wl <= wh else 0)
+        # one GPU: the blocks are the whole partition; installing needs world + 1 bounds
+        assert list(H.colour_blocks(ctx, pieces)) == [0, pieces]
+        H.set_colour_blocks(ctx, pieces, [0, pieces])
+        assert list(H.colour_blocks(ctx, pieces)) == [0, pieces]
+        with pytest.raises(SpdValidationError):
+            H.set_colour_blocks(ctx, pieces, [1, pieces])
+        H.set_colour_blocks(ctx, pieces, None)
+    finally:
+        Bd.close()
