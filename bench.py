@@ -508,10 +508,13 @@ def main():
         e2e = run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, C_d, N, pieces, blocks)
 
     # ---- the other BASELINE configs, same run (one colour per GPU) ----
-    if blocks is not None:
-        H.set_colour_blocks(ctx, pieces, None)
     configs = {}
     cfg = [c for c in args.configs.split(",") if c]
+    if blocks is not None:
+        H.set_colour_blocks(ctx, pieces, None)
+        if cfg:  # B re-placed by the one-colour-per-GPU split the configs run
+            Bstep.close()
+            Bstep, _ = place_B()
     if cfg:
         sys.path.insert(0, os.path.join(ROOT, "scripts"))
         import bench_cfg as BC
