@@ -79,6 +79,24 @@ class Env:
         return (self.rank, 1, self.world) if self.world > 1 else (0, 1, 1)
 
 
+def _block_times(env, step):
+    """Median leaf time of a few steps on every GPU (all-gathered): the
+    measurement the colour-block refinement re-weights by."""
+    torch = env.torch
+    for _ in range(2):
+        step()
+    torch.cuda.synchronize()
+    env.ctx.timing(True)
+    for _ in range(4):
+        step()
+    torch.cuda.synchronize()
+    env.ctx.timing(False)
+    t = torch.tensor([float(np.median(env.ctx.read_timing()))], dtype=torch.float64, device=env.dev)
+    allt = [torch.zeros_like(t) for _ in range(env.world)]
+    env.dist.all_gather(allt, t)
+    return [float(x[0]) for x in allt]
+
+
 def measure(env, step, kernel_share=1.0):
     """W warm-up steps, then K timed steps bracketed by barrier + synchronize,
     CUDA events on the launching stream; the leaf's own CUDA-event pairs
@@ -657,22 +675,53 @@ def config_c5(env, H, rm):
                                         a[2].data_ptr(), keep=tuple(a)))
     nin = sum(d._keep[1].numel() for d in devs)
     P = 8 if env.world == 1 else env.world
-    first, count = (0, P) if env.world == 1 else (env.rank, 1)
+    sel = {"first": 0, "count": P} if env.world == 1 else {"first": env.rank, "count": 1}
     live = {"A": None}
 
     def step():
         if live["A"] is not None:
             live["A"].close()
         H.partition_universe(env.ctx, devs[0], P, host=False)
-        live["A"], _ = H.spadd3(env.ctx, devs[0], devs[1], devs[2], first=first, count=count, pieces=P,
-                                stats=False)
+        live["A"], _ = H.spadd3(env.ctx, devs[0], devs[1], devs[2], first=sel["first"], count=sel["count"],
+                                pieces=P, stats=False)
+
+    balance = None
+    if env.world > 1 and env.args.colours_per_gpu > 1:
+        # the row split over-decomposed into colours_per_gpu x N row blocks,
+        # each GPU running a contiguous block of them balanced by the inputs'
+        # stored entries (3 x B's positions: C and D are B shifted) + rows,
+        # then refined by measured times (as the C2 headline)
+        P = env.args.colours_per_gpu * env.world
+        H.partition_universe(env.ctx, devs[0], P)
+        pos, nrow, _ = H.colour_costs(env.ctx, devs[0], P)
+        cur = (3.0 * pos + nrow).astype(np.float64)
+        bounds = H.split_colour_blocks(cur, env.world)
+        balance = {"model": "3 x positions + rows", "rounds": []}
+        for it in range(env.args.balance_rounds + 1):
+            H.set_colour_blocks(env.ctx, P, bounds)
+            sel["first"], sel["count"] = int(bounds[env.rank]), int(bounds[env.rank + 1] - bounds[env.rank])
+            if it == env.args.balance_rounds:
+                break
+            lt = _block_times(env, step)
+            balance["rounds"].append({"blocks": [int(b) for b in bounds], "leaf_ms": lt})
+            for r in range(env.world):
+                seg = slice(int(bounds[r]), int(bounds[r + 1]))
+                cur[seg] *= lt[r] / max(cur[seg].sum(), 1e-30)
+            nb = H.split_colour_blocks(cur, env.world)
+            if np.array_equal(nb, bounds):
+                break
+            bounds = nb
+        balance["final_blocks"] = [int(b) for b in bounds]
+    first, count = sel["first"], sel["count"]
 
     ms, leaf, nl = measure(env, step)
     A = live["A"]
     nA = int(np.sum(env.maxr([float(A.global_span()[3] if env.world > 1 else A.nvals())])))
     by = sum(8 * (n + 1) + 16 * d._keep[1].numel() for d in devs) + 8 * (n + 1) + 16 * nA
     out = {"workload": f"C5: SpAdd3 A=B+C+D, the C2 R-MAT and two copies with columns shifted +1/+2 "
-                       f"({nin} input nnz -> {nA}), row split into {P} colour(s)",
+                       f"({nin} input nnz -> {nA}), row split into {P} colour(s)" +
+                       ("" if balance is None else ", a contiguous cost-balanced block of them per GPU"),
+           "block_balance": balance,
            "value": float(nin) / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms, "gpu_launches": nl,
            "roofline": roofline(env, by / env.world, ms,
                                 "the SpAdd3 step (count, scan, allocate, fill; leaf = whole step)"),
@@ -703,6 +752,8 @@ def config_c5(env, H, rm):
                                           "of the same partition on rank 0's GPU: row pointer, crd, vals"}
     A.close()
     live["A"] = None
+    if balance is not None:
+        H.set_colour_blocks(env.ctx, P, None)
     if env.world == 1:
         steps = []
         nbytes = 0
