@@ -527,8 +527,15 @@ __device__ __forceinline__ int64_t chain_stop(const int* __restrict__ cont, int6
 
 constexpr int kFixupColours = 1024;  // colours whose chunk starts the fixup keeps in shared memory
 
+// One warp per 32 consecutive chunks, a lane per chunk: the common case -- a
+// tail record whose row ends in the next chunk (or at the colour's end) --
+// is summed by its own lane (tail + the next chunk's head, vectorised over
+// the row's W values), so the records of 32 chunks are in flight together;
+// rows spanning several chunks and colour-start head records go through the
+// warp-cooperative chain sums, one chunk at a time.  `vec2`: W even and the
+// output 16-byte aligned.
 __global__ void __launch_bounds__(kBlock) k_chunk_fixup(WalkGeom g, ChunkRecs rec, ColorRecs col,
-                                                        double* __restrict__ out) {
+                                                        double* __restrict__ out, int vec2) {
   // the chunk starts of this GPU's colours, so a chunk's colour is a search
   // in shared memory instead of log2(P) dependent global loads
   __shared__ int64_t cb_s[kFixupColours];
@@ -541,44 +548,78 @@ __global__ void __launch_bounds__(kBlock) k_chunk_fixup(WalkGeom g, ChunkRecs re
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t W = g.W;
-  for (int64_t v = begin + gw; v < end; v += nw) {
-    int64_t c;
-    if (in_smem) {
-      int64_t lo = 0, hi = g.c_count - 1;
-      while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (cb_s[mid] <= v) lo = mid; else hi = mid - 1;
+  for (int64_t v0 = begin + gw * 32; v0 < end; v0 += nw * 32) {
+    const int64_t v = v0 + lane;
+    const bool live = v < end;
+    int64_t c = g.c_first;
+    if (live) {
+      if (in_smem) {
+        int64_t lo = 0, hi = g.c_count - 1;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi + 1) >> 1;
+          if (cb_s[mid] <= v) lo = mid; else hi = mid - 1;
+        }
+        c = g.c_first + lo;
+      } else {
+        c = colour_of_chunk(g, v);
       }
-      c = g.c_first + lo;
-    } else {
-      c = colour_of_chunk(g, v);
     }
     const int64_t k = v - begin;
+    const int64_t cstart = live ? (in_smem ? cb_s[c - g.c_first] : g.cols[c].chunk_begin) : -1;
     const int64_t cend =
         (c + 1 < g.c_first + g.c_count ? (in_smem ? cb_s[c + 1 - g.c_first] : g.cols[c + 1].chunk_begin) : end) -
         begin;
-    const int64_t trow = rec.row[2 * k + 1];
-    if (trow >= 0) {
-      const int64_t stop = chain_stop(rec.cont, k + 1, cend);
-      const int64_t last = stop < cend ? stop : cend - 1;
-      for (int64_t j = lane; j < W; j += 32) {
-        const double sum = chain_sum(rec.val[(2 * k + 1) * W + j], rec.val + j, 2 * W, k + 1, last);
-        if (stop < cend) out[trow * W + j] = sum;
-        else col.tail_val[c * W + j] = sum;
+    const int64_t trow = live ? rec.row[2 * k + 1] : -1;
+    const int64_t hrow = live ? rec.row[2 * k] : -1;
+    const bool has_next = k + 1 < cend;
+    const int next_cont = trow >= 0 && has_next ? rec.cont[k + 1] : 0;
+    const bool fast = trow >= 0 && next_cont == 0;
+    if (fast) {  // tail + next head (or the colour's tail record), in this lane
+      const double* t = rec.val + (2 * k + 1) * W;
+      const double* h = rec.val + (2 * k + 2) * W;
+      double* o = has_next ? out + trow * W : col.tail_val + c * W;
+      if (vec2 && has_next) {  // (the colour tail records are 8-byte aligned only)
+        for (int64_t j = 0; j < W; j += 2) {
+          double2 a = *reinterpret_cast<const double2*>(t + j);
+          const double2 b = *reinterpret_cast<const double2*>(h + j);
+          a.x += b.x;
+          a.y += b.y;
+          *reinterpret_cast<double2*>(o + j) = a;
+        }
+      } else {
+        for (int64_t j = 0; j < W; j++) o[j] = has_next ? t[j] + h[j] : t[j];
       }
-      if (stop >= cend && lane == 0) col.tail_row[c] = trow;
+      if (!has_next) col.tail_row[c] = trow;
     }
-    const int64_t hrow = rec.row[2 * k];
-    if (v == (in_smem ? cb_s[c - g.c_first] : g.cols[c].chunk_begin) && hrow >= 0) {
-      const int64_t stop = rec.cont[k] == 0 ? k : chain_stop(rec.cont, k + 1, cend);
-      const int64_t last = stop < cend ? stop : cend - 1;
-      int64_t* pack = col.head_pack + c * (W + 2);
-      for (int64_t j = lane; j < W; j += 32) {
-        reinterpret_cast<double*>(pack)[2 + j] = chain_sum(0.0, rec.val + j, 2 * W, k, last);
+    unsigned slow = __ballot_sync(FULL, (trow >= 0 && !fast) || (v == cstart && hrow >= 0));
+    while (slow) {
+      const int src = __ffs(slow) - 1;
+      slow &= slow - 1;
+      const int64_t kk = __shfl_sync(FULL, k, src), cc = __shfl_sync(FULL, c, src);
+      const int64_t ce = __shfl_sync(FULL, cend, src);
+      const int64_t tr = __shfl_sync(FULL, trow, src), hr = __shfl_sync(FULL, hrow, src);
+      const bool tslow = __shfl_sync(FULL, (int)(trow >= 0 && !fast), src) != 0;
+      const bool cs = __shfl_sync(FULL, (int)(v == cstart), src) != 0;
+      if (tslow) {
+        const int64_t stop = chain_stop(rec.cont, kk + 1, ce);
+        const int64_t last = stop < ce ? stop : ce - 1;
+        for (int64_t j = lane; j < W; j += 32) {
+          const double sum = chain_sum(rec.val[(2 * kk + 1) * W + j], rec.val + j, 2 * W, kk + 1, last);
+          if (stop < ce) out[tr * W + j] = sum;
+          else col.tail_val[cc * W + j] = sum;
+        }
+        if (stop >= ce && lane == 0) col.tail_row[cc] = tr;
       }
-      if (lane == 0) {
-        pack[0] = hrow;
-        pack[1] = stop < cend ? 0 : 1;
+      if (cs && hr >= 0) {
+        const int64_t stop = rec.cont[kk] == 0 ? kk : chain_stop(rec.cont, kk + 1, ce);
+        const int64_t last = stop < ce ? stop : ce - 1;
+        int64_t* pack = col.head_pack + cc * (W + 2);
+        for (int64_t j = lane; j < W; j += 32)
+          reinterpret_cast<double*>(pack)[2 + j] = chain_sum(0.0, rec.val + j, 2 * W, kk, last);
+        if (lane == 0) {
+          pack[0] = hr;
+          pack[1] = stop < ce ? 0 : 1;
+        }
       }
     }
   }
@@ -1268,7 +1309,8 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   {
     static int grid = 0;
     if (!grid) grid = occupancy_grid(ctx, k_chunk_fixup);
-    k_chunk_fixup<<<grid, kBlock, 0, s>>>(g, rec, col, a.out);
+    const int vec2 = W % 2 == 0 && reinterpret_cast<uintptr_t>(a.out) % 16 == 0;
+    k_chunk_fixup<<<grid, kBlock, 0, s>>>(g, rec, col, a.out, vec2);
     SPD_CHECK_LAUNCH();
     launches++;
   }
