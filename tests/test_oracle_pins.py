@@ -45,6 +45,22 @@ def test_reference_own_suite_pins_the_build():
     assert r.stderr.count("CHECK FAILED") == 1
 
 
+@pytest.mark.skipif(not HAVE_REF_SRC and not os.path.exists(
+    os.path.join(os.path.dirname(ob.REF_TESTS), "dspar_ref_tests_fastpart")), reason="reference sources absent")
+def test_reference_suite_with_the_fast_partition_class():
+    """integration/partition_fast.cpp (the drop-in's dspar::Partition: sorted
+    input kept, disjointness from spans) under the reference's own 64-case
+    suite: the same single documented failure as the reference build."""
+    exe = os.path.join(os.path.dirname(ob.REF_TESTS), "dspar_ref_tests_fastpart")
+    if HAVE_REF_SRC:
+        ob.ensure_built(ref=True)
+        subprocess.run(["make", "-C", os.path.dirname(os.path.dirname(exe)), "-j8", exe], check=True,
+                       stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert "test cases: 64 | failed: 1 | checks: 1886 | failed checks: 1" in r.stdout, r.stdout + r.stderr
+    assert "test_planner.cpp:233" in r.stderr
+
+
 # ------------------------------------------------------------ partitions
 def test_divide_bounds_kat():
     # test_planner.cpp:66-73
@@ -195,3 +211,47 @@ def test_restatement_matches_dense_eval(kernel):
                     full[i, B.levels[1].crd[f]] = out[f]
         out = full
     assert np.array_equal(out.reshape(dims), dense)
+
+
+FASTPART_LIB = os.path.join(os.path.dirname(ob.REF_LIB), "libdspar_fastpart.so")
+
+
+@pytest.mark.skipif(not HAVE_REF_SRC and not os.path.exists(FASTPART_LIB), reason="reference sources absent")
+@pytest.mark.parametrize("kernel", ["spmv", "spmm", "sddmm", "spttv", "spmttkrp", "spadd3"])
+@pytest.mark.parametrize("schedule", ["row", "nonzero"])
+def test_fast_partition_gives_the_same_plan(kernel, schedule):
+    """The reference pipeline with integration/partition_fast.cpp renders the
+    same plan, bundles the same subsets (every tensor, level, region and
+    colour) with the same disjointness, and executes to the same output and
+    Stats as the reference library, over random instances and 1-7 colours."""
+    import oracle_exec as OX
+
+    if HAVE_REF_SRC:
+        ob.ensure_built(ref=True)
+        subprocess.run(["make", "-C", os.path.dirname(os.path.dirname(FASTPART_LIB)), "-j8", FASTPART_LIB],
+                       check=True, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+    if kernel == "spadd3" and schedule == "nonzero":
+        pytest.skip("SpAdd3 takes a row split only (schedule.cpp:334-336)")
+    spec = K.KERNELS[kernel]
+    sched = K.ROW if schedule == "row" else spec["nonzero"]
+    rng = np.random.default_rng(hash((kernel, schedule)) % 2**32)
+    for trial in range(6):
+        tensors = K.instance(kernel, rng)
+        pieces = int(rng.integers(1, 8))
+        args = (spec["expr"], sched, pieces, spec["formats"][OX.OUTPUT[kernel]], OX.ref_inputs(kernel, tensors))
+        a = ob.RefRun(*args).ok()
+        b = ob.RefRun(*args, lib=FASTPART_LIB).ok()
+        assert a.L.ref_rendered_plan(a.h) == b.L.ref_rendered_plan(b.h)
+        for name, t in tensors.items():
+            assert a.L.ref_bundle_disjoint(a.h, 0, name.encode()) == b.L.ref_bundle_disjoint(b.h, 0, name.encode())
+            for lvl in range(len(t.levels)):
+                for region in ("dom", "pos", "crd", "vals"):
+                    for c in range(pieces):
+                        sa, sb = a.subset(name, lvl, region, c), b.subset(name, lvl, region, c)
+                        assert (sa is None and sb is None) or np.array_equal(sa, sb), (name, lvl, region, c)
+        assert a.stats() == b.stats()
+        la, va = a.output()
+        lb, vb = b.output()
+        assert np.array_equal(va, vb)
+        for (ka, pa, ca), (kb, pb, cb) in zip(la, lb):
+            assert ka == kb and (pa is None or (np.array_equal(pa, pb) and np.array_equal(ca, cb)))
