@@ -380,6 +380,74 @@ def main():
         A.close()
         for d in devs.values():
             d.close()
+    # Uneven colour blocks (spd_context_set_colour_blocks): P = 5 x world
+    # colours, each GPU a contiguous block of a different size; the leaf ops on
+    # the whole matrix and on a piece placed by the blocks, SpAdd3 by blocks.
+    from paper_2207_13901_b200.distributed import block_owned_rows
+    P = 5 * world
+    rng = np.random.default_rng(2024)
+    costs = rng.uniform(0.2, 3.0, P)
+    bounds = H.split_colour_blocks(costs, world)
+    n, m = 3000, 2500
+    rows = np.concatenate([np.full(25000, 13), rng.integers(0, n, 60000)])
+    cols = rng.integers(0, m, rows.shape[0])
+    B = H.SparseTensor.pack((n, m), H.parse_format("ds"), np.stack([rows, cols], 1),
+                            rng.integers(1, 5, rows.shape[0]).astype(float))
+    rp = B.levels[1].rowptr()
+    Cm = K.dense(rng, (m, 32), "dd", True)
+    cv = K.dense(rng, (m,), "d", True)
+    Cd, cd = torch.from_numpy(Cm.vals).to(dev), torch.from_numpy(cv.vals).to(dev)
+    H.set_colour_blocks(ctx, P, bounds)
+    first, count = int(bounds[rank]), int(bounds[rank + 1] - bounds[rank])
+    Bd = H.DeviceTensor.upload(ctx, B)
+    whole = H.DeviceTensor.upload(ctx, B) if rank == 0 else None
+    piece, _ = H.DeviceTensor.place(ctx, whole, (n, m), H.parse_format("ds"), "nonzero")
+    for schedule in ("nonzero", "row"):
+        for name, T in (("whole", Bd), ("placed", piece)):
+            if name == "placed" and schedule == "row":
+                continue  # the piece follows the nonzero blocks
+            cols_ = H.partition_universe(ctx, T, P) if schedule == "row" else H.partition_nonzero(ctx, T, 1, P)
+            own = block_owned_rows(owned_rows(cols_, rp, schedule, n), bounds)
+            for kernel, width in (("spmm", 32), ("spmv", 1)):
+                out = torch.zeros(n * width, dtype=torch.float64, device=dev)
+                if kernel == "spmm":
+                    H.spmm(ctx, T, Cd, 32, out, first=first, count=count, pieces=P)
+                else:
+                    H.spmv(ctx, T, cd, out, first=first, count=count, pieces=P)
+                gathered = [torch.zeros_like(out) for _ in range(world)]
+                dist.all_gather(gathered, out)
+                if rank == 0:
+                    got = assemble([x.cpu().numpy() for x in gathered], own, width, n)
+                    t = {"B": B, "C": Cm} if kernel == "spmm" else {"B": B, "c": cv}
+                    want = np.asarray(oracle_exec.oracle_execute(kernel, t, schedule, P)["out"]).reshape(n, width)
+                    ok = np.array_equal(got, want)
+                    print(f"[mgpu world={world}] blocks {[int(b) for b in bounds]} {name} {kernel} {schedule}: "
+                          f"{'OK' if ok else 'MISMATCH'}", flush=True)
+                    failures += 0 if ok else 1
+    # SpAdd3 over the blocks of a row split
+    D2 = H.SparseTensor.pack((n, m), H.parse_format("ds"), np.stack([rows, (cols + 1) % m], 1),
+                             rng.integers(1, 5, rows.shape[0]).astype(float))
+    D3 = H.SparseTensor.pack((n, m), H.parse_format("ds"), np.stack([rows, (cols + 2) % m], 1),
+                             rng.integers(1, 5, rows.shape[0]).astype(float))
+    d2, d3 = H.DeviceTensor.upload(ctx, D2), H.DeviceTensor.upload(ctx, D3)
+    H.partition_universe(ctx, Bd, P)
+    A, _ = H.spadd3(ctx, Bd, d2, d3, first=first, count=count, pieces=P)
+    F = A.gather_rows(0)
+    if rank == 0:
+        g = F.download()
+        want = oracle_exec.oracle_execute("spadd3", {"B": B, "C": D2, "D": D3}, "row", P)["out"]
+        ok = (np.array_equal(g.levels[1].rowptr(), want[0]) and np.array_equal(g.levels[1].crd, want[1]) and
+              np.array_equal(g.vals, want[2]))
+        print(f"[mgpu world={world}] blocks {[int(b) for b in bounds]} spadd3 row: {'OK' if ok else 'MISMATCH'}", flush=True)
+        failures += 0 if ok else 1
+        F.close()
+    A.close()
+    for d in (d2, d3, Bd, piece):
+        d.close()
+    if whole is not None:
+        whole.close()
+    H.set_colour_blocks(ctx, P, None)
+
     ctx.close()
     dist.destroy_process_group()
     if rank == 0:
