@@ -27,8 +27,14 @@ namespace spd {
 // the next non-empty colour's first row -- and numbers the chunks (prefix
 // sum); O(log P) block steps up to 1024 colours, a serial pass above.
 __global__ void k_setup_rows(DevColor* __restrict__ cols, int64_t P, int split, int out_level,
-                             const int64_t* __restrict__ R, int64_t nrows) {
-  const int64_t c = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+                             const int64_t* __restrict__ R, int64_t nrows, int64_t* __restrict__ counters,
+                             int64_t* __restrict__ ff0, int64_t n0, int64_t* __restrict__ ff1, int64_t n1) {
+  // the call's scratch: combines / ticket counters zeroed, record slots -1
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  if (tid == 0) counters[0] = 0, counters[3] = 0;
+  for (int64_t i = tid; i < n0; i += nt) ff0[i] = -1;
+  for (int64_t i = tid; i < n1; i += nt) ff1[i] = -1;
+  const int64_t c = tid >> 5;
   if (c >= P) return;
   const spd_color pc = cols[c].pub;
   int64_t wl = 1, wh = 0;
@@ -138,8 +144,10 @@ __global__ void __launch_bounds__(kSetupMax) k_setup(DevColor* __restrict__ cols
 }
 
 void launch_setup(cudaStream_t s, DevColor* cols, int64_t P, int split, int out_level, const int64_t* R,
-                  int64_t nrows, int64_t CH, int64_t c_first, int64_t c_count, int64_t* counters) {
-  k_setup_rows<<<(unsigned)ceil_div(P * 32, 256), 256, 0, s>>>(cols, P, split, out_level, R, nrows);
+                  int64_t nrows, int64_t CH, int64_t c_first, int64_t c_count, int64_t* counters, int64_t* ff0,
+                  int64_t n0, int64_t* ff1, int64_t n1) {
+  const int64_t blocks = std::max<int64_t>(ceil_div(P * 32, 256), std::min<int64_t>(ceil_div(n0 + n1, 256), 148));
+  k_setup_rows<<<(unsigned)blocks, 256, 0, s>>>(cols, P, split, out_level, R, nrows, counters, ff0, n0, ff1, n1);
   SPD_CHECK_LAUNCH();
   k_setup<<<1, kSetupMax, 0, s>>>(cols, P, split, nrows, CH, c_first, c_count, counters);
   SPD_CHECK_LAUNCH();
@@ -1105,12 +1113,9 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
   int64_t launches = 0;
   if (stats) SPD_CUDA(cudaEventRecord(ctx->ev0, s));
   trace_mark(ctx);
-  SPD_CUDA(cudaMemsetAsync(col.head_pack, 0xff, sizeof(int64_t) * pack_slots * (W + 2), s));
-  SPD_CUDA(cudaMemsetAsync(col.counters, 0, sizeof(int64_t) * 4, s));
-  SPD_CUDA(cudaMemsetAsync(col.tail_row, 0xff, sizeof(int64_t) * P, s));
   ht.mark("scratch");
   launch_setup(s, (DevColor*)ctx->colors_dev.ptr, P, (int)ctx->split, out_level, g.R, g.nrows, g.CH, first, count,
-               col.counters);
+               col.counters, col.head_pack, pack_slots * (W + 2), col.tail_row, P);
   launches += 2;
 
   const spd_level_store& leaf = B->levels[nl - 1];
@@ -1405,7 +1410,7 @@ int spd_colour_costs(spd_context* ctx, const spd_tensor* t, int64_t* positions, 
     int64_t* cnt = (int64_t*)ctx->scratch[6].reserve(sizeof(int64_t) * (P + 4));
     // W_c as the row-reducing ops store them, then the non-empty rows in W_c
     launch_setup(s, (DevColor*)ctx->colors_dev.ptr, P, (int)ctx->split, 0, L.rowptr, L.parent_positions, 1024, 0,
-                 P, cnt + P);
+                 P, cnt + P, nullptr, 0, nullptr, 0);
     NzView z = nz_view(ctx, const_cast<spd_tensor*>(t), L.rowptr, L.parent_positions);
     k_colour_nonempty<<<(unsigned)ceil_div(P * 32, 256), 256, 0, s>>>((const DevColor*)ctx->colors_dev.ptr, P, z,
                                                                      cnt);

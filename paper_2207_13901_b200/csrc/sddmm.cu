@@ -19,7 +19,8 @@ namespace spd {
 #define FULL 0xffffffffu
 
 void launch_setup(cudaStream_t s, DevColor* cols, int64_t P, int split, int out_level, const int64_t* R,
-                  int64_t nrows, int64_t CH, int64_t c_first, int64_t c_count, int64_t* counters);
+                  int64_t nrows, int64_t CH, int64_t c_first, int64_t c_count, int64_t* counters, int64_t* ff0,
+                  int64_t n0, int64_t* ff1, int64_t n1);
 
 bool sddmm_nz_launch(spd_context* ctx, const spd_tensor* B, const WalkGeom& g, const double* C,
                      const double* D, int64_t K, int64_t dk, int64_t dj, double* Avals,
@@ -133,8 +134,8 @@ static void run_sddmm(spd_context* ctx, const spd_tensor* B, const double* C, co
   cudaStream_t s = ctx->stream;
   int64_t launches = 0;
   if (stats) SPD_CUDA(cudaEventRecord(ctx->ev0, s));
-  SPD_CUDA(cudaMemsetAsync(counters, 0, sizeof(int64_t) * 4, s));
-  launch_setup(s, (DevColor*)ctx->colors_dev.ptr, P, (int)ctx->split, 0, g.R, g.nrows, g.CH, first, count, counters);
+  launch_setup(s, (DevColor*)ctx->colors_dev.ptr, P, (int)ctx->split, 0, g.R, g.nrows, g.CH, first, count, counters,
+               nullptr, 0, nullptr, 0);
   launches += 2;
   const int64_t kt = ceil_div(K > 0 ? K : 1, 32);
   leaf_timing_begin(ctx);
