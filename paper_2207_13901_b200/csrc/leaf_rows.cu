@@ -535,13 +535,14 @@ __device__ __forceinline__ int64_t chain_stop(const int* __restrict__ cont, int6
 
 constexpr int kFixupColours = 1024;  // colours whose chunk starts the fixup keeps in shared memory
 
-// One warp per 32 consecutive chunks, a lane per chunk: the common case -- a
+// One warp per 8 consecutive chunks, 4 lanes per chunk: the common case -- a
 // tail record whose row ends in the next chunk (or at the colour's end) --
-// is summed by its own lane (tail + the next chunk's head, vectorised over
-// the row's W values), so the records of 32 chunks are in flight together;
-// rows spanning several chunks and colour-start head records go through the
-// warp-cooperative chain sums, one chunk at a time.  `vec2`: W even and the
-// output 16-byte aligned.
+// is summed by its own 4 lanes (tail + the next chunk's head, 16-byte pairs
+// interleaved over the row's W values), so the records of 8 chunks are in
+// flight together; rows spanning several chunks and colour-start head
+// records go through the warp-cooperative chain sums, one chunk at a time
+// (few per warp: hub-dense stretches of the matrix put several in a group).
+// `vec2`: W even and the output 16-byte aligned.
 __global__ void __launch_bounds__(kBlock) k_chunk_fixup(WalkGeom g, ChunkRecs rec, ColorRecs col,
                                                         double* __restrict__ out, int vec2) {
   // the chunk starts of this GPU's colours, so a chunk's colour is a search
@@ -556,8 +557,9 @@ __global__ void __launch_bounds__(kBlock) k_chunk_fixup(WalkGeom g, ChunkRecs re
   const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t W = g.W;
-  for (int64_t v0 = begin + gw * 32; v0 < end; v0 += nw * 32) {
-    const int64_t v = v0 + lane;
+  const int sub = lane & 3;  // 4 lanes per chunk, 8 chunks per warp
+  for (int64_t v0 = begin + gw * 8; v0 < end; v0 += nw * 8) {
+    const int64_t v = v0 + (lane >> 2);
     const bool live = v < end;
     int64_t c = g.c_first;
     if (live) {
@@ -582,24 +584,30 @@ __global__ void __launch_bounds__(kBlock) k_chunk_fixup(WalkGeom g, ChunkRecs re
     const bool has_next = k + 1 < cend;
     const int next_cont = trow >= 0 && has_next ? rec.cont[k + 1] : 0;
     const bool fast = trow >= 0 && next_cont == 0;
-    if (fast) {  // tail + next head (or the colour's tail record), in this lane
+    if (fast) {  // tail + next head (or the colour's tail record): 4 lanes, interleaved 16-byte pairs
       const double* t = rec.val + (2 * k + 1) * W;
       const double* h = rec.val + (2 * k + 2) * W;
       double* o = has_next ? out + trow * W : col.tail_val + c * W;
       if (vec2 && has_next) {  // (the colour tail records are 8-byte aligned only)
-        for (int64_t j = 0; j < W; j += 2) {
-          double2 a = *reinterpret_cast<const double2*>(t + j);
-          const double2 b = *reinterpret_cast<const double2*>(h + j);
-          a.x += b.x;
-          a.y += b.y;
-          *reinterpret_cast<double2*>(o + j) = a;
+        for (int64_t j0 = 2 * sub; j0 < W; j0 += 32) {
+          double2 a[4], b[4];
+#pragma unroll
+          for (int i = 0; i < 4; i++)
+            if (j0 + 8 * i < W) {
+              a[i] = __ldg(reinterpret_cast<const double2*>(t + j0 + 8 * i));
+              b[i] = __ldg(reinterpret_cast<const double2*>(h + j0 + 8 * i));
+            }
+#pragma unroll
+          for (int i = 0; i < 4; i++)
+            if (j0 + 8 * i < W)
+              *reinterpret_cast<double2*>(o + j0 + 8 * i) = make_double2(a[i].x + b[i].x, a[i].y + b[i].y);
         }
       } else {
-        for (int64_t j = 0; j < W; j++) o[j] = has_next ? t[j] + h[j] : t[j];
+        for (int64_t j = sub; j < W; j += 4) o[j] = has_next ? __ldg(t + j) + __ldg(h + j) : __ldg(t + j);
       }
-      if (!has_next) col.tail_row[c] = trow;
+      if (!has_next && sub == 0) col.tail_row[c] = trow;
     }
-    unsigned slow = __ballot_sync(FULL, (trow >= 0 && !fast) || (v == cstart && hrow >= 0));
+    unsigned slow = __ballot_sync(FULL, sub == 0 && ((trow >= 0 && !fast) || (v == cstart && hrow >= 0)));
     while (slow) {
       const int src = __ffs(slow) - 1;
       slow &= slow - 1;
