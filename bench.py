@@ -510,10 +510,11 @@ def main():
     # ---- the other BASELINE configs, same run (one colour per GPU) ----
     configs = {}
     cfg = [c for c in args.configs.split(",") if c]
+    Bblk = None
     if blocks is not None:
         H.set_colour_blocks(ctx, pieces, None)
-        if cfg:  # B re-placed by the one-colour-per-GPU split the configs run
-            Bstep.close()
+        if cfg:  # B re-placed by the one-colour-per-GPU split; SpMV keeps the balanced piece
+            Bblk = Bstep
             Bstep, _ = place_B()
     if cfg:
         sys.path.insert(0, os.path.join(ROOT, "scripts"))
@@ -543,6 +544,7 @@ def main():
             return outs
 
         rm = {"n": n, "scale": args.scale, "rp_d": rp_d, "crd_d": crd_d, "vals_d": vals_d, "Bstep": Bstep,
+              "blocks": None if Bblk is None else (Bblk, pieces, blocks),
               "host": host_B, "dense": lambda count, seed: dense_vals(count, seed),
               "gen": lambda sc: rmat_csr(sc, args.edge_factor, args.seed), "spadd3_inputs": spadd3_inputs}
         for name in cfg:
@@ -563,6 +565,8 @@ def main():
             torch.cuda.empty_cache()
             if rank == 0:
                 print(f"[bench] config {name}: {time.time() - t0:.1f} s", file=sys.stderr, flush=True)
+        if Bblk is not None:
+            Bblk.close()
 
     # ---- DRAM traffic of the headline leaf: one ncu pass in a child process ----
     traffic = None

@@ -334,6 +334,12 @@ def config_spmv_rmat(env, H, rm, x_seed):
     x_d = env.bcast(rm["dense"](n, x_seed) if env.rank == 0 else np.empty(0), torch.float64)
     y_d = torch.empty(n, dtype=torch.float64, device=env.dev)
     first, count, P = env.colours()
+    if rm.get("blocks") is not None:
+        # the headline's over-decomposed nonzero split and its cost-balanced
+        # colour blocks (B placed by them), reused for the SpMV of the same matrix
+        Bstep, P, bounds = rm["blocks"]
+        H.set_colour_blocks(env.ctx, P, bounds)
+        first, count = int(bounds[env.rank]), int(bounds[env.rank + 1] - bounds[env.rank])
 
     def step():
         H.partition_nonzero(env.ctx, Bstep, 1, P, host=False)
@@ -343,7 +349,8 @@ def config_spmv_rmat(env, H, rm, x_seed):
     flops = 2.0 * nnz
     by = 8 * (n + 1) + 16 * nnz + 8 * n + 8 * n
     out = {"workload": f"SpMV a(i)=B(i,j)*c(j) on the C2 R-MAT (scale {rm['scale']}, {nnz} nnz), nonzero split "
-                       f"into {P} colour(s)",
+                       f"into {P} colour(s)" + ("" if rm.get("blocks") is None else
+                                                 ", the headline's cost-balanced block of them per GPU"),
            "value": flops / (ms * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ms, "gpu_launches": nl,
            "roofline": roofline(env, by / env.world, leaf, "k_spmv_win<6,int> over compacted columns"),
            "effective_gbs": by / (ms * 1e-3) / 1e9}
@@ -363,6 +370,8 @@ def config_spmv_rmat(env, H, rm, x_seed):
             return y1
 
         out["multi_gpu_check"] = mgpu_check(env, H, y_d, 1, H.last_owned(env.ctx, first, count), ref)
+    if rm.get("blocks") is not None:
+        H.set_colour_blocks(env.ctx, P, None)
     if env.world == 1:
         rp, crd, vals = rm["host"]
         rs, nbytes, st = _restager(env, H, (n, n), H.parse_format("ds"), [rp], [crd], vals)
