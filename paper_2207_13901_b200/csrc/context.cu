@@ -1332,15 +1332,12 @@ int spd_context_colour_blocks(spd_context* ctx, int64_t pieces, int64_t* bounds)
     checked(ctx);
     if (!bounds) throw ValidationError("null argument");
     if (pieces < 1) throw ValidationError("pieces must be positive");
-    const int64_t saved = ctx->pieces;
-    ctx->pieces = pieces;  // the blocks a partition of `pieces` colours would get
-    for (int r = 0; r < ctx->world; r++) {
+    for (int r = 0; r < ctx->world; r++) {  // the blocks a partition of `pieces` colours gets
       int64_t f, c;
-      colour_block(ctx, r, f, c);
+      colour_block(ctx, pieces, r, f, c);
       bounds[r] = f;
     }
     bounds[ctx->world] = pieces;
-    ctx->pieces = saved;
   });
 }
 
