@@ -10,6 +10,7 @@
 // order within a row; this backend reassociates that sum (FMA, chunk and
 // colour partials), which north_star allows within 1e-10 relative.
 #include <algorithm>
+#include <mutex>
 #include <cstdlib>
 #include <cub/cub.cuh>
 
@@ -1224,12 +1225,22 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
       const int32_t* c32 = crd32_index(ctx, const_cast<spd_tensor*>(B));
       constexpr int kS = 4, kMinB = 3;
       const int smem = (kBlock / 32) * kS * 8 * 16 * (int)sizeof(double2);
+      // the dynamic shared-memory opt-in is a per-device function attribute:
+      // set once on every device a context of this process uses (the
+      // drop-in runs one host thread per GPU)
+      static std::mutex attr_mu;
+      static uint64_t attr_done = 0;
       static int grid = 0;
-      if (!grid) {
-        SPD_CUDA(cudaFuncSetAttribute(k_spmm32_nz<kS, kMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        int per_sm = 0;
-        SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmm32_nz<kS, kMinB>, kBlock, smem));
-        grid = ctx->num_sms * (per_sm > 0 ? per_sm : 1);
+      {
+        std::lock_guard<std::mutex> lk(attr_mu);
+        const uint64_t bit = uint64_t(1) << (ctx->device & 63);
+        if (!(attr_done & bit)) {
+          SPD_CUDA(cudaFuncSetAttribute(k_spmm32_nz<kS, kMinB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+          int per_sm = 0;
+          SPD_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_spmm32_nz<kS, kMinB>, kBlock, smem));
+          grid = ctx->num_sms * (per_sm > 0 ? per_sm : 1);
+          attr_done |= bit;
+        }
       }
       k_spmm32_nz<kS, kMinB><<<grid, kBlock, smem, s>>>(g, z, c32, B->vals, a.x, a.out, rec, col.counters);
     } else {  // SpMV / SpTTV: the windowed row reduction

@@ -210,7 +210,10 @@ def test_every_visible_gpu_gives_the_one_gpu_result(gpu_lib, kernel):
     sched = spec["nonzero"] or ROW
     rng = np.random.default_rng(31)
     for pieces in (3, 5):
-        t = K.instance(kernel, rng, integers=True)
+        # SpMM and SpMTTKRP at width / rank 32 too: their leaves opt in to
+        # dynamic shared memory, a per-device attribute every GPU must get
+        rank = 32 if pieces == 5 and kernel in ("spmm", "spmttkrp") else None
+        t = K.instance(kernel, rng, integers=True, rank=rank)
         args = (spec["expr"], sched, pieces, spec["formats"][OUTPUT[kernel]], ref_inputs(kernel, t))
         want = ob.RefRun(*args, mode="par", use_placements=True).ok()
         outs = []
