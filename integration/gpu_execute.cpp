@@ -28,6 +28,7 @@
 #include <exception>
 #include <thread>
 #include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -52,10 +53,62 @@ void check(int st) {
   throw std::runtime_error(msg);
 }
 
+// Contexts (stream, events, scratch, NCCL communicator) live for the process:
+// one per device for the single-GPU paths, one group per GPU count for the
+// multi-GPU path, so repeated execute() calls do not re-create streams or
+// re-initialise NCCL.  Ctx is a non-owning handle on a cached context.
+std::mutex g_ctx_mu;
+std::map<int, spd_context*> g_single;                    // device -> context
+std::map<int, std::vector<spd_context*>> g_groups;       // GPU count -> contexts with a communicator
+
+spd_context* single_context(int device) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  auto it = g_single.find(device);
+  if (it != g_single.end()) return it->second;
+  spd_context* h = nullptr;
+  check(spd_context_create(device, nullptr, &h));
+  g_single[device] = h;
+  return h;
+}
+
+// The G contexts of a multi-GPU execute (device r = rank r), created once:
+// the ranks initialise the communicator together, one host thread each.
+std::vector<spd_context*> group_contexts(int G) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  auto it = g_groups.find(G);
+  if (it != g_groups.end()) return it->second;
+  std::vector<unsigned char> uid(128, 0);
+  check(spd_nccl_unique_id(uid.data()));
+  std::vector<spd_context*> cs(G, nullptr);
+  std::vector<std::exception_ptr> errors(G);
+  std::vector<std::thread> pool;
+  for (int r = 0; r < G; r++)
+    pool.emplace_back([&, r] {
+      try {
+        check(spd_context_create(r, nullptr, &cs[r]));
+        check(spd_context_init_comm(cs[r], uid.data(), r, G));
+      } catch (...) {
+        errors[r] = std::current_exception();
+      }
+    });
+  for (auto& t : pool) t.join();
+  for (auto& e : errors)
+    if (e) std::rethrow_exception(e);
+  g_groups[G] = cs;
+  return cs;
+}
+
+// A failed multi-GPU call may leave a communicator mid-collective: its group
+// is not reused (the next call builds a fresh one).
+void drop_group(int G) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  g_groups.erase(G);
+}
+
 struct Ctx {
   spd_context* h = nullptr;
-  explicit Ctx(int device = 0) { check(spd_context_create(device, nullptr, &h)); }
-  ~Ctx() { spd_context_destroy(h); }
+  explicit Ctx(int device = 0) : h(single_context(device)) {}
+  explicit Ctx(spd_context* c) : h(c) {}
 };
 
 struct DevTensor {
@@ -436,7 +489,7 @@ static int gpus_for(int64_t pieces) {
 // backend -- and the copy of the output ranges it owns into `out`.
 struct GpuPart {
   int device = 0, rank = 0, world = 1;
-  const void* uid = nullptr;
+  spd_context* ctx = nullptr;  // the GPU's cached context (with its communicator when world > 1)
   int64_t first = 0, count = 0;
   std::vector<int64_t> work;
   int64_t combines = 0;
@@ -451,8 +504,7 @@ static void run_part(const Plan& plan, const TensorSet& tensors, const std::stri
   const std::string b_name = terms[0][0].tensor;
   const SparseTensor& Bt = tensors.at(b_name);
   const int64_t P = loop.pieces;
-  Ctx ctx(g.device);
-  if (g.world > 1) check(spd_context_init_comm(ctx.h, g.uid, g.rank, g.world));
+  Ctx ctx(g.ctx ? g.ctx : single_context(g.device));
   DevTensor B;
   upload(ctx, Bt, B);
   std::vector<spd_color> cols(P);
@@ -557,12 +609,12 @@ ExecResult execute_gpu(const Plan& plan, const TensorSet& tensors, const Machine
   const int G = gpus_for(P);
   const int64_t cmax = (P + G - 1) / G;
   std::vector<GpuPart> parts(G);
-  std::vector<unsigned char> uid(128, 0);
-  if (G > 1) check(spd_nccl_unique_id(uid.data()));
+  const std::vector<spd_context*> group = G > 1 ? group_contexts(G) : std::vector<spd_context*>{};
   const SparseTensor& outstub = tensors.at(out_name);
   std::vector<double> out(kernel == "spadd3" ? 0 : static_cast<size_t>(outstub.leaf_count()), 0.0);
   for (int r = 0; r < G; r++) {
-    parts[r].device = r, parts[r].rank = r, parts[r].world = G, parts[r].uid = uid.data();
+    parts[r].device = r, parts[r].rank = r, parts[r].world = G;
+    parts[r].ctx = G > 1 ? group[r] : nullptr;
     parts[r].first = r * cmax;
     parts[r].count = std::min<int64_t>(cmax, P - r * cmax);
   }
@@ -582,7 +634,10 @@ ExecResult execute_gpu(const Plan& plan, const TensorSet& tensors, const Machine
       });
     for (auto& t : pool) t.join();
     for (auto& e : errors)
-      if (e) std::rethrow_exception(e);
+      if (e) {
+        drop_group(G);
+        std::rethrow_exception(e);
+      }
   }
   SparseTensor result;
   if (kernel == "spadd3") {
