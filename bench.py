@@ -667,8 +667,8 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
     1/N block of C from pinned memory, NCCL all-gather of C over NVLink
     (spd_allgather), the partition step, the leaf + boundary combine, and D2H
     of the output rows this GPU owns.  Consecutive steps alternate between two
-    contexts on two streams, so step k+1's uploads overlap step k's leaf and
-    read-back (a stream of independent SpMM problems, double-buffered)."""
+    contexts on three streams, so the next steps' uploads overlap step k's leaf
+    and read-back (a stream of independent SpMM problems, triple-buffered)."""
     import ctypes as Cc
 
     import torch.distributed as dist
@@ -682,11 +682,13 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
     vals_h = vals_d.cpu().pin_memory()
     per = (n * N) // world
     C_h = C_d[rank * per:(rank + 1) * per].cpu().pin_memory()
-    # Two contexts (each with its own communicator at N > 1) on two streams:
-    # step k+1's uploads overlap step k's leaf and read-back.  Every rank
-    # issues its collectives in the same order, so the two communicators
+    # Three contexts (each with its own communicator at N > 1) on three
+    # streams: while one stream reads its output back (D2H, which orders
+    # before that stream's next uploads) the other two keep the H2D engine
+    # busy -- with two streams the H2D engine idled ~20% of every step.  Every
+    # rank issues its collectives in the same order, so the communicators
     # never wait on each other.
-    nbuf = 2 if os.environ.get("SPD_E2E_NBUF", "2") == "2" else 1
+    nbuf = max(1, int(os.environ.get("SPD_E2E_NBUF", "3")))
     streams = [torch.cuda.Stream(dev) for _ in range(nbuf)]
     ctxs = [H.Context(dev.index, stream=s.cuda_stream) for s in streams]
     if world > 1:
@@ -715,6 +717,10 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
         cx, s = ctxs[j], streams[j]
         tt = [time.perf_counter()]
         with torch.cuda.stream(s):
+            if trace:
+                ev = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+                state.setdefault("ev", []).append((state["k"], j, ev))
+                ev[4].record(s)
             if state["live"][j] is None:  # first use of this stream: upload
                 h = Cc.c_void_p()
                 if world == 1:  # spd_tensor_upload: the whole matrix
@@ -730,6 +736,8 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
                 NN.check(NN.lib().spd_tensor_restage(cx.h, Bs.h, pos_pp, crd_pp,
                                                      Cc.cast(vals_h.data_ptr(), NN.dblp)))
             tt.append(time.perf_counter())
+            if trace:
+                ev[0].record(s)
             C_devs[j][rank * per:(rank + 1) * per].copy_(C_h, non_blocking=True)
             if world > 1:
                 cx.allgather(C_devs[j], per * 8)
@@ -742,21 +750,29 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
                 H.partition_nonzero(cx, Bs, 1, pieces, host=False)
             lo, hi = state["owned"]
             tt.append(time.perf_counter())
+            if trace:
+                ev[1].record(s)
             H.spmm(cx, Bs, C_devs[j], N, A_devs[j], first=first, count=count, pieces=pieces, stats=False)
+            if trace:
+                ev[2].record(s)
             tt.append(time.perf_counter())
             key = "A_h%d" % j
             if key not in state:
                 state[key] = torch.empty(max(hi - lo + 1, 0) * N, dtype=torch.float64).pin_memory()
             if hi >= lo:
                 state[key].copy_(A_devs[j][lo * N:(hi + 1) * N], non_blocking=True)
+            if trace:
+                ev[3].record(s)
             tt.append(time.perf_counter())
         state["live"][j] = Bs
         if trace:
             print("e2e step", state["k"], "ms:", [round((b - a) * 1e3, 1) for a, b in zip(tt, tt[1:])],
                   file=sys.stderr)
 
-    one()  # warm both streams (allocator pools, communicators)
-    one()
+    # warm-up: every stream's first upload and first re-stage (allocator
+    # pools, staging buffers, communicators) happen before the timed steps
+    for _ in range(2 * nbuf):
+        one()
     for st in streams:
         st.synchronize()
     if world > 1:
@@ -768,6 +784,13 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
     for st in streams:
         st.synchronize()
     dt = (time.perf_counter() - t0) / args.e2e_steps
+    if trace and state.get("ev"):  # GPU timeline of every step: [C H2D, compute, A D2H] and gaps
+        base = state["ev"][0][2][4]
+        for k_, j_, ev in state["ev"]:
+            print(f"e2e gpu step {k_} stream {j_}: start {base.elapsed_time(ev[4]):.1f} restage "
+                  f"{ev[4].elapsed_time(ev[0]):.1f} C-h2d {ev[0].elapsed_time(ev[1]):.1f} compute "
+                  f"{ev[1].elapsed_time(ev[2]):.1f} A-d2h {ev[2].elapsed_time(ev[3]):.1f} end "
+                  f"{base.elapsed_time(ev[3]):.1f} ms", file=sys.stderr)
     plo, phi = state["live"][0].piece_span()
     for Bs in state["live"]:
         if Bs is not None:
@@ -793,7 +816,7 @@ def run_e2e(args, ctx, H, torch, dev, rank, world, n, nnz, rp_d, crd_d, vals_d, 
                     "later steps re-stage into the same device buffers (spd_tensor_restage, validated "
                     "on the GPU, derived indices rebuilt) -- its 1/N of C H2D + NCCL all-gather, the "
                     "partition step, leaf + combine, its owned output rows D2H; consecutive "
-                    "steps double-buffered on two streams; time = max over ranks, bytes = sum over "
+                    "steps triple-buffered on three streams; time = max over ranks, bytes = sum over "
                     "ranks"}
 
 
