@@ -666,3 +666,26 @@ def test_colour_costs_and_blocks(ctx, schedule, pieces):
         H.set_colour_blocks(ctx, pieces, None)
     finally:
         Bd.close()
+
+
+@pytest.mark.parametrize("pieces", [1023, 1024, 1025, 1600])
+@pytest.mark.parametrize("schedule", ["nonzero", "row"])
+def test_many_colours(ctx, pieces, schedule):
+    """Colour counts around the setup kernel's block-scan limit (1024; above
+    it the serial pass) and the fixup's shared-memory colour table: SpMV and
+    SpMM (N = 32) against the restatement, Stats included."""
+    from paper_2207_13901_b200.execute import execute
+    from paper_2207_13901_b200.host import SparseTensor, parse_format
+
+    rng = np.random.default_rng(pieces)
+    n, m = 3000, 400
+    rows = np.concatenate([np.full(2500, 11), rng.integers(0, n, 6000)])
+    cols = rng.integers(0, m, rows.shape[0])
+    B = SparseTensor.pack((n, m), parse_format("ds"), np.stack([rows, cols], 1),
+                          rng.integers(1, 5, rows.shape[0]).astype(float))
+    for kernel, t in (("spmv", {"B": B, "c": K.dense(rng, (m,), "d")}),
+                      ("spmm", {"B": B, "C": K.dense(rng, (m, 32), "dd")})):
+        want = oracle_execute(kernel, t, schedule, pieces)
+        out, st, _ = execute(kernel, t, schedule, pieces, ctx)
+        assert np.array_equal(np.asarray(out).reshape(-1), np.asarray(want["out"]).reshape(-1)), (kernel, schedule)
+        assert st.combines == want["combines"] and list(st.work) == list(want["work"])
