@@ -112,6 +112,13 @@ int spd_context_synchronize(spd_context* ctx);
 int spd_nccl_unique_id(void* out128);
 int spd_context_init_comm(spd_context* ctx, const void* unique_id128, int rank, int world);
 int spd_context_rank(const spd_context* ctx, int* rank, int* world);
+/* Aborts the context's communicator (ncclCommAbort): collectives this rank
+ * has queued stop waiting for their peers and the calls blocked on them
+ * return an error.  For a host that runs several ranks in one process (the
+ * drop-in's one thread per GPU): when one rank fails, abort the others'
+ * communicators instead of leaving them waiting.  The context stays usable
+ * without a communicator; destroy it afterwards. */
+int spd_context_abort(spd_context* ctx);
 /* In-place all-gather over the context's communicator (NVLink): rank r's
  * `bytes_per_rank` bytes at dev_buf + r*bytes_per_rank are gathered into every
  * rank's dev_buf.  Places a replicated dense operand (x / C / D) from a

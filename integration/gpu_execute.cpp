@@ -630,6 +630,10 @@ ExecResult execute_gpu(const Plan& plan, const TensorSet& tensors, const Machine
           run_part(plan, tensors, kernel, parts[r], out);
         } catch (...) {
           errors[r] = std::current_exception();
+          // the other GPUs may be waiting for this one in a collective:
+          // abort their communicators so every thread returns
+          for (int q = 0; q < G; q++)
+            if (q != r) spd_context_abort(group[q]);
         }
       });
     for (auto& t : pool) t.join();

@@ -49,6 +49,7 @@ SIGNATURES = {
     "spd_nccl_unique_id": (C.c_int, [vp]),
     "spd_context_init_comm": (C.c_int, [vp, vp, C.c_int, C.c_int]),
     "spd_context_rank": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "spd_context_abort": (C.c_int, [vp]),
     "spd_allgather": (C.c_int, [vp, vp, i64]),
     "spd_tensor_upload": (
         C.c_int,

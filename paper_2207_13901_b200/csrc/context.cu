@@ -615,6 +615,19 @@ int spd_allgather(spd_context* ctx, void* dev_buf, int64_t bytes_per_rank) {
   });
 }
 
+int spd_context_abort(spd_context* ctx) {
+  return guarded([&] {
+    checked(ctx);
+    // ncclCommAbort ends this rank's pending collectives (their kernels stop
+    // waiting for peers), so a thread blocked on them returns with an error
+    if (ctx->comm) {
+      ncclComm_t c = ctx->comm;
+      ctx->comm = nullptr;
+      ncclCommAbort(c);
+    }
+  });
+}
+
 int spd_context_rank(const spd_context* ctx, int* rank, int* world) {
   return guarded([&] {
     if (!ctx) throw ValidationError("null spd_context");

@@ -37,3 +37,13 @@ def test_two_gpu_check():
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and "MGPU_RESULT PASS" in r.stdout, r.stdout[-4000:] + r.stderr[-3000:]
     assert "blocks" in r.stdout and "MISMATCH" not in r.stdout
+
+
+@pytest.mark.skipif(_gpus() < 2, reason="needs two GPUs")
+def test_abort_unblocks_a_waiting_rank():
+    """spd_context_abort: a rank waiting in the boundary all-gather for a
+    peer that never joins returns an error once its communicator is aborted
+    (what execute_gpu does for the other GPUs when one of them fails)."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "abort_check.py")],
+                       capture_output=True, text=True, timeout=180)
+    assert "ABORT_RESULT PASS" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
