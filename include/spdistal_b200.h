@@ -107,8 +107,9 @@ int spd_context_synchronize(spd_context* ctx);
  * calls check their arguments before the first collective they enqueue, and
  * spd_tensor_place broadcasts the root's input status first, so argument
  * errors fail on every rank together; a runtime failure on one rank after
- * the others entered a collective leaves them waiting -- destroy the context
- * on every rank (ncclCommDestroy) to recover. */
+ * the others entered a collective leaves them waiting -- spd_context_abort
+ * on the waiting ranks ends it (their calls return an error), then destroy
+ * the contexts. */
 int spd_nccl_unique_id(void* out128);
 int spd_context_init_comm(spd_context* ctx, const void* unique_id128, int rank, int world);
 int spd_context_rank(const spd_context* ctx, int* rank, int* world);
