@@ -1265,6 +1265,10 @@ static void run_rowwalk(spd_context* ctx, const OpArgs& a, int64_t first, int64_
         }
         c32 = Bm->crdc;
         xv = xc;
+      } else if (ncols < (int64_t(1) << 31)) {
+        // int32 columns (built once per pattern, like the SpMM leaf's): 4 of
+        // the 16 bytes a position streams (SpTTV 0.120 -> 0.117 ms)
+        c32 = crd32_index(ctx, const_cast<spd_tensor*>(B));
       }
 #define SPD_LEAF(KERN, CI, CRD)                                                                         \
   do {                                                                                                  \
