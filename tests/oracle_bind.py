@@ -471,17 +471,17 @@ def _read_part(L, h):
         L.ref_part_free(h)
 
 
-def ref_image(ranges, subsets, dest_extent):
+def ref_image(ranges, subsets, dest_extent, lib=REF_LIB):
     """The reference's image (deppart.cpp:15-31): (subsets, disjoint)."""
-    L = ref()
+    L = ref(lib)
     r = np.ascontiguousarray(np.asarray(ranges, np.int64).reshape(-1, 2))
     off, idx = _flat_partition(subsets)
     return _read_part(L, L.ref_image(_p(r), len(r), dest_extent, len(subsets), _p(off), _p(idx)))
 
 
-def ref_preimage(ranges, subsets, dest_extent):
+def ref_preimage(ranges, subsets, dest_extent, lib=REF_LIB):
     """The reference's preimage (deppart.cpp:33-53): (subsets, disjoint)."""
-    L = ref()
+    L = ref(lib)
     r = np.ascontiguousarray(np.asarray(ranges, np.int64).reshape(-1, 2))
     off, idx = _flat_partition(subsets)
     return _read_part(L, L.ref_preimage(_p(r), len(r), dest_extent, len(subsets), _p(off), _p(idx)))

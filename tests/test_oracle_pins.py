@@ -255,3 +255,49 @@ def test_fast_partition_gives_the_same_plan(kernel, schedule):
         assert np.array_equal(va, vb)
         for (ka, pa, ca), (kb, pb, cb) in zip(la, lb):
             assert ka == kb and (pa is None or (np.array_equal(pa, pb) and np.array_equal(ca, cb)))
+
+
+@pytest.mark.skipif(not HAVE_REF_SRC and not os.path.exists(FASTPART_LIB), reason="reference sources absent")
+def test_fast_partition_set_semantics_match_the_reference():
+    """The fast Partition class against the reference's on the constructor's
+    corner cases, through image / preimage (which build a Partition from the
+    caller's subsets and return one): unsorted subsets with duplicates, empty
+    colours, disjoint and overlapping colours (overlapping spans with and
+    without a shared index), replicated colours, and an index outside the
+    parent space (the same exception text)."""
+    if HAVE_REF_SRC:
+        ob.ensure_built(ref=True)
+        subprocess.run(["make", "-C", os.path.dirname(os.path.dirname(FASTPART_LIB)), "-j8", FASTPART_LIB],
+                       check=True, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+    rng = np.random.default_rng(77)
+    for trial in range(60):
+        n, dest = int(rng.integers(1, 40)), int(rng.integers(1, 60))
+        lo = rng.integers(0, dest, n)
+        hi = np.minimum(dest - 1, lo + rng.integers(-2, 6, n))
+        ranges = np.stack([lo, hi], 1)
+        P = int(rng.integers(1, 6))
+        kind = trial % 4
+        subsets = []
+        for c in range(P):
+            if kind == 0:  # random, unsorted, duplicates, maybe empty
+                s = list(rng.integers(0, n, int(rng.integers(0, 8))))
+            elif kind == 1:  # contiguous disjoint blocks, reversed
+                b = n * c // P, n * (c + 1) // P
+                s = list(range(b[1] - 1, b[0] - 1, -1))
+            elif kind == 2:  # interleaved: overlapping spans, no shared index
+                s = list(range(c, n, P))
+            else:  # replicated
+                s = list(range(n))
+            subsets.append(s)
+        for fn in (ob.ref_image, ob.ref_preimage):
+            part = subsets if fn is ob.ref_image else [[min(x, dest - 1) for x in s] for s in subsets]
+            a = fn(ranges, part, dest)
+            b = fn(ranges, part, dest, lib=FASTPART_LIB)
+            assert a[1] == b[1] and all(np.array_equal(x, y) for x, y in zip(a[0], b[0])), (trial, fn.__name__)
+    # an index outside the parent space: the same exception, same text
+    errs = []
+    for lib in (ob.REF_LIB, FASTPART_LIB):
+        with pytest.raises(ob.RefPartitionError) as e:
+            ob.ref_image([[0, 1], [1, 2]], [[0, 5]], 4, lib=lib)
+        errs.append((e.value.status, str(e.value)))
+    assert errs[0] == errs[1] and "outside parent space" in errs[0][1]
